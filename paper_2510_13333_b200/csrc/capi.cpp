@@ -1,0 +1,704 @@
+// C-ABI for the sparse_core part of the boundary (include/nclopf_b200.h).
+// Host code: handle bookkeeping, one-time symbolic analysis (csrc/host),
+// uploads; every numeric operation is a CUDA kernel from csrc/cuda.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../include/nclopf_b200.h"
+#include "capi_internal.hpp"
+#include "cuda/dev.hpp"
+#include "host/sparse.hpp"
+
+using nclb::Error;
+
+namespace nclb {
+thread_local std::string g_err;
+cudaStream_t g_stream = nullptr;
+int g_device = -1;
+
+int set_err(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+int map_exc() {
+  try {
+    throw;
+  } catch (const Error& e) {
+    return set_err(e.code, e.msg);
+  } catch (const CudaError& e) {
+    return set_err(NCL_E_CUDA, e.msg);
+  } catch (const std::bad_alloc&) {
+    return set_err(NCL_E_NOMEM, "out of memory");
+  } catch (const std::exception& e) {
+    return set_err(NCL_E_INTERNAL, e.what());
+  }
+}
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError{std::string(what) + ": " + cudaGetErrorString(e)};
+}
+void ensure_init() {
+  if (!g_stream) {
+    int rc = ncl_init(-1);
+    if (rc != NCL_OK) throw CudaError{g_err};
+  }
+}
+void check_launch(const char* what) {
+  ck(cudaGetLastError(), what);
+}
+}  // namespace nclb
+
+using namespace nclb;
+
+#define API extern "C" __attribute__((visibility("default")))
+#define GUARD(...)    \
+  try {               \
+    __VA_ARGS__;      \
+  } catch (...) {     \
+    return map_exc(); \
+  }                   \
+  return NCL_OK;
+
+// ----------------------------------------------------------------------------
+API int ncl_init(int device) {
+  try {
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+      return set_err(NCL_E_CUDA, "ncl_init: no CUDA device (the B200 path has no CPU fallback)");
+    if (device < 0) {
+      ck(cudaGetDevice(&device), "cudaGetDevice");
+    }
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    cudaDeviceProp prop;
+    ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major < 10)
+      return set_err(NCL_E_CUDA, "ncl_init: device is not sm_100 class (built for sm_100a only)");
+    if (!g_stream) ck(cudaStreamCreateWithFlags(&g_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    g_device = device;
+  } catch (...) {
+    return map_exc();
+  }
+  return NCL_OK;
+}
+API int ncl_synchronize(void) { GUARD(ensure_init(); ck(cudaStreamSynchronize(g_stream), "sync")); }
+API const char* ncl_last_error(void) { return g_err.c_str(); }
+API void* ncl_stream(void) {
+  try {
+    ensure_init();
+  } catch (...) {
+    map_exc();
+    return nullptr;
+  }
+  return g_stream;
+}
+API int ncl_device_alloc(void** ptr, int64_t bytes) {
+  GUARD(ensure_init(); ck(cudaMalloc(ptr, std::max<int64_t>(bytes, 8)), "cudaMalloc"));
+}
+API int ncl_device_free(void* ptr) { GUARD(ck(cudaFree(ptr), "cudaFree")); }
+API int ncl_memcpy(void* dst, const void* src, int64_t bytes, int kind) {
+  GUARD({
+    ensure_init();
+    const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice : kind == 1 ? cudaMemcpyDeviceToHost
+                                                                            : cudaMemcpyDeviceToDevice;
+    if (bytes > 0) ck(cudaMemcpyAsync(dst, src, bytes, k, g_stream), "cudaMemcpyAsync");
+    ck(cudaStreamSynchronize(g_stream), "sync");
+  });
+}
+API int64_t ncl_kernel_launches(void) { return g_kernel_launches; }
+
+// ---------------------------------------------------------------------------
+// SparseSym
+// ---------------------------------------------------------------------------
+struct ncl_sym {
+  SymPattern pat;
+  DevBuf<double> vals;
+  DevBuf<int> colptr, rowind;
+  DevBuf<int> diag_pos, mv_val, mv_col;
+  DevBuf<int64_t> mv_ptr;
+  DevBuf<int> slot_ptr, slot_trip;
+  DevBuf<double> trip_vals;
+  DevBuf<double> scratch;  // 4 doubles
+  DevBuf<double> rowsum;
+  DevPattern dp;
+  uint64_t hash = 0;
+  bool dev_ready = false;  // pattern + values uploaded (lazy: host-only use needs no GPU)
+  explicit ncl_sym(int n) : pat(n) {}
+};
+
+namespace {
+uint64_t pattern_hash(const std::vector<int>& cp, const std::vector<int>& ri) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](uint64_t v) {
+    h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+  };
+  for (int v : cp) mix(static_cast<uint32_t>(v));
+  for (int v : ri) mix(static_cast<uint32_t>(v));
+  return h;
+}
+
+void require_finalized(const ncl_sym* M, const char* what) {
+  if (!M->pat.finalized()) throw Error{NCL_E_LOGIC, std::string(what) + ": matrix not finalized"};
+}
+
+// Upload pattern-level device data (first device use after finalize()).
+void upload_pattern(ncl_sym* M) {
+  if (M->dev_ready) return;
+  ensure_init();
+  const int n = M->pat.dim();
+  const auto& cp = M->pat.col_ptr();
+  const auto& ri = M->pat.row_ind();
+  const int nnz = M->pat.nnz();
+  M->colptr.upload(cp);
+  M->rowind.upload(ri);
+  M->vals.upload(M->pat.values());
+  // diagonal slots
+  std::vector<int> dpos;
+  for (int c = 0; c < n; ++c)
+    for (int p = cp[c]; p < cp[c + 1]; ++p)
+      if (ri[p] == c) dpos.push_back(p);
+  M->diag_pos.upload(dpos);
+  // symmetric SpMV gather in reference order: row i = lower-row entries
+  // (i,c), c<i ascending; then column i's entries in storage order.
+  std::vector<int64_t> ptr(n + 1, 0);
+  for (int c = 0; c < n; ++c)
+    for (int p = cp[c]; p < cp[c + 1]; ++p) {
+      const int r = ri[p];
+      if (r != c) ptr[r + 1]++;  // (r,c) contributes to row r via the lower part
+      ptr[c + 1]++;              // column c's own entries contribute to row c
+    }
+  for (int i = 0; i < n; ++i) ptr[i + 1] += ptr[i];
+  std::vector<int> mval(ptr[n]), mcol(ptr[n]);
+  {
+    std::vector<int64_t> fp(ptr.begin(), ptr.end() - 1);
+    // pass over columns ascending: for row r>c the (r,c) entry lands in row r
+    // before r's own column entries (which come at column r > c).
+    for (int c = 0; c < n; ++c) {
+      for (int p = cp[c]; p < cp[c + 1]; ++p) {
+        const int r = ri[p];
+        if (r != c) {
+          mval[fp[r]] = p;
+          mcol[fp[r]] = c;
+          fp[r]++;
+        }
+      }
+      for (int p = cp[c]; p < cp[c + 1]; ++p) {
+        const int r = ri[p];
+        mval[fp[c]] = p;
+        mcol[fp[c]] = r;  // y[c] += v x[r] (r==c for the diagonal: y[r] += v x[c])
+        fp[c]++;
+      }
+    }
+  }
+  M->mv_ptr.upload(ptr);
+  M->mv_val.upload(mval);
+  M->mv_col.upload(mcol);
+  std::vector<int> sptr, sidx;
+  M->pat.slot_trip_csr(sptr, sidx);
+  M->slot_ptr.upload(sptr);
+  M->slot_trip.upload(sidx);
+  M->scratch.alloc(8);
+  M->dp.n = n;
+  M->dp.nnz = nnz;
+  M->dp.diag_pos = M->diag_pos.p;
+  M->dp.ndiag = static_cast<int>(dpos.size());
+  M->dp.mv_ptr = M->mv_ptr.p;
+  M->dp.mv_val = M->mv_val.p;
+  M->dp.mv_col = M->mv_col.p;
+  M->dev_ready = true;
+}
+void ensure_dev(ncl_sym* M, const char* what) {
+  if (!M->pat.finalized()) throw Error{NCL_E_LOGIC, std::string(what) + ": matrix not finalized"};
+  upload_pattern(M);
+}
+}  // namespace
+
+API int ncl_sym_create(int n, ncl_sym_t* out) {
+  GUARD({
+    if (n < 0) throw Error{NCL_E_INVALID, "SparseSym: negative dimension"};
+    *out = new ncl_sym(n);
+  });
+}
+API void ncl_sym_destroy(ncl_sym_t M) { delete M; }
+API int ncl_sym_add(ncl_sym_t M, int64_t count, const int* rows, const int* cols, const double* vals) {
+  GUARD(for (int64_t k = 0; k < count; ++k) M->pat.add(rows[k], cols[k], vals[k]));
+}
+API int ncl_sym_finalize(ncl_sym_t M) {
+  GUARD({
+    M->pat.finalize();
+    M->hash = pattern_hash(M->pat.col_ptr(), M->pat.row_ind());
+  });
+}
+API int ncl_sym_begin_refill(ncl_sym_t M) { GUARD(M->pat.begin_refill()); }
+API int ncl_sym_refill(ncl_sym_t M) {
+  GUARD({
+    if (!M->pat.finalized()) throw Error{NCL_E_LOGIC, "SparseSym::refill: not finalized"};
+    ensure_dev(M, "SparseSym::refill");
+    M->trip_vals.upload(M->pat.trip_vals());
+    dev_gather_sum(M->pat.nnz(), M->slot_ptr.p, M->slot_trip.p, M->trip_vals.p, M->vals.p, g_stream);
+    check_launch("refill");
+  });
+}
+API int ncl_sym_refill_values(ncl_sym_t M, const double* tv, int where) {
+  GUARD({
+    if (!M->pat.finalized()) throw Error{NCL_E_LOGIC, "SparseSym::refill: not finalized"};
+    ensure_dev(M, "SparseSym::refill");
+    const int64_t nt = M->pat.num_trips();
+    const double* src = tv;
+    if (where == NCL_HOST) {
+      M->trip_vals.alloc(nt);
+      ck(cudaMemcpyAsync(M->trip_vals.p, tv, nt * sizeof(double), cudaMemcpyHostToDevice, g_stream), "H2D");
+      src = M->trip_vals.p;
+    }
+    dev_gather_sum(M->pat.nnz(), M->slot_ptr.p, M->slot_trip.p, src, M->vals.p, g_stream);
+    check_launch("refill_values");
+    if (where == NCL_HOST) ck(cudaStreamSynchronize(g_stream), "sync");
+  });
+}
+API int ncl_sym_dim(ncl_sym_t M) { return M->pat.dim(); }
+API int ncl_sym_nnz(ncl_sym_t M) { return M->pat.nnz(); }
+API int64_t ncl_sym_num_triplets(ncl_sym_t M) { return M->pat.num_trips(); }
+API int ncl_sym_finalized(ncl_sym_t M) { return M->pat.finalized() ? 1 : 0; }
+API int ncl_sym_get_csc(ncl_sym_t M, int* colptr, int* rowind, double* vals) {
+  GUARD({
+    const auto& cp = M->pat.col_ptr();
+    const auto& ri = M->pat.row_ind();
+    if (colptr && !cp.empty()) std::memcpy(colptr, cp.data(), cp.size() * sizeof(int));
+    if (rowind && !ri.empty()) std::memcpy(rowind, ri.data(), ri.size() * sizeof(int));
+    if (vals && M->pat.nnz() > 0 && !M->dev_ready) {
+      std::memcpy(vals, M->pat.values().data(), M->pat.nnz() * sizeof(double));
+    } else if (vals && M->pat.nnz() > 0) {
+      require_finalized(M, "SparseSym::values");
+      ck(cudaMemcpyAsync(vals, M->vals.p, M->pat.nnz() * sizeof(double), cudaMemcpyDeviceToHost, g_stream), "D2H");
+      ck(cudaStreamSynchronize(g_stream), "sync");
+    }
+  });
+}
+API int ncl_sym_set_values(ncl_sym_t M, const double* v, int where) {
+  GUARD({
+    ensure_dev(M, "SparseSym::set_values");
+    const int64_t nz = M->pat.nnz();
+    ck(cudaMemcpyAsync(M->vals.p, v, nz * sizeof(double),
+                       where == NCL_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, g_stream),
+       "set_values");
+    if (where == NCL_HOST) ck(cudaStreamSynchronize(g_stream), "sync");
+  });
+}
+API double* ncl_sym_device_values(ncl_sym_t M) {
+  try {
+    ensure_dev(M, "SparseSym::device_values");
+  } catch (...) {
+    map_exc();
+    return nullptr;
+  }
+  return M->vals.p;
+}
+
+static int scalar_op(ncl_sym_t M, double* out, int which) {
+  GUARD({
+    ensure_dev(M, "SparseSym");
+    double* d = M->scratch.p;
+    if (which == 0) dev_max_abs_diag(M->dp, M->vals.p, d, g_stream);
+    else if (which == 1) dev_rowsum_max(M->dp, M->vals.p, d, g_stream);
+    else dev_frob_sq(M->dp, M->colptr.p, M->rowind.p, M->vals.p, d, g_stream);
+    check_launch("norm");
+    double h = 0;
+    ck(cudaMemcpyAsync(&h, d, sizeof(double), cudaMemcpyDeviceToHost, g_stream), "D2H");
+    ck(cudaStreamSynchronize(g_stream), "sync");
+    *out = which == 2 ? std::sqrt(h) : h;
+  });
+}
+API int ncl_sym_max_abs_diag(ncl_sym_t M, double* out) { return scalar_op(M, out, 0); }
+API int ncl_sym_norm_inf(ncl_sym_t M, double* out) { return scalar_op(M, out, 1); }
+API int ncl_sym_frobenius_norm(ncl_sym_t M, double* out) { return scalar_op(M, out, 2); }
+
+API int ncl_sym_multiply(ncl_sym_t M, const double* x, double* y, int where) {
+  GUARD({
+    ensure_dev(M, "SparseSym::multiply");
+    const int n = M->pat.dim();
+    if (where == NCL_DEVICE) {
+      dev_spmv(M->dp, M->vals.p, x, y, g_stream);
+      check_launch("spmv");
+      return NCL_OK;
+    }
+    DevBuf<double> dx, dy;
+    dx.alloc(n);
+    dy.alloc(n);
+    ck(cudaMemcpyAsync(dx.p, x, n * sizeof(double), cudaMemcpyHostToDevice, g_stream), "H2D");
+    dev_spmv(M->dp, M->vals.p, dx.p, dy.p, g_stream);
+    check_launch("spmv");
+    ck(cudaMemcpyAsync(y, dy.p, n * sizeof(double), cudaMemcpyDeviceToHost, g_stream), "D2H");
+    ck(cudaStreamSynchronize(g_stream), "sync");
+  });
+}
+API int ncl_sym_same_pattern(ncl_sym_t A, ncl_sym_t B) {
+  return A->pat.dim() == B->pat.dim() && A->pat.col_ptr() == B->pat.col_ptr() && A->pat.row_ind() == B->pat.row_ind();
+}
+API int ncl_sym_write_matrix_market(ncl_sym_t M, char* buf, int64_t cap, int64_t* len) {
+  GUARD({
+    const int n = M->pat.dim();
+    std::vector<double> v(M->pat.values());
+    if (M->dev_ready && !v.empty()) {
+      ck(cudaMemcpyAsync(v.data(), M->vals.p, v.size() * sizeof(double), cudaMemcpyDeviceToHost, g_stream), "D2H");
+      ck(cudaStreamSynchronize(g_stream), "sync");
+    }
+    std::ostringstream os;
+    os << "%%MatrixMarket matrix coordinate real symmetric\n";
+    os << n << " " << n << " " << M->pat.nnz() << "\n";
+    char line[64];
+    const auto& cp = M->pat.col_ptr();
+    const auto& ri = M->pat.row_ind();
+    for (int c = 0; c < n && M->pat.finalized(); ++c)
+      for (int p = cp[c]; p < cp[c + 1]; ++p) {
+        std::snprintf(line, sizeof(line), "%d %d %.17g\n", ri[p] + 1, c + 1, v[p]);
+        os << line;
+      }
+    const std::string s = os.str();
+    *len = static_cast<int64_t>(s.size());
+    if (buf && cap > 0) std::memcpy(buf, s.data(), std::min<int64_t>(cap, *len));
+  });
+}
+
+// ---------------------------------------------------------------------------
+// Symbolic analysis
+// ---------------------------------------------------------------------------
+struct ncl_symb {
+  SymbolicCore core;
+  Supernodal Z;
+  uint64_t hash = 0;
+  int nnz = 0;
+  DevSymb d;
+  DevBuf<int> perm, sn_first, sn_parent, rows, upd, cptr, child, order, asrc, aoff, flags, tickets;
+  DevBuf<int64_t> sn_rptr, sn_loff, uptr, aptr;
+  bool dev_ready = false;
+};
+
+namespace {
+void upload_symb(ncl_symb* S) {
+  if (S->dev_ready) return;
+  ensure_init();
+  const Supernodal& Z = S->Z;
+  S->perm.upload(S->core.perm);
+  S->sn_first.upload(Z.sn_first);
+  S->sn_parent.upload(Z.sn_parent);
+  S->rows.upload(Z.rows);
+  S->upd.upload(Z.upd);
+  S->cptr.upload(Z.cptr);
+  S->child.upload(Z.child);
+  S->order.upload(Z.order);
+  S->sn_rptr.upload(Z.sn_rptr);
+  S->sn_loff.upload(Z.sn_loff);
+  S->uptr.upload(Z.uptr);
+  // A entries grouped by target supernode, sorted by panel offset
+  const int nsn = Z.nsn;
+  std::vector<int64_t> aptr(nsn + 1, 0);
+  std::vector<int> asn(Z.amap.size());
+  for (size_t e = 0; e < Z.amap.size(); ++e) {
+    const int64_t off = Z.amap[e];
+    const int s = static_cast<int>(std::upper_bound(Z.sn_loff.begin(), Z.sn_loff.end(), off) - Z.sn_loff.begin()) - 1;
+    asn[e] = s;
+    aptr[s + 1]++;
+  }
+  for (int s = 0; s < nsn; ++s) aptr[s + 1] += aptr[s];
+  std::vector<int> asrc(Z.amap.size()), aoff(Z.amap.size());
+  {
+    std::vector<int64_t> fp(aptr.begin(), aptr.end() - 1);
+    for (size_t e = 0; e < Z.amap.size(); ++e) {
+      const int s = asn[e];
+      const int64_t q = fp[s]++;
+      asrc[q] = static_cast<int>(e);
+      aoff[q] = static_cast<int>(Z.amap[e] - Z.sn_loff[s]);
+    }
+  }
+  S->aptr.upload(aptr);
+  S->asrc.upload(asrc);
+  S->aoff.upload(aoff);
+  S->flags.alloc(3 * std::max(1, nsn));
+  ck(cudaMemsetAsync(S->flags.p, 0, 3 * std::max(1, nsn) * sizeof(int), g_stream), "memset");
+  S->tickets.alloc(4);
+  DevSymb& d = S->d;
+  d.n = S->core.n;
+  d.nsn = nsn;
+  int nleaf = 0;
+  for (int s = 0; s < nsn; ++s)
+    if (Z.height[s] == 0) nleaf++;
+  d.nleaf = nleaf;
+  d.nnz = S->nnz;
+  d.l_storage = Z.l_storage;
+  d.perm = S->perm.p;
+  d.sn_first = S->sn_first.p;
+  d.sn_parent = S->sn_parent.p;
+  d.sn_rptr = S->sn_rptr.p;
+  d.rows = S->rows.p;
+  d.sn_loff = S->sn_loff.p;
+  d.uptr = S->uptr.p;
+  d.upd = S->upd.p;
+  d.cptr = S->cptr.p;
+  d.child = S->child.p;
+  d.order = S->order.p;
+  d.aptr = S->aptr.p;
+  d.asrc = S->asrc.p;
+  d.aoff = S->aoff.p;
+  d.flags = S->flags.p;
+  d.tickets = S->tickets.p;
+  d.epoch = 0;
+  if (Z.l_storage >= (int64_t(1) << 31) || static_cast<int64_t>(Z.amap.size()) >= (int64_t(1) << 31))
+    throw Error{NCL_E_INVALID, "analyze: factor exceeds int32 panel addressing"};
+  S->dev_ready = true;
+}
+}  // namespace
+
+API int ncl_symbolic_order(ncl_sym_t M, int* perm) {
+  GUARD({
+    if (!M->pat.finalized()) throw Error{NCL_E_LOGIC, "symbolic_order: pattern not finalized"};
+    auto p = symbolic_order(M->pat.dim(), M->pat.col_ptr(), M->pat.row_ind());
+    if (!p.empty()) std::memcpy(perm, p.data(), p.size() * sizeof(int));
+  });
+}
+
+ncl_symb* analyze_impl(ncl_sym_t M, const int* perm) {
+  if (!M->pat.finalized()) throw Error{NCL_E_LOGIC, "analyze: matrix not finalized"};
+  const int n = M->pat.dim();
+  std::vector<int> p = perm ? std::vector<int>(perm, perm + n)
+                            : symbolic_order(n, M->pat.col_ptr(), M->pat.row_ind());
+  auto S = std::make_unique<ncl_symb>();
+  S->core = analyze_core(n, M->pat.col_ptr(), M->pat.row_ind(), std::move(p));
+  S->Z = build_supernodes(S->core, M->pat.col_ptr(), M->pat.row_ind());
+  S->hash = M->hash;
+  S->nnz = M->pat.nnz();
+  return S.release();
+}
+
+API int ncl_analyze(ncl_sym_t M, const int* perm, ncl_symb_t* out) { GUARD(*out = analyze_impl(M, perm)); }
+API void ncl_symb_destroy(ncl_symb_t S) { delete S; }
+API int ncl_symb_info_get(ncl_symb_t S, ncl_symb_info* info) {
+  GUARD({
+    info->n = S->core.n;
+    info->l_nnz = S->core.l_nnz;
+    info->nsupernodes = S->Z.nsn;
+    info->max_height = S->Z.max_height;
+    info->max_width = S->Z.max_w;
+    info->max_rows = S->Z.max_nr;
+    info->l_storage = S->Z.l_storage;
+    info->flops = S->Z.flops;
+  });
+}
+API int ncl_symb_get(ncl_symb_t S, int* perm, int* iperm, int* parent, int* up_colptr, int* up_rowind,
+                     int* entry_map, int* l_colcount) {
+  GUARD({
+    auto cp = [](int* dst, const std::vector<int>& v) {
+      if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(int));
+    };
+    cp(perm, S->core.perm);
+    cp(iperm, S->core.iperm);
+    cp(parent, S->core.parent);
+    cp(up_colptr, S->core.up_colptr);
+    cp(up_rowind, S->core.up_rowind);
+    cp(entry_map, S->core.entry_map);
+    cp(l_colcount, S->core.l_colcount);
+  });
+}
+
+// ---------------------------------------------------------------------------
+// Numeric factorization
+// ---------------------------------------------------------------------------
+struct ncl_fact {
+  ncl_symb* S = nullptr;
+  std::unique_ptr<ncl_symb> owned;
+  DevFactor F;
+  DevBuf<double> L, D, xp, scal, work1, work2, work3;
+  DevBuf<int> istat;
+};
+
+namespace {
+void check_match(ncl_sym_t M, ncl_symb* S) {
+  if (M->pat.dim() != S->core.n || M->pat.nnz() != S->nnz)
+    throw Error{NCL_E_INVALID, "factorize: matrix does not match symbolic analysis"};
+  if (M->hash != S->hash) throw Error{NCL_E_INVALID, "factorize: matrix pattern differs from the analyzed pattern"};
+}
+void alloc_fact(ncl_fact* f) {
+  const int n = f->S->core.n;
+  f->L.alloc(std::max<int64_t>(1, f->S->Z.l_storage));
+  f->D.alloc(std::max(1, n));
+  f->xp.alloc(std::max(1, n));
+  f->scal.alloc(8);
+  f->istat.alloc(8);
+  f->work1.alloc(std::max(1, n));
+  f->work2.alloc(std::max(1, n));
+  f->work3.alloc(std::max(1, n));
+  f->F.L = f->L.p;
+  f->F.D = f->D.p;
+  f->F.xp = f->xp.p;
+  f->F.scal = f->scal.p;
+  f->F.istat = f->istat.p;
+}
+void run_factor(ncl_fact* f, ncl_sym_t M, double tol) {
+  dev_factor(f->S->d, M->dp, f->F, M->vals.p, tol, g_stream);
+  dev_inertia(f->S->d, f->F, g_stream);
+  check_launch("factorize");
+}
+}  // namespace
+
+API int ncl_factorize(ncl_sym_t M, ncl_symb_t S, double pivot_tol, ncl_fact_t* out) {
+  GUARD({
+    if (!M->pat.finalized()) throw Error{NCL_E_LOGIC, "factorize: matrix not finalized"};
+    auto f = std::make_unique<ncl_fact>();
+    if (S) {
+      f->S = S;
+    } else {
+      f->owned.reset(analyze_impl(M, nullptr));
+      f->S = f->owned.get();
+    }
+    check_match(M, f->S);
+    ensure_dev(M, "factorize");
+    upload_symb(f->S);
+    alloc_fact(f.get());
+    run_factor(f.get(), M, pivot_tol);
+    ck(cudaStreamSynchronize(g_stream), "factorize");
+    *out = f.release();
+  });
+}
+API int ncl_refactorize(ncl_fact_t F, ncl_sym_t M, double pivot_tol) {
+  GUARD({
+    check_match(M, F->S);
+    ensure_dev(M, "factorize");
+    run_factor(F, M, pivot_tol);
+  });
+}
+API void ncl_fact_destroy(ncl_fact_t F) { delete F; }
+API int ncl_fact_status(ncl_fact_t F, int* status, int* zpi, int* np, int* nn, int* nz) {
+  GUARD({
+    int h[4];
+    ck(cudaMemcpyAsync(h, F->istat.p, sizeof(h), cudaMemcpyDeviceToHost, g_stream), "D2H");
+    ck(cudaStreamSynchronize(g_stream), "sync");
+    const int n = F->S->core.n;
+    if (h[0] < n) {
+      *status = 1;
+      *zpi = F->S->core.perm[h[0]];
+      *np = *nn = *nz = 0;
+    } else {
+      *status = 0;
+      *zpi = -1;
+      *np = h[1];
+      *nn = h[2];
+      *nz = h[3];
+    }
+  });
+}
+API int ncl_fact_diagonal(ncl_fact_t F, double* d) {
+  GUARD({
+    const int n = F->S->core.n;
+    if (n > 0) ck(cudaMemcpyAsync(d, F->D.p, n * sizeof(double), cudaMemcpyDeviceToHost, g_stream), "D2H");
+    ck(cudaStreamSynchronize(g_stream), "sync");
+  });
+}
+namespace {
+bool fact_ok_sync(ncl_fact_t F) {
+  int h = 0;
+  ck(cudaMemcpyAsync(&h, F->istat.p, sizeof(int), cudaMemcpyDeviceToHost, g_stream), "D2H");
+  ck(cudaStreamSynchronize(g_stream), "sync");
+  return h >= F->S->core.n;
+}
+}  // namespace
+API int ncl_fact_solve(ncl_fact_t F, double* x, int where) {
+  GUARD({
+    const int n = F->S->core.n;
+    if (where == NCL_DEVICE) {
+      dev_solve(F->S->d, F->F, x, x, g_stream);
+      check_launch("solve");
+      return NCL_OK;
+    }
+    ck(cudaMemcpyAsync(F->work1.p, x, n * sizeof(double), cudaMemcpyHostToDevice, g_stream), "H2D");
+    dev_solve(F->S->d, F->F, F->work1.p, F->work1.p, g_stream);
+    check_launch("solve");
+    ck(cudaMemcpyAsync(x, F->work1.p, n * sizeof(double), cudaMemcpyDeviceToHost, g_stream), "D2H");
+    ck(cudaStreamSynchronize(g_stream), "sync");
+  });
+}
+
+// solve_refined (sparse_sym.cpp:371-401): x = F\b; up to max_sweeps
+// refinement sweeps while ||b - Mx||_inf / max(1,||b||_inf) > target.
+// The residual norm decision needs one scalar D2H per sweep.
+int solve_refined_dev(ncl_fact_t F, ncl_sym_t M, const double* db, double* dx, double target, int max_sweeps,
+                      double* residual, int* sweeps, int* converged) {
+  const int n = F->S->core.n;
+  double* r = F->work2.p;
+  double* sc = F->scal.p + 4;  // [4]=bnorm [5]=rnorm
+  dev_solve(F->S->d, F->F, db, dx, g_stream);
+  ck(cudaMemsetAsync(sc, 0, sizeof(double), g_stream), "memset");
+  dev_absmax(db, n, sc, g_stream);
+  double bnorm = 0;
+  ck(cudaMemcpyAsync(&bnorm, sc, sizeof(double), cudaMemcpyDeviceToHost, g_stream), "D2H");
+  ck(cudaStreamSynchronize(g_stream), "sync");
+  const double scale = std::max(1.0, bnorm);
+  *converged = 0;
+  *residual = std::numeric_limits<double>::infinity();
+  for (int sweep = 0; sweep <= max_sweeps; ++sweep) {
+    dev_residual(M->dp, M->vals.p, db, dx, r, sc + 1, g_stream);
+    double rn = 0;
+    ck(cudaMemcpyAsync(&rn, sc + 1, sizeof(double), cudaMemcpyDeviceToHost, g_stream), "D2H");
+    ck(cudaStreamSynchronize(g_stream), "sync");
+    *residual = rn / scale;
+    *sweeps = sweep;
+    if (*residual <= target) {
+      *converged = 1;
+      return NCL_OK;
+    }
+    if (sweep == max_sweeps) break;
+    dev_solve(F->S->d, F->F, r, r, g_stream);
+    dev_axpy_inplace(dx, r, n, g_stream);
+  }
+  check_launch("solve_refined");
+  return NCL_OK;
+}
+
+API int ncl_solve_refined(ncl_fact_t F, ncl_sym_t M, const double* b, double target, int max_sweeps, double* x,
+                          int where, double* residual, int* sweeps, int* converged) {
+  GUARD({
+    if (!fact_ok_sync(F)) throw Error{NCL_E_LOGIC, "solve_refined: factorization not usable"};
+    check_match(M, F->S);
+    ensure_dev(M, "solve_refined");
+    const int n = F->S->core.n;
+    if (where == NCL_DEVICE) {
+      solve_refined_dev(F, M, b, x, target, max_sweeps, residual, sweeps, converged);
+      return NCL_OK;
+    }
+    ck(cudaMemcpyAsync(F->work3.p, b, n * sizeof(double), cudaMemcpyHostToDevice, g_stream), "H2D");
+    solve_refined_dev(F, M, F->work3.p, F->work1.p, target, max_sweeps, residual, sweeps, converged);
+    ck(cudaMemcpyAsync(x, F->work1.p, n * sizeof(double), cudaMemcpyDeviceToHost, g_stream), "D2H");
+    ck(cudaStreamSynchronize(g_stream), "sync");
+  });
+}
+
+API int ncl_fact_get_L(ncl_fact_t F, int* lp, int* li, double* lx) {
+  GUARD({
+    const Supernodal& Z = F->S->Z;
+    const int n = F->S->core.n;
+    std::vector<double> Lh(Z.l_storage);
+    if (Z.l_storage > 0)
+      ck(cudaMemcpyAsync(Lh.data(), F->L.p, Z.l_storage * sizeof(double), cudaMemcpyDeviceToHost, g_stream), "D2H");
+    ck(cudaStreamSynchronize(g_stream), "sync");
+    int64_t pos = 0;
+    if (lp) lp[0] = 0;
+    for (int s = 0; s < Z.nsn; ++s) {
+      const int f = Z.sn_first[s], w = Z.sn_first[s + 1] - f;
+      const int64_t rb = Z.sn_rptr[s];
+      const int nr = static_cast<int>(Z.sn_rptr[s + 1] - rb);
+      for (int c = 0; c < w; ++c) {
+        for (int i = c + 1; i < nr; ++i) {
+          if (li) li[pos] = Z.rows[rb + i];
+          if (lx) lx[pos] = Lh[Z.sn_loff[s] + static_cast<int64_t>(c) * nr + i];
+          ++pos;
+        }
+        if (lp) lp[f + c + 1] = static_cast<int>(pos);
+      }
+    }
+    (void)n;
+  });
+}

@@ -1,0 +1,64 @@
+// Internal helpers shared by the C-ABI translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <limits>
+#include <string>
+#include <vector>
+
+namespace nclb {
+
+struct CudaError {
+  std::string msg;
+};
+
+extern cudaStream_t g_stream;
+extern thread_local std::string g_err;
+void ck(cudaError_t e, const char* what);
+void ensure_init();
+void check_launch(const char* what);
+int set_err(int code, const std::string& msg);
+int map_exc();
+
+// Owning device buffer (cudaMalloc/cudaFree), sized in elements.
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  int64_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) {
+    o.p = nullptr;
+    o.n = 0;
+  }
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(int64_t count) {
+    if (count <= n && p) return;
+    release();
+    const int64_t bytes = std::max<int64_t>(count, 1) * static_cast<int64_t>(sizeof(T));
+    ck(cudaMalloc(reinterpret_cast<void**>(&p), bytes), "cudaMalloc");
+    n = std::max<int64_t>(count, 1);
+  }
+  void upload(const std::vector<T>& v) {
+    alloc(static_cast<int64_t>(v.size()));
+    if (!v.empty())
+      ck(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, g_stream), "upload");
+    ck(cudaStreamSynchronize(g_stream), "upload sync");
+  }
+  void download(std::vector<T>& v, int64_t count) const {
+    v.resize(count);
+    if (count > 0) ck(cudaMemcpyAsync(v.data(), p, count * sizeof(T), cudaMemcpyDeviceToHost, g_stream), "download");
+    ck(cudaStreamSynchronize(g_stream), "download sync");
+  }
+};
+
+}  // namespace nclb

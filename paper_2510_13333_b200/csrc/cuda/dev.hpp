@@ -1,0 +1,81 @@
+// Device-side data structures and launch entry points for the sparse
+// LDLᵀ path (K3 factor, K4 solve, K5 SpMV/refinement, K6 norms).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace nclb {
+
+// Number of library kernel launches issued so far (evidence for the bench's
+// gpu_launches key). Incremented by every dev_* wrapper.
+extern int64_t g_kernel_launches;
+
+// Symbolic schedule resident in HBM (built once from host Supernodal).
+struct DevSymb {
+  int n = 0, nsn = 0, nleaf = 0;
+  int64_t nnz = 0, l_storage = 0;
+  int* perm = nullptr;       // [n]
+  int* sn_first = nullptr;   // [nsn+1]
+  int* sn_parent = nullptr;  // [nsn]
+  int64_t* sn_rptr = nullptr;
+  int* rows = nullptr;
+  int64_t* sn_loff = nullptr;
+  int64_t* uptr = nullptr;
+  int* upd = nullptr;   // (d, p0, p1) triples
+  int* cptr = nullptr;  // children CSR
+  int* child = nullptr;
+  int* order = nullptr;  // ticket order, leaves first
+  int64_t* aptr = nullptr;   // [nsn+1] A entries per supernode
+  int* asrc = nullptr;       // source value slot
+  int* aoff = nullptr;       // offset inside panel
+  // scheduling state
+  int* flags = nullptr;     // [3*nsn] epoch flags: factor, fwd, bwd
+  int* tickets = nullptr;   // [4]
+  int epoch = 0;
+};
+
+// Pattern-level device data of one SparseSym (independent of the ordering).
+struct DevPattern {
+  int n = 0;
+  int64_t nnz = 0;
+  int* diag_pos = nullptr;  // value slots of the stored diagonal entries
+  int ndiag = 0;
+  // bit-exact symmetric SpMV row gather in the reference multiply order
+  // (sparse_sym.cpp:105-115): row i lists (value slot, x index)
+  int64_t* mv_ptr = nullptr;  // [n+1]
+  int* mv_val = nullptr;
+  int* mv_col = nullptr;
+};
+
+struct DevFactor {
+  double* L = nullptr;  // panels
+  double* D = nullptr;  // [n] by pivot position
+  double* xp = nullptr;  // [n] permuted work vector
+  double* scal = nullptr;  // [4]: thresh, maxdiag, scratch
+  int* istat = nullptr;    // [4]: zp position, npos, nneg, nzero
+};
+
+// all launches are asynchronous on `st`
+void dev_factor(const DevSymb& S, const DevPattern& P, DevFactor& F, const double* kvals, double pivot_tol,
+                cudaStream_t st);
+void dev_inertia(const DevSymb& S, DevFactor& F, cudaStream_t st);
+// x := M^{-1} b (in place allowed: x may alias b)
+void dev_solve(const DevSymb& S, DevFactor& F, const double* b, double* x, cudaStream_t st);
+void dev_spmv(const DevPattern& P, const double* kvals, const double* x, double* y, cudaStream_t st);
+// r = b - M x ; *out_max = max|r| (zeroed here), fused
+void dev_residual(const DevPattern& P, const double* kvals, const double* b, const double* x, double* r,
+                  double* out_max, cudaStream_t st);
+void dev_absmax(const double* v, int64_t n, double* out, cudaStream_t st);  // out must be zeroed
+void dev_axpy_inplace(double* x, const double* d, int64_t n, cudaStream_t st);  // x += d
+void dev_max_abs_diag(const DevPattern& P, const double* kvals, double* out, cudaStream_t st);
+void dev_rowsum_max(const DevPattern& P, const double* kvals, double* out, cudaStream_t st);
+// sum over stored entries of (diag ? v^2 : 2 v^2), deterministic two-level tree
+void dev_frob_sq(const DevPattern& P, const int* colptr, const int* rowind, const double* kvals, double* out,
+                 cudaStream_t st);
+int dev_num_sms();
+void dev_gather_sum(int64_t nslots, const int* ptr, const int* idx, const double* src, double* dst,
+                    cudaStream_t st);
+
+}  // namespace nclb

@@ -1,0 +1,426 @@
+// Host symbolic layer. See sparse.hpp for the contract; every function below
+// names the reference routine whose semantics it reproduces.
+#include "sparse.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <queue>
+
+#include "../../../include/nclopf_expr_program.h"
+
+namespace nclb {
+
+static inline void fail(int code, const char* msg) { throw Error{code, msg}; }
+
+// --- SparseSym::add (sparse_sym.cpp:12-26) ---------------------------------
+void SymPattern::add(int row, int col, double value) {
+  if (row < col) fail(NCL_E_INVALID, "SparseSym::add: row < col (store lower triangle)");
+  if (col < 0 || row >= n_) fail(NCL_E_INVALID, "SparseSym::add: index out of range");
+  if (!finalized_) {
+    trows_.push_back(row);
+    tcols_.push_back(col);
+    tvals_.push_back(value);
+    return;
+  }
+  // refill mode: coordinates must replay the original assembly order
+  if (cursor_ >= static_cast<int64_t>(trows_.size()) || trows_[cursor_] != row || tcols_[cursor_] != col)
+    fail(NCL_E_LOGIC, "SparseSym::add: refill coordinates do not match original assembly");
+  tvals_[cursor_] = value;
+  ++cursor_;
+}
+
+// --- SparseSym::finalize (sparse_sym.cpp:28-56) -----------------------------
+// Stable (col,row) ordering realised as a stable counting sort on col
+// followed by a stable sort on row inside each column; identical order to the
+// reference's std::stable_sort with the same comparator.
+void SymPattern::finalize() {
+  if (finalized_) fail(NCL_E_LOGIC, "SparseSym::finalize: already finalized");
+  const int64_t nt = static_cast<int64_t>(trows_.size());
+  std::vector<int64_t> cstart(n_ + 1, 0);
+  for (int64_t k = 0; k < nt; ++k) cstart[tcols_[k] + 1]++;
+  for (int c = 0; c < n_; ++c) cstart[c + 1] += cstart[c];
+  std::vector<int> order(nt);
+  {
+    std::vector<int64_t> fillp(cstart.begin(), cstart.end() - 1);
+    for (int64_t k = 0; k < nt; ++k) order[fillp[tcols_[k]]++] = static_cast<int>(k);
+  }
+  for (int c = 0; c < n_; ++c) {
+    auto b = order.begin() + cstart[c], e = order.begin() + cstart[c + 1];
+    if (e - b > 1)
+      std::stable_sort(b, e, [&](int a, int bb) { return trows_[a] < trows_[bb]; });
+  }
+  colptr_.assign(n_ + 1, 0);
+  rowind_.clear();
+  rowind_.reserve(nt);
+  trip_slot_.assign(nt, -1);
+  int prev_row = -1, prev_col = -1;
+  for (int64_t s = 0; s < nt; ++s) {
+    const int k = order[s];
+    if (trows_[k] != prev_row || tcols_[k] != prev_col) {
+      rowind_.push_back(trows_[k]);
+      colptr_[tcols_[k] + 1]++;
+      prev_row = trows_[k];
+      prev_col = tcols_[k];
+    }
+    trip_slot_[k] = static_cast<int>(rowind_.size()) - 1;
+  }
+  for (int c = 0; c < n_; ++c) colptr_[c + 1] += colptr_[c];
+  finalized_ = true;
+  refill();
+}
+
+void SymPattern::begin_refill() {
+  if (!finalized_) fail(NCL_E_LOGIC, "SparseSym::begin_refill: not finalized");
+  cursor_ = 0;
+}
+
+// --- SparseSym::refill (sparse_sym.cpp:63-67): host copy of the merge, used
+// only to keep the reference-compatible host accessor values() coherent. The
+// hot-path refill is the GPU gather in csrc/cuda/assemble.cu.
+void SymPattern::refill() {
+  if (!finalized_) fail(NCL_E_LOGIC, "SparseSym::refill: not finalized");
+  vals_.assign(rowind_.size(), 0.0);
+  for (size_t k = 0; k < tvals_.size(); ++k) vals_[trip_slot_[k]] += tvals_[k];
+}
+
+void SymPattern::slot_trip_csr(std::vector<int>& ptr, std::vector<int>& idx) const {
+  const int nz = nnz();
+  ptr.assign(nz + 1, 0);
+  for (int s : trip_slot_) ptr[s + 1]++;
+  for (int s = 0; s < nz; ++s) ptr[s + 1] += ptr[s];
+  idx.resize(trip_slot_.size());
+  std::vector<int> fillp(ptr.begin(), ptr.end() - 1);
+  for (size_t k = 0; k < trip_slot_.size(); ++k) idx[fillp[trip_slot_[k]]++] = static_cast<int>(k);
+}
+
+// --- symbolic_order (sparse_sym.cpp:139-191) --------------------------------
+// Same rule: repeatedly eliminate the node with the lexicographically smallest
+// (current degree, original index); its neighbours become a clique. The
+// reference keeps a std::set of (degree,node); we keep a binary min-heap of
+// packed 64-bit keys with lazy invalidation (a popped key is live iff the node
+// is alive and its stored degree still equals the key's degree). Keys are
+// unique per (degree,node), so the pop sequence equals the set's begin()
+// sequence. Adjacency lists stay sorted; the clique merge is the same
+// (adj[u] \ {v}) ∪ (clique \ {u}).
+std::vector<int> symbolic_order(int n, const std::vector<int>& cp, const std::vector<int>& ri) {
+  std::vector<int> cnt(n + 1, 0);
+  for (int c = 0; c < n; ++c)
+    for (int p = cp[c]; p < cp[c + 1]; ++p) {
+      const int r = ri[p];
+      if (r != c) {
+        cnt[r]++;
+        cnt[c]++;
+      }
+    }
+  std::vector<std::vector<int>> adj(n);
+  for (int i = 0; i < n; ++i) adj[i].reserve(cnt[i]);
+  for (int c = 0; c < n; ++c)
+    for (int p = cp[c]; p < cp[c + 1]; ++p) {
+      const int r = ri[p];
+      if (r != c) {
+        adj[r].push_back(c);
+        adj[c].push_back(r);
+      }
+    }
+  for (auto& a : adj) {
+    std::sort(a.begin(), a.end());
+    a.erase(std::unique(a.begin(), a.end()), a.end());
+  }
+
+  using Key = uint64_t;
+  auto key = [](int deg, int node) { return (static_cast<Key>(deg) << 32) | static_cast<uint32_t>(node); };
+  std::vector<Key> heapv;
+  heapv.reserve(static_cast<size_t>(n) * 4);
+  for (int i = 0; i < n; ++i) heapv.push_back(key(static_cast<int>(adj[i].size()), i));
+  std::priority_queue<Key, std::vector<Key>, std::greater<Key>> heap(std::greater<Key>(), std::move(heapv));
+
+  std::vector<char> dead(n, 0);
+  std::vector<int> perm;
+  perm.reserve(n);
+  std::vector<int> clique, merged;
+  while (!heap.empty()) {
+    const Key k = heap.top();
+    heap.pop();
+    const int v = static_cast<int>(k & 0xffffffffu);
+    const int deg = static_cast<int>(k >> 32);
+    if (dead[v] || deg != static_cast<int>(adj[v].size())) continue;
+    perm.push_back(v);
+    dead[v] = 1;
+    clique.swap(adj[v]);
+    for (int u : clique) {
+      std::vector<int>& au = adj[u];
+      const int old = static_cast<int>(au.size());
+      merged.clear();
+      merged.reserve(au.size() + clique.size());
+      size_t i = 0, j = 0;
+      const size_t na = au.size(), nc = clique.size();
+      while (i < na || j < nc) {
+        int x;
+        if (j >= nc || (i < na && au[i] < clique[j])) {
+          x = au[i++];
+        } else if (i >= na || clique[j] < au[i]) {
+          x = clique[j++];
+        } else {
+          x = au[i++];
+          ++j;
+        }
+        if (x != v && x != u) merged.push_back(x);
+      }
+      au.swap(merged);
+      if (static_cast<int>(au.size()) != old) heap.push(key(static_cast<int>(au.size()), u));
+    }
+    clique.clear();
+    std::vector<int>().swap(clique);
+  }
+  return perm;
+}
+
+// --- analyze(M, perm) (sparse_sym.cpp:198-260) ------------------------------
+SymbolicCore analyze_core(int n, const std::vector<int>& cp, const std::vector<int>& ri,
+                          std::vector<int> perm) {
+  if (static_cast<int>(perm.size()) != n) fail(NCL_E_INVALID, "analyze: bad permutation");
+  SymbolicCore S;
+  S.n = n;
+  S.perm = std::move(perm);
+  S.iperm.assign(n, -1);
+  for (int k = 0; k < n; ++k) {
+    if (S.perm[k] < 0 || S.perm[k] >= n || S.iperm[S.perm[k]] != -1)
+      fail(NCL_E_INVALID, "analyze: permutation is not a bijection");
+    S.iperm[S.perm[k]] = k;
+  }
+  // Permuted upper CSC: (i,j) lower -> column max(pi,pj), row min(pi,pj),
+  // columns ascending, rows ascending inside a column (keys are unique).
+  const int nnz = cp[n];
+  S.up_colptr.assign(n + 1, 0);
+  S.up_rowind.resize(nnz);
+  S.entry_map.resize(nnz);
+  for (int c = 0; c < n; ++c)
+    for (int p = cp[c]; p < cp[c + 1]; ++p) {
+      const int pi = S.iperm[ri[p]], pj = S.iperm[c];
+      S.up_colptr[std::max(pi, pj) + 1]++;
+    }
+  for (int c = 0; c < n; ++c) S.up_colptr[c + 1] += S.up_colptr[c];
+  {
+    std::vector<int> fillp(S.up_colptr.begin(), S.up_colptr.end() - 1);
+    std::vector<int> src(nnz);
+    for (int c = 0; c < n; ++c)
+      for (int p = cp[c]; p < cp[c + 1]; ++p) {
+        const int pi = S.iperm[ri[p]], pj = S.iperm[c];
+        const int col = std::max(pi, pj);
+        const int q = fillp[col]++;
+        S.up_rowind[q] = std::min(pi, pj);
+        src[q] = p;
+      }
+    std::vector<std::pair<int, int>> tmp;
+    for (int c = 0; c < n; ++c) {
+      const int b = S.up_colptr[c], e = S.up_colptr[c + 1];
+      if (e - b > 1) {
+        tmp.clear();
+        for (int q = b; q < e; ++q) tmp.emplace_back(S.up_rowind[q], src[q]);
+        std::sort(tmp.begin(), tmp.end());
+        for (int q = b; q < e; ++q) {
+          S.up_rowind[q] = tmp[q - b].first;
+          src[q] = tmp[q - b].second;
+        }
+      }
+    }
+    for (int q = 0; q < nnz; ++q) S.entry_map[src[q]] = q;
+  }
+  // Elimination tree + column counts via row subtrees (flag marking).
+  S.parent.assign(n, -1);
+  S.l_colcount.assign(n, 0);
+  std::vector<int> flag(n, -1);
+  for (int k = 0; k < n; ++k) {
+    flag[k] = k;
+    for (int p = S.up_colptr[k]; p < S.up_colptr[k + 1]; ++p) {
+      int i = S.up_rowind[p];
+      while (i < k && flag[i] != k) {
+        if (S.parent[i] == -1) S.parent[i] = k;
+        S.l_colcount[i]++;
+        flag[i] = k;
+        i = S.parent[i];
+      }
+    }
+  }
+  S.l_nnz = 0;
+  for (int c = 0; c < n; ++c) S.l_nnz += S.l_colcount[c];
+  return S;
+}
+
+// --- supernodal schedule (product-only) -------------------------------------
+Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
+                            const std::vector<int>& ri, int /*relax_small*/) {
+  const int n = S.n;
+  Supernodal Z;
+  // 1. partition: j+1 joins j's supernode iff parent[j]==j+1 and
+  //    colcount[j]==colcount[j+1]+1 (nested structure, identical rows).
+  Z.sn_first.push_back(0);
+  for (int j = 0; j + 1 < n; ++j) {
+    const bool join = S.parent[j] == j + 1 && S.l_colcount[j] == S.l_colcount[j + 1] + 1;
+    if (!join) Z.sn_first.push_back(j + 1);
+  }
+  if (n > 0) Z.sn_first.push_back(n);
+  else Z.sn_first.assign(1, 0);
+  Z.nsn = static_cast<int>(Z.sn_first.size()) - 1;
+  const int nsn = Z.nsn;
+  Z.sn_of_col.assign(n, -1);
+  for (int s = 0; s < nsn; ++s)
+    for (int j = Z.sn_first[s]; j < Z.sn_first[s + 1]; ++j) Z.sn_of_col[j] = s;
+  Z.sn_parent.assign(nsn, -1);
+  for (int s = 0; s < nsn; ++s) {
+    const int last = Z.sn_first[s + 1] - 1;
+    if (S.parent[last] >= 0) Z.sn_parent[s] = Z.sn_of_col[S.parent[last]];
+  }
+  // children CSR
+  Z.cptr.assign(nsn + 1, 0);
+  for (int s = 0; s < nsn; ++s)
+    if (Z.sn_parent[s] >= 0) Z.cptr[Z.sn_parent[s] + 1]++;
+  for (int s = 0; s < nsn; ++s) Z.cptr[s + 1] += Z.cptr[s];
+  Z.child.resize(Z.cptr[nsn]);
+  {
+    std::vector<int> fp(Z.cptr.begin(), Z.cptr.end() - 1);
+    for (int s = 0; s < nsn; ++s)
+      if (Z.sn_parent[s] >= 0) Z.child[fp[Z.sn_parent[s]]++] = s;
+  }
+  // 2. lower structure of A (permuted): column j holds rows i>j. Transpose
+  //    of the permuted upper CSC.
+  std::vector<int> lcp(n + 1, 0), lri;
+  for (int c = 0; c < n; ++c)
+    for (int p = S.up_colptr[c]; p < S.up_colptr[c + 1]; ++p)
+      if (S.up_rowind[p] < c) lcp[S.up_rowind[p] + 1]++;
+  for (int j = 0; j < n; ++j) lcp[j + 1] += lcp[j];
+  lri.resize(lcp[n]);
+  {
+    std::vector<int> fp(lcp.begin(), lcp.end() - 1);
+    for (int c = 0; c < n; ++c)
+      for (int p = S.up_colptr[c]; p < S.up_colptr[c + 1]; ++p)
+        if (S.up_rowind[p] < c) lri[fp[S.up_rowind[p]]++] = c;  // ascending c
+  }
+  // 3. row structures, children before parents (supernodes are numbered in
+  //    column order and a parent's columns follow its children's).
+  Z.sn_rptr.assign(nsn + 1, 0);
+  std::vector<std::vector<int>> R(nsn);
+  std::vector<int> mark(n, -1), buf;
+  for (int s = 0; s < nsn; ++s) {
+    const int f = Z.sn_first[s], l = Z.sn_first[s + 1];
+    buf.clear();
+    for (int j = f; j < l; ++j) {
+      for (int p = lcp[j]; p < lcp[j + 1]; ++p) {
+        const int r = lri[p];
+        if (r >= l && mark[r] != s) {
+          mark[r] = s;
+          buf.push_back(r);
+        }
+      }
+    }
+    for (int q = Z.cptr[s]; q < Z.cptr[s + 1]; ++q) {
+      const int c = Z.child[q];
+      for (int r : R[c])
+        if (r >= l && mark[r] != s) {
+          mark[r] = s;
+          buf.push_back(r);
+        }
+      // child's structure is no longer needed once merged into its parent
+    }
+    std::sort(buf.begin(), buf.end());
+    R[s].reserve(l - f + buf.size());
+    for (int j = f; j < l; ++j) R[s].push_back(j);
+    R[s].insert(R[s].end(), buf.begin(), buf.end());
+    for (int q = Z.cptr[s]; q < Z.cptr[s + 1]; ++q) {
+      // keep child rows: the update lists below need them; freed later
+    }
+  }
+  // verify against the reference column counts (fill pattern identity)
+  for (int s = 0; s < nsn; ++s) {
+    const int f = Z.sn_first[s], l = Z.sn_first[s + 1];
+    const int nr = static_cast<int>(R[s].size());
+    for (int j = f; j < l; ++j)
+      if (S.l_colcount[j] != nr - (j - f) - 1) fail(NCL_E_INTERNAL, "supernode structure disagrees with l_colcount");
+  }
+  for (int s = 0; s < nsn; ++s) Z.sn_rptr[s + 1] = Z.sn_rptr[s] + static_cast<int64_t>(R[s].size());
+  Z.rows.resize(Z.sn_rptr[nsn]);
+  for (int s = 0; s < nsn; ++s) std::copy(R[s].begin(), R[s].end(), Z.rows.begin() + Z.sn_rptr[s]);
+  Z.sn_loff.assign(nsn + 1, 0);
+  for (int s = 0; s < nsn; ++s) {
+    const int64_t w = Z.sn_first[s + 1] - Z.sn_first[s];
+    const int64_t nr = static_cast<int64_t>(R[s].size());
+    Z.sn_loff[s + 1] = Z.sn_loff[s] + w * nr;
+    Z.max_w = std::max<int>(Z.max_w, static_cast<int>(w));
+    Z.max_nr = std::max<int>(Z.max_nr, static_cast<int>(nr));
+  }
+  Z.l_storage = Z.sn_loff[nsn];
+  // 4. update lists (d ascending inside every target list)
+  Z.uptr.assign(nsn + 1, 0);
+  for (int d = 0; d < nsn; ++d) {
+    const int w = Z.sn_first[d + 1] - Z.sn_first[d];
+    const auto& Rd = R[d];
+    int prev = -1;
+    for (size_t i = w; i < Rd.size(); ++i) {
+      const int t = Z.sn_of_col[Rd[i]];
+      if (t != prev) {
+        Z.uptr[t + 1]++;
+        prev = t;
+      }
+    }
+  }
+  for (int s = 0; s < nsn; ++s) Z.uptr[s + 1] += Z.uptr[s];
+  Z.upd.resize(3 * Z.uptr[nsn]);
+  {
+    std::vector<int64_t> fp(Z.uptr.begin(), Z.uptr.end() - 1);
+    for (int d = 0; d < nsn; ++d) {
+      const int w = Z.sn_first[d + 1] - Z.sn_first[d];
+      const auto& Rd = R[d];
+      size_t i = w;
+      while (i < Rd.size()) {
+        const int t = Z.sn_of_col[Rd[i]];
+        size_t e = i;
+        while (e < Rd.size() && Z.sn_of_col[Rd[e]] == t) ++e;
+        const int64_t q = fp[t]++;
+        Z.upd[3 * q] = d;
+        Z.upd[3 * q + 1] = static_cast<int>(i);
+        Z.upd[3 * q + 2] = static_cast<int>(e);
+        i = e;
+      }
+    }
+  }
+  // 5. heights and ticket order (leaves first)
+  Z.height.assign(nsn, 0);
+  for (int s = 0; s < nsn; ++s)
+    if (Z.sn_parent[s] >= 0) Z.height[Z.sn_parent[s]] = std::max(Z.height[Z.sn_parent[s]], Z.height[s] + 1);
+  Z.max_height = 0;
+  for (int s = 0; s < nsn; ++s) Z.max_height = std::max(Z.max_height, Z.height[s]);
+  Z.order.resize(nsn);
+  {
+    std::vector<int> hc(Z.max_height + 2, 0);
+    for (int s = 0; s < nsn; ++s) hc[Z.height[s] + 1]++;
+    for (int h = 0; h <= Z.max_height; ++h) hc[h + 1] += hc[h];
+    for (int s = 0; s < nsn; ++s) Z.order[hc[Z.height[s]]++] = s;
+  }
+  // 6. A -> panel map, diagonal positions
+  const int nnz = cp[n];
+  Z.amap.resize(nnz);
+  Z.diag_pos.clear();
+  for (int c = 0; c < n; ++c)
+    for (int p = cp[c]; p < cp[c + 1]; ++p) {
+      const int r = ri[p];
+      if (r == c) Z.diag_pos.push_back(p);
+      const int pi = S.iperm[r], pj = S.iperm[c];
+      const int lo = std::min(pi, pj), hi = std::max(pi, pj);
+      const int s = Z.sn_of_col[lo];
+      const int f = Z.sn_first[s];
+      const int* rb = Z.rows.data() + Z.sn_rptr[s];
+      const int nr = static_cast<int>(Z.sn_rptr[s + 1] - Z.sn_rptr[s]);
+      const int pos = static_cast<int>(std::lower_bound(rb, rb + nr, hi) - rb);
+      Z.amap[p] = Z.sn_loff[s] + static_cast<int64_t>(lo - f) * nr + pos;
+    }
+  double fl = 0.0;
+  for (int j = 0; j < n; ++j) {
+    const double c = S.l_colcount[j];
+    fl += c * c + 2.0 * c;
+  }
+  Z.flops = fl;
+  return Z;
+}
+
+}  // namespace nclb

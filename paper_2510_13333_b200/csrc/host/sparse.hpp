@@ -1,0 +1,117 @@
+// Host-side sparse pattern container and one-time symbolic analysis.
+//
+// Clean-room re-implementation of the reference sparse_core *semantics*
+// (/root/reference/proj/include/nclopf/sparse_sym.hpp:20-88,
+//  /root/reference/proj/src/sparse_sym.cpp:12-262): the pattern, the
+// duplicate map, the ordering, the etree and the column counts must be
+// bit-identical to the reference, because the north_star requires the
+// symbolic analysis to match exactly. All numeric work on values happens on
+// the GPU (csrc/cuda); this file never touches per-iteration values except
+// for the reference-compatible host accessors.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace nclb {
+
+struct Error {
+  int code;  // NCL_E_* (include/nclopf_expr_program.h)
+  std::string msg;
+};
+
+// SparseSym pattern: lower-triangle COO -> CSC with deterministic duplicate
+// summation. Mirrors SparseSym::add/finalize/begin_refill/refill
+// (sparse_sym.cpp:12-67).
+class SymPattern {
+ public:
+  explicit SymPattern(int n) : n_(n) {}
+  int dim() const { return n_; }
+  bool finalized() const { return finalized_; }
+
+  // throws Error{NCL_E_INVALID|NCL_E_LOGIC}
+  void add(int row, int col, double value);
+  void finalize();
+  void begin_refill();
+  void refill();  // host-side merge of recorded triplets (reference refill semantics)
+
+  int nnz() const { return static_cast<int>(rowind_.size()); }
+  const std::vector<int>& col_ptr() const { return colptr_; }
+  const std::vector<int>& row_ind() const { return rowind_; }
+  const std::vector<double>& values() const { return vals_; }
+  std::vector<double>& values_mut() { return vals_; }
+  // triplet k -> value slot (the refill map, sparse_sym.cpp:41-51)
+  const std::vector<int>& trip_slot() const { return trip_slot_; }
+  int64_t num_trips() const { return static_cast<int64_t>(trows_.size()); }
+  const std::vector<int>& trip_rows() const { return trows_; }
+  const std::vector<int>& trip_cols() const { return tcols_; }
+  const std::vector<double>& trip_vals() const { return tvals_; }
+  // CSR over value slots listing triplet indices in triplet order; the GPU
+  // refill gathers with it so sums happen in the reference order (:66).
+  void slot_trip_csr(std::vector<int>& ptr, std::vector<int>& idx) const;
+  bool in_refill() const { return finalized_; }
+  int64_t refill_cursor() const { return cursor_; }
+
+ private:
+  int n_;
+  bool finalized_ = false;
+  std::vector<int> trows_, tcols_;
+  std::vector<double> tvals_;
+  std::vector<int> trip_slot_;
+  std::vector<int> colptr_, rowind_;
+  std::vector<double> vals_;
+  int64_t cursor_ = 0;
+};
+
+// Exact minimum degree, (degree, index)-lexicographic, explicit clique fill.
+// Bit-identical to symbolic_order (sparse_sym.cpp:139-191).
+std::vector<int> symbolic_order(int n, const std::vector<int>& colptr, const std::vector<int>& rowind);
+
+// Reference-compatible SymbolicFactor fields (sparse_sym.hpp:74-85).
+struct SymbolicCore {
+  int n = 0;
+  std::vector<int> perm, iperm, parent;
+  std::vector<int> up_colptr, up_rowind, entry_map;
+  std::vector<int> l_colcount;
+  int64_t l_nnz = 0;
+};
+
+// analyze(M, perm) (sparse_sym.cpp:198-260). Throws Error on a bad perm.
+SymbolicCore analyze_core(int n, const std::vector<int>& colptr, const std::vector<int>& rowind,
+                          std::vector<int> perm);
+
+// ---------------------------------------------------------------------------
+// Supernodal schedule consumed by the GPU factor/solve kernels (product-only;
+// does not alter perm/etree/fill).
+// ---------------------------------------------------------------------------
+struct Supernodal {
+  int nsn = 0;
+  std::vector<int> sn_first;   // [nsn+1] first column (permuted index) of each supernode
+  std::vector<int> sn_of_col;  // [n]
+  std::vector<int> sn_parent;  // [nsn] parent supernode or -1
+  std::vector<int64_t> sn_rptr;  // [nsn+1] offsets into rows
+  std::vector<int> rows;         // row structure R_s (permuted, ascending; starts with the s columns)
+  std::vector<int64_t> sn_loff;  // [nsn+1] offsets of dense column-major panels (nr x w)
+  int64_t l_storage = 0;
+  // update lists: for target s, entries [uptr[s], uptr[s+1]) of (d, p0, p1)
+  std::vector<int64_t> uptr;
+  std::vector<int> upd;  // triples
+  // children lists (supernode etree)
+  std::vector<int> cptr, child;
+  // ticket order (leaves first by height) and heights
+  std::vector<int> order;
+  std::vector<int> height;
+  int max_height = 0;
+  // A -> panel offsets for every entry of the source lower CSC
+  std::vector<int64_t> amap;
+  // diagonal entry positions of the source CSC (for max|diag|)
+  std::vector<int> diag_pos;
+  int max_w = 0, max_nr = 0;
+  double flops = 0.0;  // sum_j (c_j^2 + 2 c_j) over reference column counts
+};
+
+Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& colptr,
+                            const std::vector<int>& rowind, int relax_small = 0);
+
+}  // namespace nclb

@@ -1,0 +1,144 @@
+"""GPU parity of the numeric LDLᵀ / solves / SpMV against the reference
+(oracle/_ref) on identical inputs, through the C-ABI.
+
+Tolerances: D and x agree with the reference within 1e-10 relative (the
+factor sums in a different but fixed order); status, zero_pivot_index and
+inertia must be identical; SpMV, norms and refill are bit-exact."""
+import numpy as np
+import pytest
+
+from oracle.ref import RefFactorization, RefSparseSym, RefSymbolic
+from paper_2510_13333_b200 import sparse as ps
+from tests import matgen
+
+pytestmark = pytest.mark.gpu
+
+
+def both(n, r, c, v):
+    A = ps.SparseSym(n)
+    A.add_many(r, c, v)
+    A.finalize()
+    return A, RefSparseSym(n, r, c, v)
+
+
+def relerr(a, b):
+    return np.max(np.abs(a - b)) / max(1.0, np.max(np.abs(b)))
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_quasi_definite_parity(gpu, seed):
+    rng = np.random.default_rng(seed)
+    n1, n2 = int(rng.integers(3, 40)), int(rng.integers(2, 30))
+    (r, c, v), K = matgen.quasi_definite(n1, n2, 0.25, rng)
+    n = n1 + n2
+    A, B = both(n, r, c, v)
+    Sa = ps.analyze(A)
+    Fa = ps.factorize(A, Sa)
+    Fb = RefFactorization(B, RefSymbolic(B))
+    assert Fa.status == Fb.status == "ok"
+    ia = Fa.inertia
+    assert (ia.n_pos, ia.n_neg, ia.n_zero) == Fb.inertia == (n1, n2, 0)
+    assert relerr(Fa.diagonal(), Fb.diagonal()) < 1e-10
+    b = rng.standard_normal(n)
+    assert relerr(Fa.solve(b), Fb.solve(b)) < 1e-9
+    ra = ps.solve_refined(Fa, A, b)
+    xb, resb, swb, cvb = Fb.solve_refined(b)
+    assert ra.converged and cvb
+    assert relerr(ra.x, xb) < 1e-9
+    # L itself (reference CSC layout)
+    lp, li, lx = Fa.L_csc()
+    rp, ri, rx = Fb.L_csc(Sa.l_nnz)
+    np.testing.assert_array_equal(lp, rp)
+    np.testing.assert_array_equal(li, ri)
+    assert relerr(lx, rx) < 1e-9
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_kkt_like_parity_and_determinism(gpu, seed):
+    rng = np.random.default_rng(100 + seed)
+    r, c, v = matgen.kkt_like(int(rng.integers(500, 3000)), int(rng.integers(200, 1500)), rng)
+    n = int(max(r.max(), c.max()) + 1)
+    A, B = both(n, r, c, v)
+    Sa = ps.analyze(A)
+    Fa = ps.factorize(A, Sa)
+    Fb = RefFactorization(B, RefSymbolic(B))
+    assert Fa.status == Fb.status
+    ia = Fa.inertia
+    assert (ia.n_pos, ia.n_neg, ia.n_zero) == Fb.inertia
+    assert relerr(Fa.diagonal(), Fb.diagonal()) < 1e-10
+    b = rng.standard_normal(n)
+    ra = ps.solve_refined(Fa, A, b)
+    xb, *_ = Fb.solve_refined(b)
+    assert relerr(ra.x, xb) < 1e-8
+    # bitwise determinism
+    Fa2 = ps.factorize(A, Sa)
+    assert np.array_equal(Fa.diagonal(), Fa2.diagonal())
+    assert np.array_equal(Fa.solve(b), Fa2.solve(b))
+
+
+def test_spec_kats_gpu(gpu):
+    A, _ = both(3, [0, 1, 2], [0, 1, 2], [1.0, 1.0, 1.0])
+    F = ps.factorize(A)
+    assert F.ok() and F.inertia.n_pos == 3
+    np.testing.assert_array_equal(ps.solve_refined(F, A, [1, 2, 3]).x, [1, 2, 3])
+    A, _ = both(2, [0, 1], [0, 1], [2.0, -3.0])
+    F = ps.factorize(A)
+    assert (F.inertia.n_pos, F.inertia.n_neg) == (1, 1)
+    np.testing.assert_allclose(ps.solve_refined(F, A, [2, 3]).x, [1, -1])
+    A, _ = both(2, [0, 1, 1], [0, 0, 1], [0.0, 1.0, 0.0])
+    F = ps.factorize(A)
+    assert F.status == "zero_pivot" and F.zero_pivot_index == 0
+    A, _ = both(2, [0, 1], [0, 1], [1e13, 5.0])
+    F = ps.factorize(A)
+    assert F.status == "zero_pivot" and F.zero_pivot_index == 1
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_zero_pivot_first_index_matches(gpu, seed):
+    rng = np.random.default_rng(seed)
+    (r, c, v), K = matgen.quasi_definite(20, 10, 0.3, rng)
+    # make one diagonal vanish structurally after elimination: zero a whole row/col
+    z = int(rng.integers(0, 30))
+    keep = (r != z) & (c != z)
+    r, c, v = r[keep], c[keep], v[keep]
+    r = np.concatenate([r, [z]]); c = np.concatenate([c, [z]]); v = np.concatenate([v, [0.0]])
+    A, B = both(30, r, c, v)
+    Fa = ps.factorize(A)
+    Fb = RefFactorization(B)
+    assert Fa.status == Fb.status == "zero_pivot"
+    assert Fa.zero_pivot_index == Fb.zero_pivot_index == z
+
+
+def test_spmv_norms_refill_bit_exact(gpu):
+    rng = np.random.default_rng(9)
+    r, c, v = matgen.kkt_like(800, 300, rng)
+    r, c, v = matgen.shuffled_with_duplicates(r, c, v, rng, ndup=50)
+    n = 1100
+    A, B = both(n, r, c, v)
+    x = rng.standard_normal(n)
+    assert np.array_equal(A.multiply(x), B.multiply(x))
+    assert A.max_abs_diag() == B.max_abs_diag()
+    assert A.norm_inf() == B.norm_inf()
+    assert abs(A.frobenius_norm() - B.frobenius_norm()) <= 1e-12 * B.frobenius_norm()
+    # refill with new values in the original triplet order
+    v2 = rng.standard_normal(len(v))
+    A.begin_refill(); A.add_many(r, c, v2); A.refill()
+    B.begin_refill(); B.add_many(r, c, v2); B.refill()
+    assert np.array_equal(A.values(), B.csc()[2])
+    A.refill_values(v)
+    B.begin_refill(); B.add_many(r, c, v); B.refill()
+    assert np.array_equal(A.values(), B.csc()[2])
+
+
+def test_supernodal_wide_fronts(gpu):
+    """Dense-ish blocks -> wide supernodes (exercises the in-panel dense LDLᵀ)."""
+    rng = np.random.default_rng(11)
+    (r, c, v), K = matgen.quasi_definite(90, 60, 0.9, rng)
+    A, B = both(150, r, c, v)
+    Sa = ps.analyze(A)
+    assert Sa.info().max_width > 8
+    Fa = ps.factorize(A, Sa)
+    Fb = RefFactorization(B)
+    assert relerr(Fa.diagonal(), Fb.diagonal()) < 1e-10
+    b = rng.standard_normal(150)
+    assert relerr(ps.solve_refined(Fa, A, b).x, Fb.solve_refined(b)[0]) < 1e-9
