@@ -113,6 +113,94 @@ int ncl_solve_refined(ncl_fact_t F, ncl_sym_t M, const double* b, double target,
  * (lp[n+1], li[l_nnz], lx[l_nnz]) */
 int ncl_fact_get_L(ncl_fact_t F, int* lp, int* li, double* lx);
 
+/* ---- model_ad: model.hpp:29-109, model.cpp, expr.hpp:108-135 ------------- */
+typedef struct ncl_builder* ncl_builder_t; /* nclopf::ModelBuilder   (model.hpp:74-97) */
+typedef struct ncl_model* ncl_model_t;     /* nclopf::ModelFunctions (model.hpp:29-71) */
+
+int ncl_builder_create(int num_vars, ncl_builder_t* out);                  /* ModelBuilder(int) */
+void ncl_builder_destroy(ncl_builder_t B);
+int ncl_builder_num_vars(ncl_builder_t B);
+int ncl_builder_num_rows(ncl_builder_t B);
+/* add_template(ExpressionTemplate(f, num_var_slots, name)); f as a node program */
+int ncl_builder_add_template(ncl_builder_t B, int nnodes, const ncl_expr_node* nodes, int num_var_slots,
+                             const char* name, int* tmpl_id);
+int ncl_builder_add_rows(ncl_builder_t B, int count, int* first_row);       /* add_rows() */
+/* add_objective_term x count: vars[count*nv], params[count*np] (np may be 0) */
+int ncl_builder_add_objective_terms(ncl_builder_t B, int tmpl_id, int64_t count, int nv, const int* vars, int np,
+                                    const double* params);
+/* add_constraint_term x count: rows[count] */
+int ncl_builder_add_constraint_terms(ncl_builder_t B, int tmpl_id, int64_t count, const int* rows, int nv,
+                                     const int* vars, int np, const double* params);
+/* build() && : consumes the builder's content (B stays valid but empty) */
+int ncl_builder_build(ncl_builder_t B, ncl_model_t* out);
+
+void ncl_model_destroy(ncl_model_t M);
+int ncl_model_sizes(ncl_model_t M, int* num_vars, int* num_cons, int64_t* nnz_jac, int64_t* nnz_hess);
+int ncl_model_jac_coords(ncl_model_t M, int* rows, int* cols);   /* jac_coords()  */
+int ncl_model_hess_coords(ncl_model_t M, int* rows, int* cols);  /* hess_coords() */
+int ncl_model_eval_objective(ncl_model_t M, const double* w, double* out, int where);
+int ncl_model_eval_grad_objective(ncl_model_t M, const double* w, double* grad, int where);
+int ncl_model_eval_constraints(ncl_model_t M, const double* w, double* c, int where);
+int ncl_model_eval_jacobian(ncl_model_t M, const double* w, double* vals, int where);
+int ncl_model_eval_hessian_lag(ncl_model_t M, const double* w, double sigma, const double* lam, double* vals,
+                               int where);
+/* hessian_lag(): a finalized SparseSym of sigma*H_phi + sum lam_k H_k */
+int ncl_model_hessian_lag(ncl_model_t M, const double* w, double sigma, const double* lam, ncl_sym_t* out);
+int ncl_model_jac_times(ncl_model_t M, const double* jac_vals, const double* v, double* out, int where);
+int ncl_model_jac_trans_times(ncl_model_t M, const double* jac_vals, const double* y, double* out, int where);
+/* Device fast path used by the IPM: one launch evaluates value, gradient and
+ * Hessian programs of every family; gathers into obj[1], grad[n], c[m],
+ * jac[nnz_jac], hess[nnz_hess] (any may be NULL). Asynchronous. */
+int ncl_model_eval_all_device(ncl_model_t M, const double* w, double sigma, const double* lam, double* obj,
+                              double* grad, double* c, double* jac, double* hess);
+/* Pending DomainError of device-path evaluations: returns NCL_E_DOMAIN (and
+ * clears it) if any evaluation left the smooth domain. Synchronizes. */
+int ncl_model_check_domain(ncl_model_t M);
+/* fd_check(m, w, seed, tol) (model.hpp:99-109): errs[3] = grad/jac/hess */
+int ncl_fd_check(ncl_model_t M, const double* w, unsigned seed, double tol, double* errs, int* pass);
+
+/* ---- condensed Newton matrix (ipm.assemble_newton) ------ */
+/* K = H + Sigma_x + delta_w I + J^T D J over the fixed pattern
+ * hess_coords U diag U {J^T J}, assembled in a fixed triplet order (see
+ * csrc/host/kkt.hpp) so a reference SparseSym fed the same triplets
+ * (ncl_kkt_triplets) refills to bit-identical values. */
+typedef struct ncl_kkt* ncl_kkt_t;
+int ncl_kkt_create(int n, int m, int64_t nnz_hess, const int* hess_rows, const int* hess_cols, int64_t nnz_jac,
+                   const int* jac_rows, const int* jac_cols, ncl_kkt_t* out);
+int ncl_kkt_create_for_model(ncl_model_t M, ncl_kkt_t* out);
+void ncl_kkt_destroy(ncl_kkt_t K);
+ncl_sym_t ncl_kkt_matrix(ncl_kkt_t K);            /* borrowed; values live on the device */
+int64_t ncl_kkt_num_triplets(ncl_kkt_t K);
+int ncl_kkt_triplets(ncl_kkt_t K, int* rows, int* cols);
+/* all vectors on the device (where=NCL_DEVICE, async) or host (synchronous):
+ * hess[nnz_hess], jac[nnz_jac], sigma_x[n], D[m] */
+int ncl_kkt_assemble(ncl_kkt_t K, const double* hess, const double* jac, const double* sigma_x, double delta_w,
+                     const double* D, int where);
+
+/* ---- scopf_builder (Eq. 2-4) -------------------- */
+/* Host-side problem generation: a corrective AC-SCOPF with complementarity
+ * recourse in the paper's variable layout, as a neutral spec (templates +
+ * instances + bounds) that any ModelBuilder (this library's or the
+ * reference's) can consume. grid: 0 = MATPOWER case9, 1 = seeded geometric
+ * synthetic grid (nb, nl, ng, seed). K non-islanding line outages. */
+typedef struct ncl_scopf* ncl_scopf_t;
+typedef struct ncl_scopf_info {
+  int n, m, nfam, K, nb, nl, ng, ncomp;
+  int nvar_scen, ncon_scen;
+} ncl_scopf_info;
+int ncl_scopf_create(int grid, int nb, int nl, int ng, uint64_t seed, int K, ncl_scopf_t* out);
+void ncl_scopf_destroy(ncl_scopf_t S);
+int ncl_scopf_get_info(ncl_scopf_t S, ncl_scopf_info* info);
+/* family f: name (<=63 chars), node count, slots, params per instance,
+ * objective flag, instance count */
+int ncl_scopf_family_info(ncl_scopf_t S, int f, char* name, int* nnodes, int* nslots, int* np, int* objective,
+                          int64_t* ninst);
+int ncl_scopf_family_data(ncl_scopf_t S, int f, ncl_expr_node* nodes, int* rows, int* vars, double* params);
+/* variable bounds/start (n), row bounds (m); +-inf for absent bounds */
+int ncl_scopf_bounds(ncl_scopf_t S, double* xl, double* xu, double* x0, double* gl, double* gu);
+int ncl_scopf_contingencies(ncl_scopf_t S, int* branch_ids);
+int ncl_scopf_build_model(ncl_scopf_t S, ncl_model_t* out); /* this library's ModelBuilder */
+
 #ifdef __cplusplus
 }
 #endif

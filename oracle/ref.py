@@ -223,3 +223,92 @@ class RefFactorization:
         _chk(lib().ref_solve_refined(self.h, self.M.h, _p(b), float(target), int(max_sweeps), _p(x), C.byref(r),
                                      C.byref(s), C.byref(cv)))
         return x, r.value, s.value, bool(cv.value)
+
+
+class RefModel:
+    """The reference nclopf::ModelFunctions, built from the same spec
+    (template node programs + instances) as the product model."""
+
+    def __init__(self, h):
+        self.h = h
+        n, m, nj, nh = C.c_int(), C.c_int(), C.c_int64(), C.c_int64()
+        lib().ref_mf_sizes(h, C.byref(n), C.byref(m), C.byref(nj), C.byref(nh))
+        self.n, self.m, self.nnzj, self.nnzh = n.value, m.value, nj.value, nh.value
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ref_mf_free(self.h)
+            self.h = None
+
+    @staticmethod
+    def from_families(n, m, families):
+        """families: iterable of objects with name, nodes (ctypes array),
+        nslots, np, objective, rows, vars[ninst, nslots], params[ninst, np]."""
+        L = lib()
+        b = L.ref_mb_new(int(n))
+        try:
+            if m:
+                L.ref_mb_add_rows(b, int(m))
+            for F in families:
+                tid = C.c_int()
+                _chk(L.ref_mb_add_template(b, len(F.nodes), C.cast(F.nodes, C.c_void_p), int(F.nslots),
+                                           F.name.encode(), C.byref(tid)))
+                cnt = F.vars.shape[0] if F.nslots else len(F.rows)
+                if cnt == 0:
+                    continue
+                v = np.ascontiguousarray(F.vars, np.int32)
+                p = np.ascontiguousarray(F.params, np.float64) if F.np else None
+                r = None if F.objective else np.ascontiguousarray(F.rows, np.int32)
+                _chk(L.ref_mb_add_terms(b, tid.value, 1 if F.objective else 0, cnt, int(F.nslots), _p(v),
+                                        int(F.np), _p(p), _p(r)))
+            h = C.c_void_p()
+            _chk(L.ref_mb_build(b, C.byref(h)))
+        finally:
+            L.ref_mb_free(b)
+        return RefModel(h)
+
+    def jac_coords(self):
+        r, c = np.empty(self.nnzj, np.int32), np.empty(self.nnzj, np.int32)
+        lib().ref_mf_jac_coords(self.h, _p(r), _p(c))
+        return r, c
+
+    def hess_coords(self):
+        r, c = np.empty(self.nnzh, np.int32), np.empty(self.nnzh, np.int32)
+        lib().ref_mf_hess_coords(self.h, _p(r), _p(c))
+        return r, c
+
+    def eval_objective(self, w):
+        o = C.c_double()
+        _chk(lib().ref_mf_eval_objective(self.h, _p(np.ascontiguousarray(w, np.float64)), C.byref(o)))
+        return o.value
+
+    def _v(self, fn, w, size, *extra):
+        out = np.empty(size)
+        _chk(fn(self.h, _p(np.ascontiguousarray(w, np.float64)), *extra, _p(out)))
+        return out
+
+    def eval_grad_objective(self, w): return self._v(lib().ref_mf_eval_grad, w, self.n)
+    def eval_constraints(self, w): return self._v(lib().ref_mf_eval_cons, w, self.m)
+    def eval_jacobian(self, w): return self._v(lib().ref_mf_eval_jac, w, self.nnzj)
+
+    def eval_hessian_lag(self, w, sigma, lam):
+        return self._v(lib().ref_mf_eval_hess, w, self.nnzh, float(sigma),
+                       _p(np.ascontiguousarray(lam, np.float64)))
+
+    def jac_times(self, jv, v):
+        out = np.empty(self.m)
+        _chk(lib().ref_mf_jac_times(self.h, _p(np.ascontiguousarray(jv)), _p(np.ascontiguousarray(v)), _p(out)))
+        return out
+
+    def jac_trans_times(self, jv, y):
+        out = np.empty(self.n)
+        _chk(lib().ref_mf_jac_trans_times(self.h, _p(np.ascontiguousarray(jv)), _p(np.ascontiguousarray(y)),
+                                          _p(out)))
+        return out
+
+    def fd_check(self, w, seed, tol=1e-6):
+        errs = np.zeros(3)
+        ok = C.c_int()
+        _chk(lib().ref_mf_fd_check(self.h, _p(np.ascontiguousarray(w, np.float64)), int(seed), float(tol), _p(errs),
+                                   C.byref(ok)))
+        return dict(grad_err=errs[0], jac_err=errs[1], hess_err=errs[2], pass_=bool(ok.value))

@@ -116,23 +116,7 @@ API int64_t ncl_kernel_launches(void) { return g_kernel_launches; }
 // ---------------------------------------------------------------------------
 // SparseSym
 // ---------------------------------------------------------------------------
-struct ncl_sym {
-  SymPattern pat;
-  DevBuf<double> vals;
-  DevBuf<int> colptr, rowind;
-  DevBuf<int> diag_pos, mv_val, mv_col;
-  DevBuf<int64_t> mv_ptr;
-  DevBuf<int> slot_ptr, slot_trip;
-  DevBuf<double> trip_vals;
-  DevBuf<double> scratch;  // 4 doubles
-  DevBuf<double> rowsum;
-  DevPattern dp;
-  uint64_t hash = 0;
-  bool dev_ready = false;  // pattern + values uploaded (lazy: host-only use needs no GPU)
-  explicit ncl_sym(int n) : pat(n) {}
-};
-
-namespace {
+namespace nclb {
 uint64_t pattern_hash(const std::vector<int>& cp, const std::vector<int>& ri) {
   uint64_t h = 1469598103934665603ull;
   auto mix = [&](uint64_t v) {
@@ -217,7 +201,7 @@ void ensure_dev(ncl_sym* M, const char* what) {
   if (!M->pat.finalized()) throw Error{NCL_E_LOGIC, std::string(what) + ": matrix not finalized"};
   upload_pattern(M);
 }
-}  // namespace
+}  // namespace nclb
 
 API int ncl_sym_create(int n, ncl_sym_t* out) {
   GUARD({

@@ -62,3 +62,30 @@ struct DevBuf {
 };
 
 }  // namespace nclb
+
+#include "../../include/nclopf_b200.h"
+#include "cuda/dev.hpp"
+#include "host/sparse.hpp"
+
+// SparseSym handle (shared by the C-ABI translation units).
+struct ncl_sym {
+  nclb::SymPattern pat;
+  nclb::DevBuf<double> vals;
+  nclb::DevBuf<int> colptr, rowind;
+  nclb::DevBuf<int> diag_pos, mv_val, mv_col;
+  nclb::DevBuf<int64_t> mv_ptr;
+  nclb::DevBuf<int> slot_ptr, slot_trip;
+  nclb::DevBuf<double> trip_vals;
+  nclb::DevBuf<double> scratch;
+  nclb::DevBuf<double> rowsum;
+  nclb::DevPattern dp;
+  uint64_t hash = 0;
+  bool dev_ready = false;  // pattern + values uploaded (lazy: host-only use needs no GPU)
+  explicit ncl_sym(int n) : pat(n) {}
+};
+
+namespace nclb {
+uint64_t pattern_hash(const std::vector<int>& cp, const std::vector<int>& ri);
+void upload_pattern(ncl_sym* M);
+void ensure_dev(ncl_sym* M, const char* what);
+}  // namespace nclb

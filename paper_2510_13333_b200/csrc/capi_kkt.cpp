@@ -1,0 +1,92 @@
+// C-ABI for the condensed Newton matrix (K2 assembly).
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <vector>
+
+#include "capi_internal.hpp"
+#include "host/kkt.hpp"
+
+using namespace nclb;
+
+#define API extern "C" __attribute__((visibility("default")))
+#define GUARD(...)    \
+  try {               \
+    __VA_ARGS__;      \
+  } catch (...) {     \
+    return map_exc(); \
+  }                   \
+  return NCL_OK;
+
+struct ncl_kkt {
+  KktMap map;
+  std::unique_ptr<ncl_sym> K;
+  bool dev_ready = false;
+  DevBuf<int> slot_h, slot_diag, jterm;
+  DevBuf<int64_t> jptr;
+  DevBuf<double> h, j, s, d;  // host-path staging
+};
+
+namespace {
+void kkt_upload(ncl_kkt* k) {
+  if (k->dev_ready) return;
+  ensure_dev(k->K.get(), "kkt");
+  k->slot_h.upload(k->map.slot_h);
+  k->slot_diag.upload(k->map.slot_diag);
+  k->jptr.upload(k->map.jptr);
+  k->jterm.upload(k->map.jterm);
+  k->dev_ready = true;
+}
+}  // namespace
+
+API int ncl_kkt_create(int n, int m, int64_t nnzh, const int* hr, const int* hcl, int64_t nnzj, const int* jr,
+                       const int* jcl, ncl_kkt_t* out) {
+  GUARD({
+    std::vector<std::pair<int, int>> hc(nnzh), jc(nnzj);
+    for (int64_t k = 0; k < nnzh; ++k) hc[k] = {hr[k], hcl[k]};
+    for (int64_t k = 0; k < nnzj; ++k) {
+      jc[k] = {jr[k], jcl[k]};
+      if (k > 0 && jc[k] < jc[k - 1]) throw Error{NCL_E_INVALID, "kkt: jacobian coordinates must be row-sorted"};
+    }
+    auto k = std::make_unique<ncl_kkt>();
+    k->K = std::make_unique<ncl_sym>(n);
+    k->map = build_kkt(n, m, hc, jc, k->K->pat);
+    k->K->hash = pattern_hash(k->K->pat.col_ptr(), k->K->pat.row_ind());
+    *out = k.release();
+  });
+}
+API void ncl_kkt_destroy(ncl_kkt_t K) { delete K; }
+API ncl_sym_t ncl_kkt_matrix(ncl_kkt_t K) { return K->K.get(); }
+API int64_t ncl_kkt_num_triplets(ncl_kkt_t K) { return static_cast<int64_t>(K->map.trow.size()); }
+API int ncl_kkt_triplets(ncl_kkt_t K, int* rows, int* cols) {
+  GUARD({
+    std::copy(K->map.trow.begin(), K->map.trow.end(), rows);
+    std::copy(K->map.tcol.begin(), K->map.tcol.end(), cols);
+  });
+}
+API int ncl_kkt_assemble(ncl_kkt_t K, const double* hess, const double* jac, const double* sigx, double dw,
+                         const double* D, int where) {
+  GUARD({
+    kkt_upload(K);
+    const KktMap& m = K->map;
+    const int64_t nnz = K->K->pat.nnz();
+    if (where == NCL_DEVICE) {
+      dev_kkt_assemble(nnz, K->slot_h.p, K->slot_diag.p, K->jptr.p, K->jterm.p, hess, jac, sigx, dw, D,
+                       K->K->vals.p, g_stream);
+      check_launch("kkt_assemble");
+      return NCL_OK;
+    }
+    auto put = [](DevBuf<double>& b, const double* src, int64_t n) {
+      b.alloc(n);
+      if (n > 0) ck(cudaMemcpyAsync(b.p, src, n * sizeof(double), cudaMemcpyHostToDevice, g_stream), "H2D");
+    };
+    put(K->h, hess, m.nnzh);
+    put(K->j, jac, m.nnzj);
+    put(K->s, sigx, m.n);
+    put(K->d, D, m.m);
+    dev_kkt_assemble(nnz, K->slot_h.p, K->slot_diag.p, K->jptr.p, K->jterm.p, K->h.p, K->j.p, K->s.p, dw, K->d.p,
+                     K->K->vals.p, g_stream);
+    check_launch("kkt_assemble");
+    ck(cudaStreamSynchronize(g_stream), "sync");
+  });
+}

@@ -1,0 +1,124 @@
+// C-ABI for the SCOPF problem generator (host setup code).
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/nclopf_b200.h"
+#include "capi_internal.hpp"
+#include "host/scopf.hpp"
+#include "host/sparse.hpp"
+
+using namespace nclb;
+
+#define API extern "C" __attribute__((visibility("default")))
+#define GUARD(...)    \
+  try {               \
+    __VA_ARGS__;      \
+  } catch (...) {     \
+    return map_exc(); \
+  }                   \
+  return NCL_OK;
+
+struct ncl_scopf {
+  Grid grid;
+  ModelSpec spec;
+};
+
+API int ncl_scopf_create(int grid, int nb, int nl, int ng, uint64_t seed, int K, ncl_scopf_t* out) {
+  GUARD({
+    auto s = std::make_unique<ncl_scopf>();
+    try {
+      s->grid = grid == 0 ? grid_case9() : grid_synthetic(nb, nl, ng, seed);
+    } catch (const std::invalid_argument& e) {
+      throw Error{NCL_E_INVALID, e.what()};
+    }
+    const auto cont = select_contingencies(s->grid, K);
+    if (static_cast<int>(cont.size()) < K)
+      throw Error{NCL_E_INVALID, "scopf: fewer non-islanding contingencies than requested"};
+    s->spec = build_scopf(s->grid, cont);
+    *out = s.release();
+  });
+}
+API void ncl_scopf_destroy(ncl_scopf_t S) { delete S; }
+API int ncl_scopf_get_info(ncl_scopf_t S, ncl_scopf_info* info) {
+  GUARD({
+    const ModelSpec& p = S->spec;
+    info->n = p.n;
+    info->m = p.m;
+    info->nfam = static_cast<int>(p.fams.size());
+    info->K = p.K;
+    info->nb = p.nb;
+    info->nl = p.nl;
+    info->ng = p.ng;
+    info->ncomp = static_cast<int>(p.comp_rows.size());
+    info->nvar_scen = p.nvar_scen;
+    info->ncon_scen = p.ncon_scen;
+  });
+}
+API int ncl_scopf_family_info(ncl_scopf_t S, int f, char* name, int* nnodes, int* nslots, int* np, int* objective,
+                              int64_t* ninst) {
+  GUARD({
+    if (f < 0 || f >= static_cast<int>(S->spec.fams.size())) throw Error{NCL_E_INVALID, "scopf: bad family"};
+    const SpecFamily& F = S->spec.fams[f];
+    if (name) {
+      std::strncpy(name, F.name.c_str(), 63);
+      name[63] = 0;
+    }
+    *nnodes = static_cast<int>(F.nodes.size());
+    *nslots = F.nslots;
+    *np = F.np;
+    *objective = F.objective ? 1 : 0;
+    *ninst = F.ninst();
+  });
+}
+API int ncl_scopf_family_data(ncl_scopf_t S, int f, ncl_expr_node* nodes, int* rows, int* vars, double* params) {
+  GUARD({
+    const SpecFamily& F = S->spec.fams.at(f);
+    if (nodes) std::memcpy(nodes, F.nodes.data(), F.nodes.size() * sizeof(ncl_expr_node));
+    if (rows && !F.rows.empty()) std::memcpy(rows, F.rows.data(), F.rows.size() * sizeof(int));
+    if (vars && !F.vars.empty()) std::memcpy(vars, F.vars.data(), F.vars.size() * sizeof(int));
+    if (params && !F.params.empty()) std::memcpy(params, F.params.data(), F.params.size() * sizeof(double));
+  });
+}
+API int ncl_scopf_bounds(ncl_scopf_t S, double* xl, double* xu, double* x0, double* gl, double* gu) {
+  GUARD({
+    const ModelSpec& p = S->spec;
+    auto cp = [](double* d, const std::vector<double>& v) {
+      if (d && !v.empty()) std::memcpy(d, v.data(), v.size() * sizeof(double));
+    };
+    cp(xl, p.xl);
+    cp(xu, p.xu);
+    cp(x0, p.x0);
+    cp(gl, p.gl);
+    cp(gu, p.gu);
+  });
+}
+API int ncl_scopf_contingencies(ncl_scopf_t S, int* ids) {
+  GUARD(if (!S->spec.contingencies.empty()) std::memcpy(ids, S->spec.contingencies.data(),
+                                                         S->spec.contingencies.size() * sizeof(int)));
+}
+API int ncl_scopf_build_model(ncl_scopf_t S, ncl_model_t* out) {
+  GUARD({
+    const ModelSpec& p = S->spec;
+    ncl_builder_t B = nullptr;
+    int rc = ncl_builder_create(p.n, &B);
+    if (rc != NCL_OK) return rc;
+    std::unique_ptr<ncl_builder, void (*)(ncl_builder_t)> guard(B, ncl_builder_destroy);
+    int first = 0;
+    if ((rc = ncl_builder_add_rows(B, p.m, &first)) != NCL_OK) return rc;
+    for (const SpecFamily& F : p.fams) {
+      int tid = 0;
+      if ((rc = ncl_builder_add_template(B, static_cast<int>(F.nodes.size()), F.nodes.data(), F.nslots,
+                                         F.name.c_str(), &tid)) != NCL_OK)
+        return rc;
+      const int64_t cnt = F.ninst();
+      if (cnt == 0) continue;
+      rc = F.objective ? ncl_builder_add_objective_terms(B, tid, cnt, F.nslots, F.vars.data(), F.np, F.params.data())
+                       : ncl_builder_add_constraint_terms(B, tid, cnt, F.rows.data(), F.nslots, F.vars.data(), F.np,
+                                                          F.params.data());
+      if (rc != NCL_OK) return rc;
+    }
+    if ((rc = ncl_builder_build(B, out)) != NCL_OK) return rc;
+  });
+}

@@ -77,5 +77,8 @@ void dev_frob_sq(const DevPattern& P, const int* colptr, const int* rowind, cons
 int dev_num_sms();
 void dev_gather_sum(int64_t nslots, const int* ptr, const int* idx, const double* src, double* dst,
                     cudaStream_t st);
+void dev_kkt_assemble(int64_t nnz, const int* slot_h, const int* slot_diag, const int64_t* jptr, const int* jterm,
+                      const double* H, const double* J, const double* sigx, double dw, const double* D, double* K,
+                      cudaStream_t st);
 
 }  // namespace nclb

@@ -1,0 +1,105 @@
+"""SCOPF problem generator binding (C-ABI ncl_scopf_*): the paper-layout
+corrective AC-SCOPF on MATPOWER case9 or seeded synthetic geometric grids."""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from ._lib import P, check, i32, i64, lib, register
+from .model import ExprNode, ModelFunctions
+from .sparse import _ptr
+
+
+class ScopfInfo(C.Structure):
+    _fields_ = [("n", i32), ("m", i32), ("nfam", i32), ("K", i32), ("nb", i32), ("nl", i32), ("ng", i32),
+                ("ncomp", i32), ("nvar_scen", i32), ("ncon_scen", i32)]
+
+
+register({
+    "ncl_scopf_create": (i32, [i32, i32, i32, i32, C.c_uint64, i32, C.POINTER(P)]),
+    "ncl_scopf_destroy": (None, [P]),
+    "ncl_scopf_get_info": (i32, [P, C.POINTER(ScopfInfo)]),
+    "ncl_scopf_family_info": (i32, [P, i32, C.c_char_p, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32),
+                                    C.POINTER(i32), C.POINTER(i64)]),
+    "ncl_scopf_family_data": (i32, [P, i32, P, P, P, P]),
+    "ncl_scopf_bounds": (i32, [P, P, P, P, P, P]),
+    "ncl_scopf_contingencies": (i32, [P, P]),
+    "ncl_scopf_build_model": (i32, [P, C.POINTER(P)]),
+})
+
+# Grid sizes of the BASELINE.json configs
+GRIDS = {
+    "case9": (0, 9, 9, 3),
+    "case118": (1, 118, 186, 54),        # same-size synthetic (no MATPOWER data offline)
+    "activsg500": (1, 500, 597, 56),
+    "activsg2000": (1, 2000, 3206, 432),
+}
+
+
+@dataclass
+class Family:
+    name: str
+    nodes: object
+    nslots: int
+    np: int
+    objective: bool
+    rows: np.ndarray
+    vars: np.ndarray
+    params: np.ndarray
+
+
+class Scopf:
+    def __init__(self, grid: str = "case9", K: int = 0, seed: int = 2510):
+        kind, nb, nl, ng = GRIDS[grid]
+        h = C.c_void_p()
+        check(lib.ncl_scopf_create(kind, nb, nl, ng, seed, K, C.byref(h)))
+        self._h = h
+        s = ScopfInfo()
+        check(lib.ncl_scopf_get_info(h, C.byref(s)))
+        self.info = s
+        self.n, self.m, self.K = s.n, s.m, s.K
+        self.grid = grid
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.ncl_scopf_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def families(self):
+        out = []
+        for f in range(self.info.nfam):
+            name = C.create_string_buffer(64)
+            nn, ns, np_, obj, ni = C.c_int(), C.c_int(), C.c_int(), C.c_int(), C.c_int64()
+            check(lib.ncl_scopf_family_info(self._h, f, name, C.byref(nn), C.byref(ns), C.byref(np_), C.byref(obj),
+                                            C.byref(ni)))
+            nodes = (ExprNode * nn.value)()
+            rows = np.empty(0 if obj.value else ni.value, np.int32)
+            vars_ = np.empty(ni.value * ns.value, np.int32)
+            params = np.empty(ni.value * np_.value, np.float64)
+            check(lib.ncl_scopf_family_data(self._h, f, nodes, _ptr(rows), _ptr(vars_), _ptr(params)))
+            out.append(Family(name.value.decode(), nodes, ns.value, np_.value, bool(obj.value), rows,
+                              vars_.reshape(ni.value, ns.value), params.reshape(ni.value, np_.value)))
+        return out
+
+    def bounds(self):
+        xl, xu, x0 = (np.empty(self.n) for _ in range(3))
+        gl, gu = np.empty(self.m), np.empty(self.m)
+        check(lib.ncl_scopf_bounds(self._h, _ptr(xl), _ptr(xu), _ptr(x0), _ptr(gl), _ptr(gu)))
+        return dict(xl=xl, xu=xu, x0=x0, gl=gl, gu=gu)
+
+    def contingencies(self):
+        ids = np.empty(self.K, np.int32)
+        check(lib.ncl_scopf_contingencies(self._h, _ptr(ids)))
+        return ids
+
+    def build_model(self) -> ModelFunctions:
+        h = C.c_void_p()
+        check(lib.ncl_scopf_build_model(self._h, C.byref(h)))
+        return ModelFunctions(h)
