@@ -200,6 +200,33 @@ Grid grid_synthetic(int nb, int nl, int ng, uint64_t seed) {
         }
     }
   }
+  // leaf-pairing chords: an MST leaf's only line is a bridge (its outage
+  // islands the bus). Pair leaves greedily by distance so each chord closes a
+  // short cycle through both; ACTIVSg-size grids then admit >= 256
+  // non-islanding line outages like the real cases do.
+  {
+    std::vector<int> deg0(nb, 0);
+    for (const auto& e : edges) deg0[e.first]++, deg0[e.second]++;
+    std::vector<int> leaves;
+    for (int i = 0; i < nb; ++i)
+      if (deg0[i] == 1) leaves.push_back(i);
+    std::vector<std::pair<double, std::pair<int, int>>> lp;
+    for (size_t a = 0; a < leaves.size(); ++a)
+      for (size_t b = a + 1; b < leaves.size(); ++b)
+        lp.push_back({dist(leaves[a], leaves[b]), {leaves[a], leaves[b]}});
+    std::sort(lp.begin(), lp.end());
+    std::vector<char> used(nb, 0);
+    const int budget = (nl - static_cast<int>(edges.size())) * 3 / 4;
+    int added = 0;
+    for (const auto& c : lp) {
+      if (added >= budget) break;
+      const int u = c.second.first, v = c.second.second;
+      if (used[u] || used[v]) continue;
+      used[u] = used[v] = 1;
+      edges.emplace_back(u, v);
+      ++added;
+    }
+  }
   // nearest-neighbour chords (8-NN candidates, shortest first)
   {
     std::vector<std::pair<double, std::pair<int, int>>> cand;
