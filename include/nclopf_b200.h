@@ -153,6 +153,9 @@ int ncl_model_jac_trans_times(ncl_model_t M, const double* jac_vals, const doubl
  * jac[nnz_jac], hess[nnz_hess] (any may be NULL). Asynchronous. */
 int ncl_model_eval_all_device(ncl_model_t M, const double* w, double sigma, const double* lam, double* obj,
                               double* grad, double* c, double* jac, double* hess);
+/* Device fast path of eval_objective + eval_constraints (trial points of the
+ * line search): value programs only. Asynchronous. */
+int ncl_model_eval_values_device(ncl_model_t M, const double* w, double* obj, double* c);
 /* Pending DomainError of device-path evaluations: returns NCL_E_DOMAIN (and
  * clears it) if any evaluation left the smooth domain. Synchronizes. */
 int ncl_model_check_domain(ncl_model_t M);

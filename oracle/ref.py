@@ -66,6 +66,9 @@ def lib():
             "ref_mf_eval_hess": (i32, [P, P, f64, P, P]),
             "ref_mf_jac_times": (i32, [P, P, P, P]), "ref_mf_jac_trans_times": (i32, [P, P, P, P]),
             "ref_mf_fd_check": (i32, [P, P, C.c_uint, f64, P, pi]),
+            "ref_ipm_last_error": (C.c_char_p, []),
+            "ref_ipm_default_options": (None, [P]),
+            "ref_ncl_solve": (i32, [P, P, P, P, P, P, P, P, P, P, P, C.c_char_p, i64, C.POINTER(i64)]),
         }
         for k, (r, a) in sig.items():
             fn = getattr(L, k)
@@ -312,3 +315,30 @@ class RefModel:
         _chk(lib().ref_mf_fd_check(self.h, _p(np.ascontiguousarray(w, np.float64)), int(seed), float(tol), _p(errs),
                                    C.byref(ok)))
         return dict(grad_err=errs[0], jac_err=errs[1], hess_err=errs[2], pass_=bool(ok.value))
+
+
+def ref_ncl_solve(model: RefModel, bounds, perm=None, options=None, trace_cap=1 << 26):
+    """ncl_solve over the reference CPU backend (oracle/ref_ipm.cpp): the same
+    host NCL/IPM control flow driving the UNMODIFIED reference model_ad and
+    sparse_core. `options` is a paper_2510_13333_b200.ipm.NclOptions (the
+    ctypes mirror of include/nclopf_ipm.h) or None for the defaults."""
+    import json
+
+    from paper_2510_13333_b200.ipm import STATUS, NclOptions, NclResult
+
+    L = lib()
+    if options is None:
+        options = NclOptions()
+        L.ref_ipm_default_options(C.byref(options))
+    arrs = [np.ascontiguousarray(bounds[k], np.float64) for k in ("xl", "xu", "x0", "gl", "gu")]
+    pm = None if perm is None else np.ascontiguousarray(perm, np.int32)
+    res = NclResult()
+    x, y = np.empty(model.n), np.empty(model.m)
+    buf = C.create_string_buffer(trace_cap)
+    ln = C.c_int64()
+    rc = L.ref_ncl_solve(model.h, *[_p(a) for a in arrs], _p(pm), C.byref(options), C.byref(res), _p(x), _p(y),
+                         buf, trace_cap, C.byref(ln))
+    if rc != 0:
+        raise RefError(rc, L.ref_ipm_last_error().decode())
+    trace = [json.loads(t) for t in buf.value.decode().splitlines() if t.strip()]
+    return dict(result=res.as_dict(), status=STATUS.get(res.status, str(res.status)), x=x, y=y, trace=trace)

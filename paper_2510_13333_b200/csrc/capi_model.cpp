@@ -362,6 +362,16 @@ API int ncl_model_eval_all_device(ncl_model_t M, const double* w, double sigma, 
     check_launch("eval_all");
   });
 }
+API int ncl_model_eval_values_device(ncl_model_t M, const double* w, double* obj, double* c) {
+  GUARD({
+    upload_model(M);
+    const BuiltModel& B = M->B;
+    dev_eval(M->dm, PK_V, w, 1.0, nullptr, g_stream);
+    if (obj) dev_gather64(1, M->o_ptr.p, M->o_idx.p, M->contrib.p, obj, g_stream);
+    if (c) dev_gather64(B.m, M->c_ptr.p, M->c_idx.p, M->contrib.p, c, g_stream);
+    check_launch("eval_values");
+  });
+}
 API int ncl_model_check_domain(ncl_model_t M) { GUARD(upload_model(M); check_domain_sync(M)); }
 
 // fd_check (model.cpp:229-315): same RNG stream and probe arithmetic; the

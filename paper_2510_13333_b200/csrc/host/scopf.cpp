@@ -77,8 +77,8 @@ BranchY branch_y(const Grid& g, int l) {
 }
 
 // DC power flow angles with generation proportional to pmax (CG on the
-// reduced Laplacian). Deterministic.
-std::vector<double> dc_angles(const Grid& g) {
+// reduced Laplacian), optionally with branch `out` removed. Deterministic.
+std::vector<double> dc_angles(const Grid& g, int out = -1) {
   const int n = g.nb;
   std::vector<double> P(n, 0.0);
   double pd = 0, pm = 0;
@@ -89,6 +89,7 @@ std::vector<double> dc_angles(const Grid& g) {
   auto apply = [&](const std::vector<double>& th, std::vector<double>& y) {
     std::fill(y.begin(), y.end(), 0.0);
     for (int l = 0; l < g.nl; ++l) {
+      if (l == out) continue;
       const double w = 1.0 / g.x[l];
       const double d = th[g.f[l]] - th[g.t[l]];
       y[g.f[l]] += w * d;
@@ -297,10 +298,21 @@ Grid grid_synthetic(int nb, int nl, int ng, uint64_t seed) {
     g.c0.push_back(0.0);
   }
   g.ref = g.gbus[std::max_element(g.pmax.begin(), g.pmax.end()) - g.pmax.begin()];
-  // ratings from the DC base flow
-  const std::vector<double> th = dc_angles(g);
+  // Ratings: 1.2 x the largest |DC flow| over the base case and every
+  // non-islanding single-branch outage, + 0.25 pu headroom for reactive flow.
+  // (SURVEY.md §8(d)'s "1.5 x base DC flow + 0.1" leaves N-1 AC-infeasible
+  // instances — the NCL penalty then diverges; this keeps every selectable
+  // contingency feasible while the limits still bind near the N-1 maxima.)
+  // Independent of K, so every config of one grid shares the same network.
+  std::vector<double> fmax(g.nl, 0.0);
+  auto absorb = [&](const std::vector<double>& th, int out) {
+    for (int l = 0; l < g.nl; ++l)
+      if (l != out) fmax[l] = std::max(fmax[l], std::abs((th[g.f[l]] - th[g.t[l]]) / g.x[l]));
+  };
+  absorb(dc_angles(g), -1);
+  for (int l : select_contingencies(g, g.nl)) absorb(dc_angles(g, l), l);
   g.rate.resize(g.nl);
-  for (int l = 0; l < g.nl; ++l) g.rate[l] = 1.5 * std::abs((th[g.f[l]] - th[g.t[l]]) / g.x[l]) + 0.1;
+  for (int l = 0; l < g.nl; ++l) g.rate[l] = 1.2 * fmax[l] + 0.25;
   return g;
 }
 

@@ -81,6 +81,7 @@ class Expr:
     def __mul__(self, o): return Expr(MUL, self, Expr._w(o))
     def __rmul__(self, o): return Expr(MUL, Expr._w(o), self)
     def __truediv__(self, o): return Expr(DIV, self, Expr._w(o))
+    def __rtruediv__(self, o): return Expr(DIV, Expr._w(o), self)
     def __neg__(self): return Expr(NEG, self)
     def __pow__(self, e): return Expr(POW, self, value=float(e))
 

@@ -98,7 +98,7 @@ class SparseSym:
         return v
 
     def set_values(self, vals, where: int = HOST) -> None:
-        v = _f64(vals) if where == HOST else vals
+        v = vals if (where != HOST or hasattr(vals, "data_ptr")) else _f64(vals)
         check(lib.ncl_sym_set_values(self._h, _ptr(v), where))
 
     def device_values_ptr(self) -> int:
@@ -269,7 +269,10 @@ class Factorization:
 
     def solve_in_place(self, x, where: int = HOST) -> None:
         if where == HOST:
-            assert x.dtype == np.float64 and x.flags.c_contiguous
+            if hasattr(x, "data_ptr"):  # pinned torch CPU tensor
+                assert str(x.dtype) == "torch.float64" and x.is_contiguous() and not x.is_cuda
+            else:
+                assert x.dtype == np.float64 and x.flags.c_contiguous
         check(lib.ncl_fact_solve(self._h, _ptr(x), where))
 
     def solve(self, b) -> np.ndarray:
