@@ -45,6 +45,7 @@ register({
     "ncl_model_jac_times": (i32, [P, P, P, P, i32]),
     "ncl_model_jac_trans_times": (i32, [P, P, P, P, i32]),
     "ncl_model_eval_all_device": (i32, [P, P, f64, P, P, P, P, P, P]),
+    "ncl_model_eval_values_device": (i32, [P, P, P, P]),
     "ncl_model_check_domain": (i32, [P]),
     "ncl_fd_check": (i32, [P, P, C.c_uint, f64, P, C.POINTER(i32)]),
 })
