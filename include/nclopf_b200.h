@@ -87,6 +87,8 @@ typedef struct ncl_symb_info {
   int max_rows;           /* tallest supernode panel */
   int64_t l_storage;      /* doubles in the dense supernode panels */
   double flops;           /* sum_j (c_j^2 + 2 c_j) */
+  int64_t cb_storage;     /* doubles in the multifrontal contribution blocks */
+  int nsplit;             /* supernodes below this ticket run warp-per-task, above CTA-per-task */
 } ncl_symb_info;
 int ncl_symb_info_get(ncl_symb_t S, ncl_symb_info* info);
 int ncl_symb_get(ncl_symb_t S, int* perm, int* iperm, int* parent, int* up_colptr, int* up_rowind,

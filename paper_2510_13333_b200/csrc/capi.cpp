@@ -358,8 +358,8 @@ struct ncl_symb {
   uint64_t hash = 0;
   int nnz = 0;
   DevSymb d;
-  DevBuf<int> perm, sn_first, sn_parent, rows, upd, cptr, child, order, asrc, aoff, flags, tickets;
-  DevBuf<int64_t> sn_rptr, sn_loff, uptr, aptr;
+  DevBuf<int> perm, sn_first, sn_parent, rows, relp, cptr, child, order, asrc, aoff, flags, tickets;
+  DevBuf<int64_t> sn_rptr, sn_loff, cb_off, aptr;
   bool dev_ready = false;
 };
 
@@ -372,13 +372,13 @@ void upload_symb(ncl_symb* S) {
   S->sn_first.upload(Z.sn_first);
   S->sn_parent.upload(Z.sn_parent);
   S->rows.upload(Z.rows);
-  S->upd.upload(Z.upd);
+  S->relp.upload(Z.relp);
   S->cptr.upload(Z.cptr);
   S->child.upload(Z.child);
   S->order.upload(Z.order);
   S->sn_rptr.upload(Z.sn_rptr);
   S->sn_loff.upload(Z.sn_loff);
-  S->uptr.upload(Z.uptr);
+  S->cb_off.upload(Z.cb_off);
   // A entries grouped by target supernode, sorted by panel offset
   const int nsn = Z.nsn;
   std::vector<int64_t> aptr(nsn + 1, 0);
@@ -409,10 +409,9 @@ void upload_symb(ncl_symb* S) {
   DevSymb& d = S->d;
   d.n = S->core.n;
   d.nsn = nsn;
-  int nleaf = 0;
-  for (int s = 0; s < nsn; ++s)
-    if (Z.height[s] == 0) nleaf++;
-  d.nleaf = nleaf;
+  d.nleaf = Z.nleaf;
+  d.nsplit = Z.nsplit;
+  d.cb_storage = Z.cb_storage;
   d.nnz = S->nnz;
   d.l_storage = Z.l_storage;
   d.perm = S->perm.p;
@@ -421,8 +420,8 @@ void upload_symb(ncl_symb* S) {
   d.sn_rptr = S->sn_rptr.p;
   d.rows = S->rows.p;
   d.sn_loff = S->sn_loff.p;
-  d.uptr = S->uptr.p;
-  d.upd = S->upd.p;
+  d.relp = S->relp.p;
+  d.cb_off = S->cb_off.p;
   d.cptr = S->cptr.p;
   d.child = S->child.p;
   d.order = S->order.p;
@@ -471,6 +470,8 @@ API int ncl_symb_info_get(ncl_symb_t S, ncl_symb_info* info) {
     info->max_rows = S->Z.max_nr;
     info->l_storage = S->Z.l_storage;
     info->flops = S->Z.flops;
+    info->cb_storage = S->Z.cb_storage;
+    info->nsplit = S->Z.nsplit;
   });
 }
 API int ncl_symb_get(ncl_symb_t S, int* perm, int* iperm, int* parent, int* up_colptr, int* up_rowind,
@@ -496,7 +497,7 @@ struct ncl_fact {
   ncl_symb* S = nullptr;
   std::unique_ptr<ncl_symb> owned;
   DevFactor F;
-  DevBuf<double> L, D, xp, scal, work1, work2, work3;
+  DevBuf<double> L, CB, CV, D, xp, scal, work1, work2, work3;
   DevBuf<int> istat;
 };
 
@@ -509,6 +510,8 @@ void check_match(ncl_sym_t M, ncl_symb* S) {
 void alloc_fact(ncl_fact* f) {
   const int n = f->S->core.n;
   f->L.alloc(std::max<int64_t>(1, f->S->Z.l_storage));
+  f->CB.alloc(std::max<int64_t>(1, f->S->Z.cb_storage));
+  f->CV.alloc(std::max<int64_t>(1, static_cast<int64_t>(f->S->Z.rows.size())));
   f->D.alloc(std::max(1, n));
   f->xp.alloc(std::max(1, n));
   f->scal.alloc(8);
@@ -517,6 +520,8 @@ void alloc_fact(ncl_fact* f) {
   f->work2.alloc(std::max(1, n));
   f->work3.alloc(std::max(1, n));
   f->F.L = f->L.p;
+  f->F.CB = f->CB.p;
+  f->F.CV = f->CV.p;
   f->F.D = f->D.p;
   f->F.xp = f->xp.p;
   f->F.scal = f->scal.p;
@@ -668,21 +673,25 @@ API int ncl_fact_get_L(ncl_fact_t F, int* lp, int* li, double* lx) {
     if (Z.l_storage > 0)
       ck(cudaMemcpyAsync(Lh.data(), F->L.p, Z.l_storage * sizeof(double), cudaMemcpyDeviceToHost, g_stream), "D2H");
     ck(cudaStreamSynchronize(g_stream), "sync");
-    int64_t pos = 0;
-    if (lp) lp[0] = 0;
-    for (int s = 0; s < Z.nsn; ++s) {
-      const int f = Z.sn_first[s], w = Z.sn_first[s + 1] - f;
+    // reference layout: only the true structure of L (amalgamated panels
+    // also hold explicit zeros outside it)
+    std::vector<int64_t> tp;
+    std::vector<int> ti;
+    true_L_structure(F->S->core, tp, ti);
+    for (int j = 0; j <= n; ++j)
+      if (lp) lp[j] = static_cast<int>(tp[j]);
+    for (int j = 0; j < n; ++j) {
+      const int s = Z.sn_of_col[j], f = Z.sn_first[s];
       const int64_t rb = Z.sn_rptr[s];
       const int nr = static_cast<int>(Z.sn_rptr[s + 1] - rb);
-      for (int c = 0; c < w; ++c) {
-        for (int i = c + 1; i < nr; ++i) {
-          if (li) li[pos] = Z.rows[rb + i];
-          if (lx) lx[pos] = Lh[Z.sn_loff[s] + static_cast<int64_t>(c) * nr + i];
-          ++pos;
-        }
-        if (lp) lp[f + c + 1] = static_cast<int>(pos);
+      const int* R = Z.rows.data() + rb;
+      int q = 0;
+      for (int64_t p = tp[j]; p < tp[j + 1]; ++p) {
+        const int r = ti[p];
+        while (R[q] < r) ++q;
+        if (li) li[p] = r;
+        if (lx) lx[p] = Lh[Z.sn_loff[s] + static_cast<int64_t>(j - f) * nr + q];
       }
     }
-    (void)n;
   });
 }

@@ -14,7 +14,7 @@ extern int64_t g_kernel_launches;
 
 // Symbolic schedule resident in HBM (built once from host Supernodal).
 struct DevSymb {
-  int n = 0, nsn = 0, nleaf = 0;
+  int n = 0, nsn = 0, nleaf = 0, nsplit = 0;
   int64_t nnz = 0, l_storage = 0;
   int* perm = nullptr;       // [n]
   int* sn_first = nullptr;   // [nsn+1]
@@ -22,8 +22,9 @@ struct DevSymb {
   int64_t* sn_rptr = nullptr;
   int* rows = nullptr;
   int64_t* sn_loff = nullptr;
-  int64_t* uptr = nullptr;
-  int* upd = nullptr;   // (d, p0, p1) triples
+  int* relp = nullptr;       // [rows] child row -> position in the parent's row list
+  int64_t* cb_off = nullptr; // [nsn+1] contribution-block offsets ((nr-w)^2 each)
+  int64_t cb_storage = 0;
   int* cptr = nullptr;  // children CSR
   int* child = nullptr;
   int* order = nullptr;  // ticket order, leaves first
@@ -51,6 +52,8 @@ struct DevPattern {
 
 struct DevFactor {
   double* L = nullptr;  // panels
+  double* CB = nullptr; // contribution blocks (multifrontal Schur updates)
+  double* CV = nullptr; // [rows] forward-solve contribution vectors
   double* D = nullptr;  // [n] by pivot position
   double* xp = nullptr;  // [n] permuted work vector
   double* scal = nullptr;  // [4]: thresh, maxdiag, scratch

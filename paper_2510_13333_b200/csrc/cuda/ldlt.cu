@@ -4,17 +4,19 @@
 // (/root/reference/proj/src/sparse_sym.cpp:268-337), solve_in_place (:346-363)
 // and SparseSym::multiply/max_abs_diag/norm_inf (:69-115).
 //
-// Factorization: supernodal LEFT-looking LDLᵀ, 1x1 pivots in the fixed
-// symbolic order, no pivoting. One warp owns one supernode panel and gathers
-// every descendant update into it in a fixed order (so results are
-// deterministic run to run — SPEC.md:69), then factors its dense diagonal
-// block and scales the off-diagonal rows. Scheduling is a single persistent
-// launch: tasks come from one ticket counter in leaves-first height order
-// (leaves in chunks), and each inner task waits on its children's epoch
-// flags (release/acquire at gpu scope). Deadlock freedom: the minimum
-// outstanding ticket only depends on smaller tickets held by running warps.
+// Factorization: MULTIFRONTAL supernodal LDLᵀ with 1x1 pivots in the fixed
+// symbolic order (no pivoting; the NCL regularisation keeps K quasi-definite,
+// PAPER.md:431-433). Every supernode assembles its front from its own A
+// entries and its children's contribution blocks only (extend-add in
+// ascending child order: deterministic run to run), factors its
+// pivot columns and leaves its Schur complement for its parent. One
+// persistent launch per team size: warps for the wide bottom of the
+// elimination tree, CTAs for the narrow top; dependencies are epoch flags
+// (release/acquire at gpu scope) on the children, tickets are issued in
+// leaves-first height order.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "dev.hpp"
@@ -23,8 +25,6 @@ namespace nclb {
 
 namespace {
 
-constexpr int kWarps = 4;          // warps per CTA of the persistent kernels
-constexpr int kRelCap = 256;       // cached relative indices per warp
 constexpr unsigned kFull = 0xffffffffu;
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -40,49 +40,70 @@ __device__ __forceinline__ void wait_flag(const int* f, int epoch) {
   while (ld_acquire(f) != epoch) __nanosleep(32);
 }
 
-__device__ __forceinline__ int lower_bound_i(const int* __restrict__ a, int n, int key) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (__ldg(a + mid) < key) lo = mid + 1;
-    else hi = mid;
-  }
-  return lo;
-}
 
 __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
   // non-negative doubles order like their bit patterns
   atomicMax(reinterpret_cast<unsigned long long*>(addr), static_cast<unsigned long long>(__double_as_longlong(v)));
 }
 
-// Task queue: one ticket counter for the whole launch. Tickets below
-// nleaf_chunks hand out chunks of kLeafChunk leaves (no dependencies); later
-// tickets hand out single inner supernodes in leaves-first height order.
-// Only running warps take tickets, so the minimum outstanding task always
-// has all of its (smaller-ticket) dependencies finished or in progress by a
-// running warp: no deadlock even if not every CTA is resident.
+// ---------------------------------------------------------------------------
+// Multifrontal numeric LDLᵀ (K3). Tasks are supernodes in leaves-first
+// height order (Z.order). Supernode s with panel P (nr x w, column-major,
+// the L storage) and contribution block CB_s ((nr-w)^2, column-major):
+//   1. wait for the children's epoch flags,
+//   2. P := A entries (scatter), CB_s := 0,
+//   3. extend-add every child's CB into (P | CB_s) through the relative row
+//      map, children in ascending index order (deterministic sums),
+//   4. dense right-looking LDLᵀ of the w pivot columns of P,
+//   5. CB_s -= L21 D L21ᵀ (lower triangle),
+//   6. publish (fence + release flag).
+// Team = one warp (NT = 32) for the wide bottom of the tree, one CTA
+// (NT = 256) for the narrow top (tickets >= Z.nsplit), two launches.
+// ---------------------------------------------------------------------------
 constexpr int kLeafChunk = 8;
-struct TaskCursor {
-  int cur = 0, end = 0;
-};
-__device__ __forceinline__ int next_task(TaskCursor& tc, int nleaf, int nsn, int* ticket, int lane) {
-  if (tc.cur < tc.end) return tc.cur++;
-  int t = 0;
-  if (lane == 0) t = atomicAdd(ticket, 1);
-  t = __shfl_sync(kFull, t, 0);
-  const int nchunks = (nleaf + kLeafChunk - 1) / kLeafChunk;
-  if (t < nchunks) {
-    tc.cur = t * kLeafChunk;
-    tc.end = min(nleaf, tc.cur + kLeafChunk);
-    return tc.cur++;
-  }
-  const int s = nleaf + (t - nchunks);
-  return s < nsn ? s : -1;
+
+template <int NT>
+__device__ __forceinline__ void team_sync() {
+  if constexpr (NT == 32) __syncwarp();
+  else __syncthreads();
 }
+
+// Task claiming: warps claim individually (leaves in chunks of kLeafChunk),
+// CTAs claim one task at a time. Tickets are handed out in order, so the
+// minimum outstanding task always has its dependencies finished or held by a
+// running team: no deadlock even when not every team is resident.
+template <int NT>
+struct Claim {
+  int cur = 0, end = 0;
+  __device__ __forceinline__ int next(int* ticket, int t0, int t1, int nleaf, int tid, int* sh) {
+    if constexpr (NT == 32) {
+      if (cur < end) return cur++;
+      int t = 0;
+      if (tid == 0) t = atomicAdd(ticket, 1);
+      t = __shfl_sync(kFull, t, 0);
+      const int nl = max(0, min(nleaf, t1) - t0);  // leaves inside this phase
+      const int nchunks = (nl + kLeafChunk - 1) / kLeafChunk;
+      if (t < nchunks) {
+        cur = t0 + t * kLeafChunk;
+        end = min(t0 + nl, cur + kLeafChunk);
+        return cur++;
+      }
+      const int k = t0 + nl + (t - nchunks);
+      return k < t1 ? k : -1;
+    } else {
+      __syncthreads();
+      if (tid == 0) *sh = atomicAdd(ticket, 1);
+      __syncthreads();
+      const int k = t0 + *sh;
+      return k < t1 ? k : -1;
+    }
+  }
+};
 
 struct FactorArgs {
   DevSymb S;
   double* L;
+  double* CB;
   double* D;
   const double* kvals;
   const double* thresh;
@@ -90,89 +111,94 @@ struct FactorArgs {
   int* flags;
   int* ticket;
   int epoch;
+  int t0, t1;  // ticket range of this launch
 };
 
-__global__ void __launch_bounds__(kWarps * 32) factor_kernel(FactorArgs a) {
-  __shared__ int s_rel[kWarps][kRelCap];
-  const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
+template <int NT>
+__device__ __forceinline__ void factor_task(const FactorArgs& a, int s, int tid, double thresh) {
   const DevSymb& S = a.S;
-  const double thresh = __ldcg(a.thresh);
-  TaskCursor tc;
-  int* rel = s_rel[wib];
-  for (;;) {
-    const int t = next_task(tc, S.nleaf, S.nsn, a.ticket, lane);
-    if (t < 0) break;
-    const int s = __ldg(S.order + t);
-    // wait for children (their subtrees are complete by induction)
-    if (lane == 0)
-      for (int q = __ldg(S.cptr + s); q < __ldg(S.cptr + s + 1); ++q) wait_flag(a.flags + __ldg(S.child + q), a.epoch);
-    __syncwarp();
-    const int f = __ldg(S.sn_first + s);
-    const int w = __ldg(S.sn_first + s + 1) - f;
-    const int64_t rb = __ldg(S.sn_rptr + s);
-    const int nr = static_cast<int>(__ldg(S.sn_rptr + s + 1) - rb);
-    const int* Rs = S.rows + rb;
-    double* P = a.L + __ldg(S.sn_loff + s);
-    // zero-fill and scatter A (each panel entry has at most one A entry)
-    for (int i = lane; i < w * nr; i += 32) P[i] = 0.0;
-    __syncwarp();
-    for (int64_t e = __ldg(S.aptr + s) + lane; e < __ldg(S.aptr + s + 1); e += 32)
-      P[__ldg(S.aoff + e)] = __ldg(a.kvals + __ldg(S.asrc + e));
-    __syncwarp();
-    // gather descendant updates in list order
-    for (int64_t u = __ldg(S.uptr + s); u < __ldg(S.uptr + s + 1); ++u) {
-      const int d = __ldg(S.upd + 3 * u), p0 = __ldg(S.upd + 3 * u + 1), p1 = __ldg(S.upd + 3 * u + 2);
-      const int fd = __ldg(S.sn_first + d);
-      const int wd = __ldg(S.sn_first + d + 1) - fd;
-      const int64_t rbd = __ldg(S.sn_rptr + d);
-      const int nd = static_cast<int>(__ldg(S.sn_rptr + d + 1) - rbd);
-      const int* Rd = S.rows + rbd;
-      const double* Ld = a.L + __ldg(S.sn_loff + d);
-      const double* Dd = a.D + fd;
-      const int ntail = nd - p0;
-      const bool cached = ntail <= kRelCap;
-      if (cached) {
-        for (int p = lane; p < ntail; p += 32) rel[p] = lower_bound_i(Rs, nr, __ldg(Rd + p0 + p));
+  if (tid == 0)
+    for (int q = __ldg(S.cptr + s); q < __ldg(S.cptr + s + 1); ++q) wait_flag(a.flags + __ldg(S.child + q), a.epoch);
+  team_sync<NT>();
+  const int f = __ldg(S.sn_first + s);
+  const int w = __ldg(S.sn_first + s + 1) - f;
+  const int64_t rb = __ldg(S.sn_rptr + s);
+  const int nr = static_cast<int>(__ldg(S.sn_rptr + s + 1) - rb);
+  const int m2 = nr - w;
+  double* P = a.L + __ldg(S.sn_loff + s);
+  double* C = a.CB + __ldg(S.cb_off + s);
+  // 2. clear, scatter A (each panel entry holds at most one A entry)
+  for (int i = tid; i < w * nr; i += NT) P[i] = 0.0;
+  for (int i = tid; i < m2 * m2; i += NT) C[i] = 0.0;
+  team_sync<NT>();
+  for (int64_t e = __ldg(S.aptr + s) + tid; e < __ldg(S.aptr + s + 1); e += NT)
+    P[__ldg(S.aoff + e)] = __ldg(a.kvals + __ldg(S.asrc + e));
+  team_sync<NT>();
+  // 3. extend-add the children's contribution blocks
+  for (int q = __ldg(S.cptr + s); q < __ldg(S.cptr + s + 1); ++q) {
+    const int c = __ldg(S.child + q);
+    const int fc = __ldg(S.sn_first + c);
+    const int wc = __ldg(S.sn_first + c + 1) - fc;
+    const int64_t rbc = __ldg(S.sn_rptr + c);
+    const int m2c = static_cast<int>(__ldg(S.sn_rptr + c + 1) - rbc) - wc;
+    const int* rel = S.relp + rbc + wc;
+    const double* Cc = a.CB + __ldg(S.cb_off + c);
+    for (int j = 0; j < m2c; ++j) {
+      const int rj = __ldg(rel + j);
+      for (int i = j + tid; i < m2c; i += NT) {
+        const int ri = __ldg(rel + i);
+        const double v = __ldcg(Cc + static_cast<int64_t>(j) * m2c + i);
+        if (rj < w) P[static_cast<int64_t>(rj) * nr + ri] += v;
+        else C[static_cast<int64_t>(rj - w) * m2 + (ri - w)] += v;
       }
-      __syncwarp();
-      for (int q = p0; q < p1; ++q) {
-        const int c = __ldg(Rd + q) - f;
-        for (int p = q + lane; p < nd; p += 32) {
-          double acc = 0.0;
-          for (int k = 0; k < wd; ++k) {
-            const double lqk = __ldcg(Ld + static_cast<int64_t>(k) * nd + q);
-            const double dk = __ldcg(Dd + k);
-            acc += __ldcg(Ld + static_cast<int64_t>(k) * nd + p) * (dk * lqk);
-          }
-          const int r = cached ? rel[p - p0] : lower_bound_i(Rs, nr, __ldg(Rd + p));
-          P[static_cast<int64_t>(c) * nr + r] -= acc;
-        }
-      }
-      __syncwarp();
     }
-    // dense LDLᵀ of the panel (right-looking inside the supernode)
+    team_sync<NT>();
+  }
+  // 4. dense LDLᵀ of the w pivot columns (right-looking inside the panel)
+  for (int c = 0; c < w; ++c) {
+    double* Pc = P + static_cast<int64_t>(c) * nr;
+    const double dc = Pc[c];
+    if (tid == 0) {
+      a.D[f + c] = dc;
+      if (fabs(dc) <= thresh) atomicMin(a.zp, f + c);
+    }
+    for (int i = c + 1 + tid; i < nr; i += NT) Pc[i] = Pc[i] / dc;
+    team_sync<NT>();
+    const int rem = w - c - 1;
+    for (int e = tid; e < rem * nr; e += NT) {
+      const int c2 = c + 1 + e / nr, i = e % nr;
+      if (i >= c2) P[static_cast<int64_t>(c2) * nr + i] -= Pc[i] * (dc * Pc[c2]);
+    }
+    team_sync<NT>();
+  }
+  // 5. Schur update of the contribution block: C -= L21 D L21ᵀ (lower)
+  for (int e = tid; e < m2 * m2; e += NT) {
+    const int i = e % m2, j = e / m2;
+    if (i < j) continue;
+    double acc = 0.0;
     for (int c = 0; c < w; ++c) {
-      double* Pc = P + static_cast<int64_t>(c) * nr;
-      const double dc = Pc[c];
-      if (lane == 0) {
-        a.D[f + c] = dc;
-        if (fabs(dc) <= thresh) atomicMin(a.zp, f + c);
-      }
-      for (int i = c + 1 + lane; i < nr; i += 32) Pc[i] = Pc[i] / dc;
-      __syncwarp();
-      for (int c2 = c + 1; c2 < w; ++c2) {
-        const double lc2 = Pc[c2] * dc;
-        double* P2 = P + static_cast<int64_t>(c2) * nr;
-        for (int i = c2 + lane; i < nr; i += 32) P2[i] -= Pc[i] * lc2;
-      }
-      __syncwarp();
+      const double* Pc = P + static_cast<int64_t>(c) * nr;
+      acc += Pc[w + i] * (Pc[c] * Pc[w + j]);
     }
-    __syncwarp();
-    if (lane == 0) {
-      __threadfence();
-      st_release(a.flags + s, a.epoch);
-    }
+    C[e] -= acc;
+  }
+  team_sync<NT>();
+  if (tid == 0) {
+    __threadfence();
+    st_release(a.flags + s, a.epoch);
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT == 32 ? 128 : NT) factor_kernel(FactorArgs a) {
+  __shared__ int s_ticket;
+  const int tid = NT == 32 ? (threadIdx.x & 31) : threadIdx.x;
+  const double thresh = __ldcg(a.thresh);
+  Claim<NT> cl;
+  for (;;) {
+    const int t = cl.next(a.ticket, a.t0, a.t1, a.S.nleaf, tid, &s_ticket);
+    if (t < 0) break;
+    factor_task<NT>(a, __ldg(a.S.order + t), tid, thresh);
   }
 }
 
@@ -213,104 +239,148 @@ __global__ void inertia_kernel(const double* __restrict__ D, int n, const double
 }
 
 // ---------------------------------------------------------------------------
-// Solves: forward (with fused gather permutation), backward (with fused D⁻¹
-// and scatter un-permutation). Same persistent schedule as the factor.
+// Solves (K4), same task order and team split as the factorization.
+// Forward, multifrontal: supernode s gathers b through the permutation
+// (px[k] = b[perm[k]], sparse_sym.cpp:349), extend-adds its children's
+// contribution vectors (CV, rows below their columns), runs the unit-lower
+// triangular solve of its w columns and leaves -L21 x1 in its own CV.
+// Backward, roots first: T_c = sum_{i>=w} L_ic x_{R_i} over ancestor values
+// (parallel over columns), then the w x w unit-upper block, D^{-1} fused,
+// result scattered through the permutation (sparse_sym.cpp:351-362).
 // ---------------------------------------------------------------------------
 struct SolveArgs {
   DevSymb S;
   const double* L;
   const double* D;
+  double* CV;
   double* xp;
   const double* b;
   double* x;
   int* flags;
   int* ticket;
   int epoch;
+  int t0, t1;
 };
 
-__global__ void __launch_bounds__(kWarps * 32) fwd_kernel(SolveArgs a) {
-  const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
+template <int NT>
+__device__ __forceinline__ void fwd_task(const SolveArgs& a, int s, int tid) {
   const DevSymb& S = a.S;
-  TaskCursor tc;
-  for (;;) {
-    const int t = next_task(tc, S.nleaf, S.nsn, a.ticket, lane);
-    if (t < 0) break;
-    const int s = __ldg(S.order + t);
-    if (lane == 0)
-      for (int q = __ldg(S.cptr + s); q < __ldg(S.cptr + s + 1); ++q) wait_flag(a.flags + __ldg(S.child + q), a.epoch);
-    __syncwarp();
-    const int f = __ldg(S.sn_first + s);
-    const int w = __ldg(S.sn_first + s + 1) - f;
-    const int64_t rb = __ldg(S.sn_rptr + s);
-    const int nr = static_cast<int>(__ldg(S.sn_rptr + s + 1) - rb);
-    const double* P = a.L + __ldg(S.sn_loff + s);
-    // gather b through the permutation (px[k] = b[perm[k]], sparse_sym.cpp:349)
-    for (int c = lane; c < w; c += 32) a.xp[f + c] = __ldcg(a.b + __ldg(S.perm + f + c));
-    __syncwarp();
-    for (int64_t u = __ldg(S.uptr + s); u < __ldg(S.uptr + s + 1); ++u) {
-      const int d = __ldg(S.upd + 3 * u), p0 = __ldg(S.upd + 3 * u + 1), p1 = __ldg(S.upd + 3 * u + 2);
-      const int fd = __ldg(S.sn_first + d);
-      const int wd = __ldg(S.sn_first + d + 1) - fd;
-      const int64_t rbd = __ldg(S.sn_rptr + d);
-      const int nd = static_cast<int>(__ldg(S.sn_rptr + d + 1) - rbd);
-      const int* Rd = S.rows + rbd;
-      const double* Ld = a.L + __ldg(S.sn_loff + d);
-      for (int q = p0 + lane; q < p1; q += 32) {
-        double acc = 0.0;
-        for (int k = 0; k < wd; ++k) acc += __ldg(Ld + static_cast<int64_t>(k) * nd + q) * __ldcg(a.xp + fd + k);
-        const int r = __ldg(Rd + q);
-        a.xp[r] -= acc;
-      }
-      __syncwarp();
+  if (tid == 0)
+    for (int q = __ldg(S.cptr + s); q < __ldg(S.cptr + s + 1); ++q) wait_flag(a.flags + __ldg(S.child + q), a.epoch);
+  team_sync<NT>();
+  const int f = __ldg(S.sn_first + s);
+  const int w = __ldg(S.sn_first + s + 1) - f;
+  const int64_t rb = __ldg(S.sn_rptr + s);
+  const int nr = static_cast<int>(__ldg(S.sn_rptr + s + 1) - rb);
+  const double* P = a.L + __ldg(S.sn_loff + s);
+  double* cv = a.CV + rb;
+  double* xs = a.xp + f;
+  for (int k = tid; k < nr; k += NT) {
+    if (k < w) xs[k] = __ldcg(a.b + __ldg(S.perm + f + k));
+    else cv[k] = 0.0;
+  }
+  team_sync<NT>();
+  for (int q = __ldg(S.cptr + s); q < __ldg(S.cptr + s + 1); ++q) {
+    const int c = __ldg(S.child + q);
+    const int wc = __ldg(S.sn_first + c + 1) - __ldg(S.sn_first + c);
+    const int64_t rbc = __ldg(S.sn_rptr + c);
+    const int m2c = static_cast<int>(__ldg(S.sn_rptr + c + 1) - rbc) - wc;
+    for (int k = tid; k < m2c; k += NT) {
+      const int r = __ldg(S.relp + rbc + wc + k);
+      const double v = __ldcg(a.CV + rbc + wc + k);
+      if (r < w) xs[r] += v;
+      else cv[r] += v;
     }
-    // unit-lower diagonal block
-    for (int c = 0; c < w; ++c) {
-      const double xc = a.xp[f + c];
-      for (int c2 = c + 1 + lane; c2 < w; c2 += 32) a.xp[f + c2] -= P[static_cast<int64_t>(c) * nr + c2] * xc;
-      __syncwarp();
+    team_sync<NT>();
+  }
+  for (int c = 0; c < w; ++c) {
+    const double xc = xs[c];
+    const double* Pc = P + static_cast<int64_t>(c) * nr;
+    for (int i = c + 1 + tid; i < nr; i += NT) {
+      const double u = Pc[i] * xc;
+      if (i < w) xs[i] -= u;
+      else cv[i] -= u;
     }
-    if (lane == 0) {
-      __threadfence();
-      st_release(a.flags + s, a.epoch);
-    }
+    team_sync<NT>();
+  }
+  if (tid == 0) {
+    __threadfence();
+    st_release(a.flags + s, a.epoch);
   }
 }
 
-__global__ void __launch_bounds__(kWarps * 32) bwd_kernel(SolveArgs a) {
-  const int lane = threadIdx.x & 31;
+template <int NT>
+__device__ __forceinline__ void bwd_task(const SolveArgs& a, int s, int tid) {
   const DevSymb& S = a.S;
+  const int ps = __ldg(S.sn_parent + s);
+  if (tid == 0 && ps >= 0) wait_flag(a.flags + ps, a.epoch);
+  team_sync<NT>();
+  const int f = __ldg(S.sn_first + s);
+  const int w = __ldg(S.sn_first + s + 1) - f;
+  const int64_t rb = __ldg(S.sn_rptr + s);
+  const int nr = static_cast<int>(__ldg(S.sn_rptr + s + 1) - rb);
+  const int* Rs = S.rows + rb;
+  const double* P = a.L + __ldg(S.sn_loff + s);
+  double* T = a.CV + rb;  // the first w CV slots are free during the backward sweep
+  double* xs = a.xp + f;
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int c = warp; c < w; c += NT / 32) {
+    const double* Pc = P + static_cast<int64_t>(c) * nr;
+    double acc = 0.0;
+    for (int i = w + lane; i < nr; i += 32) acc += Pc[i] * __ldcg(a.xp + __ldg(Rs + i));
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+    if (lane == 0) T[c] = acc;
+  }
+  team_sync<NT>();
+  for (int c = w - 1; c >= 0; --c) {
+    if (tid == 0) {
+      const double v = xs[c] / __ldg(a.D + f + c) - T[c];
+      xs[c] = v;
+      a.x[__ldg(S.perm + f + c)] = v;
+    }
+    team_sync<NT>();
+    const double v = xs[c];
+    for (int c2 = tid; c2 < c; c2 += NT) T[c2] += P[static_cast<int64_t>(c2) * nr + c] * v;
+    team_sync<NT>();
+  }
+  if (tid == 0) {
+    __threadfence();
+    st_release(a.flags + s, a.epoch);
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT == 32 ? 128 : NT) fwd_kernel(SolveArgs a) {
+  __shared__ int s_ticket;
+  const int tid = NT == 32 ? (threadIdx.x & 31) : threadIdx.x;
+  Claim<NT> cl;
   for (;;) {
-    int t = 0;
-    if (lane == 0) t = atomicAdd(a.ticket, 1);
-    t = __shfl_sync(kFull, t, 0);
-    if (t >= S.nsn) break;
-    const int s = __ldg(S.order + (S.nsn - 1 - t));  // roots first
-    const int ps = __ldg(S.sn_parent + s);
-    if (lane == 0 && ps >= 0) wait_flag(a.flags + ps, a.epoch);
-    __syncwarp();
-    const int f = __ldg(S.sn_first + s);
-    const int w = __ldg(S.sn_first + s + 1) - f;
-    const int64_t rb = __ldg(S.sn_rptr + s);
-    const int nr = static_cast<int>(__ldg(S.sn_rptr + s + 1) - rb);
-    const int* Rs = S.rows + rb;
-    const double* P = a.L + __ldg(S.sn_loff + s);
-    for (int c = w - 1; c >= 0; --c) {
-      const double* Pc = P + static_cast<int64_t>(c) * nr;
-      double acc = 0.0;
-      for (int i = c + 1 + lane; i < nr; i += 32) acc += Pc[i] * __ldcg(a.xp + __ldg(Rs + i));
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
-      if (lane == 0) {
-        const double v = a.xp[f + c] / __ldg(a.D + f + c) - acc;
-        a.xp[f + c] = v;
-        a.x[__ldg(S.perm + f + c)] = v;
-      }
-      __syncwarp();
+    const int t = cl.next(a.ticket, a.t0, a.t1, a.S.nleaf, tid, &s_ticket);
+    if (t < 0) break;
+    fwd_task<NT>(a, __ldg(a.S.order + t), tid);
+  }
+}
+
+// tickets in reverse order (roots first); no leaf chunking
+template <int NT>
+__global__ void __launch_bounds__(NT == 32 ? 128 : NT) bwd_kernel(SolveArgs a) {
+  __shared__ int s_ticket;
+  const int tid = NT == 32 ? (threadIdx.x & 31) : threadIdx.x;
+  for (;;) {
+    int t;
+    if constexpr (NT == 32) {
+      t = 0;
+      if (tid == 0) t = atomicAdd(a.ticket, 1);
+      t = __shfl_sync(kFull, t, 0);
+    } else {
+      __syncthreads();
+      if (tid == 0) s_ticket = atomicAdd(a.ticket, 1);
+      __syncthreads();
+      t = s_ticket;
     }
-    if (lane == 0) {
-      __threadfence();
-      st_release(a.flags + s, a.epoch);
-    }
+    const int k = a.t1 - 1 - t;
+    if (k < a.t0) break;
+    bwd_task<NT>(a, __ldg(a.S.order + k), tid);
   }
 }
 
@@ -399,12 +469,6 @@ int num_sms() {
   return g_num_sms;
 }
 
-int persistent_grid(const void* fn) {
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kWarps * 32, 0);
-  if (per_sm <= 0) per_sm = 1;
-  return num_sms() * per_sm;
-}
 
 int grid_for(int64_t n, int block) {
   const int64_t g = (n + block - 1) / block;
@@ -421,6 +485,15 @@ void dev_max_abs_diag(const DevPattern& P, const double* kvals, double* out, cud
   if (P.ndiag > 0) COUNT(1), maxdiag_kernel<<<grid_for(P.ndiag, 256), 256, 0, st>>>(P.diag_pos, P.ndiag, kvals, out);
 }
 
+template <class K>
+int persistent_grid(K fn, int threads, int ntasks) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0);
+  if (per_sm <= 0) per_sm = 1;
+  const int g = num_sms() * per_sm;
+  return std::max(1, std::min(g, ntasks));
+}
+
 void dev_factor(const DevSymb& S0, const DevPattern& P, DevFactor& F, const double* kvals, double pivot_tol,
                 cudaStream_t st) {
   DevSymb& S = const_cast<DevSymb&>(S0);
@@ -429,10 +502,22 @@ void dev_factor(const DevSymb& S0, const DevPattern& P, DevFactor& F, const doub
   thresh_kernel<<<1, 1, 0, st>>>(F.scal, pivot_tol, F.istat, S.n);
   S.epoch++;
   cudaMemsetAsync(S.tickets, 0, 4 * sizeof(int), st);
-  FactorArgs a{S, F.L, F.D, kvals, F.scal, F.istat, S.flags, S.tickets + 0, S.epoch};
-  static int grid = 0;
-  if (!grid) grid = persistent_grid(reinterpret_cast<const void*>(factor_kernel));
-  if (S.nsn > 0) COUNT(1), factor_kernel<<<grid, kWarps * 32, 0, st>>>(a);
+  FactorArgs a{S, F.L, F.CB, F.D, kvals, F.scal, F.istat, S.flags, S.tickets + 0, S.epoch, 0, S.nsplit};
+  if (S.nsplit > 0) {
+    static int g = 0;
+    if (!g) g = persistent_grid(factor_kernel<32>, 128, 1 << 30);
+    COUNT(1);
+    factor_kernel<32><<<g, 128, 0, st>>>(a);
+  }
+  if (S.nsplit < S.nsn) {
+    static int g2 = 0;
+    if (!g2) g2 = persistent_grid(factor_kernel<256>, 256, 1 << 30);
+    a.ticket = S.tickets + 1;
+    a.t0 = S.nsplit;
+    a.t1 = S.nsn;
+    COUNT(1);
+    factor_kernel<256><<<std::min(g2, S.nsn - S.nsplit), 256, 0, st>>>(a);
+  }
 }
 
 void dev_inertia(const DevSymb& S, DevFactor& F, cudaStream_t st) {
@@ -444,15 +529,33 @@ void dev_solve(const DevSymb& S0, DevFactor& F, const double* b, double* x, cuda
   DevSymb& S = const_cast<DevSymb&>(S0);
   if (S.n == 0) return;
   S.epoch++;
-  cudaMemsetAsync(S.tickets + 1, 0, 2 * sizeof(int), st);
-  static int gf = 0, gb = 0;
-  if (!gf) gf = persistent_grid(reinterpret_cast<const void*>(fwd_kernel));
-  if (!gb) gb = persistent_grid(reinterpret_cast<const void*>(bwd_kernel));
-  SolveArgs a{S, F.L, F.D, F.xp, b, x, S.flags + S.nsn, S.tickets + 1, S.epoch};
-  COUNT(2);
-  fwd_kernel<<<gf, kWarps * 32, 0, st>>>(a);
-  SolveArgs bb{S, F.L, F.D, F.xp, b, x, S.flags + 2 * S.nsn, S.tickets + 2, S.epoch};
-  bwd_kernel<<<gb, kWarps * 32, 0, st>>>(bb);
+  cudaMemsetAsync(S.tickets, 0, 4 * sizeof(int), st);
+  static int gf = 0, gf2 = 0, gb = 0, gb2 = 0;
+  if (!gf) {
+    gf = persistent_grid(fwd_kernel<32>, 128, 1 << 30);
+    gf2 = persistent_grid(fwd_kernel<256>, 256, 1 << 30);
+    gb = persistent_grid(bwd_kernel<32>, 128, 1 << 30);
+    gb2 = persistent_grid(bwd_kernel<256>, 256, 1 << 30);
+  }
+  const int ntop = S.nsn - S.nsplit;
+  SolveArgs fa{S, F.L, F.D, F.CV, F.xp, b, x, S.flags + S.nsn, S.tickets + 0, S.epoch, 0, S.nsplit};
+  if (S.nsplit > 0) COUNT(1), fwd_kernel<32><<<gf, 128, 0, st>>>(fa);
+  if (ntop > 0) {
+    fa.ticket = S.tickets + 1;
+    fa.t0 = S.nsplit;
+    fa.t1 = S.nsn;
+    COUNT(1);
+    fwd_kernel<256><<<std::min(gf2, ntop), 256, 0, st>>>(fa);
+  }
+  SolveArgs ba{S, F.L, F.D, F.CV, F.xp, b, x, S.flags + 2 * S.nsn, S.tickets + 2, S.epoch, S.nsplit, S.nsn};
+  if (ntop > 0) COUNT(1), bwd_kernel<256><<<std::min(gb2, ntop), 256, 0, st>>>(ba);
+  if (S.nsplit > 0) {
+    ba.ticket = S.tickets + 3;
+    ba.t0 = 0;
+    ba.t1 = S.nsplit;
+    COUNT(1);
+    bwd_kernel<32><<<gb, 128, 0, st>>>(ba);
+  }
 }
 
 void dev_spmv(const DevPattern& P, const double* kvals, const double* x, double* y, cudaStream_t st) {

@@ -249,19 +249,82 @@ SymbolicCore analyze_core(int n, const std::vector<int>& cp, const std::vector<i
 }
 
 // --- supernodal schedule (product-only) -------------------------------------
+// True column structure of L (reference layout): row k of L is the etree reach
+// of A's row k (the same row-subtree walk as the colcounts above,
+// sparse_sym.cpp:241-258); transposed into columns with rows ascending.
+void true_L_structure(const SymbolicCore& S, std::vector<int64_t>& lp, std::vector<int>& li) {
+  const int n = S.n;
+  lp.assign(n + 1, 0);
+  for (int j = 0; j < n; ++j) lp[j + 1] = lp[j] + S.l_colcount[j];
+  li.resize(lp[n]);
+  std::vector<int64_t> fp(lp.begin(), lp.end() - 1);
+  std::vector<int> flag(n, -1);
+  for (int k = 0; k < n; ++k) {
+    flag[k] = k;
+    for (int p = S.up_colptr[k]; p < S.up_colptr[k + 1]; ++p) {
+      int i = S.up_rowind[p];
+      while (i < k && flag[i] != k) {
+        li[fp[i]++] = k;  // k ascending: rows sorted inside every column
+        flag[i] = k;
+        i = S.parent[i];
+      }
+    }
+  }
+}
+
 Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
-                            const std::vector<int>& ri, int /*relax_small*/) {
+                            const std::vector<int>& ri, int relax) {
   const int n = S.n;
   Supernodal Z;
-  // 1. partition: j+1 joins j's supernode iff parent[j]==j+1 and
-  //    colcount[j]==colcount[j+1]+1 (nested structure, identical rows).
-  Z.sn_first.push_back(0);
+  // 1a. fundamental partition: j+1 joins j's supernode iff parent[j]==j+1 and
+  //     colcount[j]==colcount[j+1]+1 (nested structure, identical rows).
+  std::vector<int> fund{0};
   for (int j = 0; j + 1 < n; ++j) {
     const bool join = S.parent[j] == j + 1 && S.l_colcount[j] == S.l_colcount[j + 1] + 1;
-    if (!join) Z.sn_first.push_back(j + 1);
+    if (!join) fund.push_back(j + 1);
   }
-  if (n > 0) Z.sn_first.push_back(n);
-  else Z.sn_first.assign(1, 0);
+  if (n > 0) fund.push_back(n);
+  else fund.assign(1, 0);
+  // 1b. relaxed amalgamation (CHOLMOD-style thresholds): a run of fundamental
+  //     supernodes is merged into the next one when that one is its etree
+  //     parent AND is adjacent in the (fixed, reference) column order, and the
+  //     explicit zeros introduced stay small. Structurally-zero entries of a
+  //     merged panel stay exactly 0.0 through the factorization, so D, the
+  //     solution and the true-structure entries of L are unaffected up to
+  //     summation order; perm/etree/colcounts are untouched.
+  Z.sn_first.push_back(0);
+  if (n > 0) {
+    const int nf = static_cast<int>(fund.size()) - 1;
+    auto true_nnz = [&](int a, int b) {  // columns [a, b)
+      int64_t t = 0;
+      for (int j = a; j < b; ++j) t += S.l_colcount[j] + 1;
+      return t;
+    };
+    int g0 = 0;                                  // first column of the open group
+    int64_t gtrue = true_nnz(fund[0], fund[1]);  // true entries of the group
+    for (int t = 0; t + 1 < nf; ++t) {
+      const int l = fund[t + 1];                 // group ends at l
+      const int W = l - g0;
+      bool merge = false;
+      if (relax && S.parent[l - 1] == l) {       // next fundamental sn is the parent, adjacent
+        const int wp = fund[t + 2] - l;
+        const int64_t nrp = S.l_colcount[l] + 1;  // rows of the parent panel (incl. its columns)
+        const int64_t Wm = W + wp;
+        const int64_t nrm = W + nrp;
+        const int64_t dense = Wm * nrm - Wm * (Wm - 1) / 2;
+        const int64_t tru = gtrue + true_nnz(l, fund[t + 2]);
+        const double z = dense > 0 ? static_cast<double>(dense - tru) / static_cast<double>(dense) : 0.0;
+        merge = Wm <= 256 && (Wm <= 4 || (Wm <= 16 && z < 0.8) || (Wm <= 48 && z < 0.1) || z < 0.05);
+        if (merge) gtrue = tru;
+      }
+      if (!merge) {
+        Z.sn_first.push_back(l);
+        g0 = l;
+        gtrue = true_nnz(l, fund[t + 2]);
+      }
+    }
+    Z.sn_first.push_back(n);
+  }
   Z.nsn = static_cast<int>(Z.sn_first.size()) - 1;
   const int nsn = Z.nsn;
   Z.sn_of_col.assign(n, -1);
@@ -272,7 +335,7 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
     const int last = Z.sn_first[s + 1] - 1;
     if (S.parent[last] >= 0) Z.sn_parent[s] = Z.sn_of_col[S.parent[last]];
   }
-  // children CSR
+  // children CSR (ascending child index = ascending columns)
   Z.cptr.assign(nsn + 1, 0);
   for (int s = 0; s < nsn; ++s)
     if (Z.sn_parent[s] >= 0) Z.cptr[Z.sn_parent[s] + 1]++;
@@ -283,8 +346,7 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
     for (int s = 0; s < nsn; ++s)
       if (Z.sn_parent[s] >= 0) Z.child[fp[Z.sn_parent[s]]++] = s;
   }
-  // 2. lower structure of A (permuted): column j holds rows i>j. Transpose
-  //    of the permuted upper CSC.
+  // 2. lower structure of A (permuted): column j holds rows i>j.
   std::vector<int> lcp(n + 1, 0), lri;
   for (int c = 0; c < n; ++c)
     for (int p = S.up_colptr[c]; p < S.up_colptr[c + 1]; ++p)
@@ -295,17 +357,17 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
     std::vector<int> fp(lcp.begin(), lcp.end() - 1);
     for (int c = 0; c < n; ++c)
       for (int p = S.up_colptr[c]; p < S.up_colptr[c + 1]; ++p)
-        if (S.up_rowind[p] < c) lri[fp[S.up_rowind[p]]++] = c;  // ascending c
+        if (S.up_rowind[p] < c) lri[fp[S.up_rowind[p]]++] = c;
   }
-  // 3. row structures, children before parents (supernodes are numbered in
-  //    column order and a parent's columns follow its children's).
+  // 3. row structures R_s = cols(s) ∪ (A rows ∪ children's rows below s),
+  //    children before parents.
   Z.sn_rptr.assign(nsn + 1, 0);
   std::vector<std::vector<int>> R(nsn);
   std::vector<int> mark(n, -1), buf;
   for (int s = 0; s < nsn; ++s) {
     const int f = Z.sn_first[s], l = Z.sn_first[s + 1];
     buf.clear();
-    for (int j = f; j < l; ++j) {
+    for (int j = f; j < l; ++j)
       for (int p = lcp[j]; p < lcp[j + 1]; ++p) {
         const int r = lri[p];
         if (r >= l && mark[r] != s) {
@@ -313,75 +375,58 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
           buf.push_back(r);
         }
       }
-    }
-    for (int q = Z.cptr[s]; q < Z.cptr[s + 1]; ++q) {
-      const int c = Z.child[q];
-      for (int r : R[c])
+    for (int q = Z.cptr[s]; q < Z.cptr[s + 1]; ++q)
+      for (int r : R[Z.child[q]])
         if (r >= l && mark[r] != s) {
           mark[r] = s;
           buf.push_back(r);
         }
-      // child's structure is no longer needed once merged into its parent
-    }
     std::sort(buf.begin(), buf.end());
     R[s].reserve(l - f + buf.size());
     for (int j = f; j < l; ++j) R[s].push_back(j);
     R[s].insert(R[s].end(), buf.begin(), buf.end());
-    for (int q = Z.cptr[s]; q < Z.cptr[s + 1]; ++q) {
-      // keep child rows: the update lists below need them; freed later
-    }
   }
-  // verify against the reference column counts (fill pattern identity)
+  // structure check against the reference column counts: exact for
+  // fundamental columns, a superset inside amalgamated panels
   for (int s = 0; s < nsn; ++s) {
     const int f = Z.sn_first[s], l = Z.sn_first[s + 1];
     const int nr = static_cast<int>(R[s].size());
-    for (int j = f; j < l; ++j)
-      if (S.l_colcount[j] != nr - (j - f) - 1) fail(NCL_E_INTERNAL, "supernode structure disagrees with l_colcount");
+    for (int j = f; j < l; ++j) {
+      const int have = nr - (j - f) - 1;
+      if (relax ? have < S.l_colcount[j] : have != S.l_colcount[j])
+        fail(NCL_E_INTERNAL, "supernode structure disagrees with l_colcount");
+    }
   }
   for (int s = 0; s < nsn; ++s) Z.sn_rptr[s + 1] = Z.sn_rptr[s] + static_cast<int64_t>(R[s].size());
   Z.rows.resize(Z.sn_rptr[nsn]);
   for (int s = 0; s < nsn; ++s) std::copy(R[s].begin(), R[s].end(), Z.rows.begin() + Z.sn_rptr[s]);
+  // panels (nr x w, column-major) and contribution blocks (m2 x m2, m2 = nr - w)
   Z.sn_loff.assign(nsn + 1, 0);
+  Z.cb_off.assign(nsn + 1, 0);
   for (int s = 0; s < nsn; ++s) {
     const int64_t w = Z.sn_first[s + 1] - Z.sn_first[s];
     const int64_t nr = static_cast<int64_t>(R[s].size());
     Z.sn_loff[s + 1] = Z.sn_loff[s] + w * nr;
+    Z.cb_off[s + 1] = Z.cb_off[s] + (nr - w) * (nr - w);
     Z.max_w = std::max<int>(Z.max_w, static_cast<int>(w));
     Z.max_nr = std::max<int>(Z.max_nr, static_cast<int>(nr));
   }
   Z.l_storage = Z.sn_loff[nsn];
-  // 4. update lists (d ascending inside every target list)
-  Z.uptr.assign(nsn + 1, 0);
-  for (int d = 0; d < nsn; ++d) {
-    const int w = Z.sn_first[d + 1] - Z.sn_first[d];
-    const auto& Rd = R[d];
-    int prev = -1;
-    for (size_t i = w; i < Rd.size(); ++i) {
-      const int t = Z.sn_of_col[Rd[i]];
-      if (t != prev) {
-        Z.uptr[t + 1]++;
-        prev = t;
-      }
-    }
-  }
-  for (int s = 0; s < nsn; ++s) Z.uptr[s + 1] += Z.uptr[s];
-  Z.upd.resize(3 * Z.uptr[nsn]);
-  {
-    std::vector<int64_t> fp(Z.uptr.begin(), Z.uptr.end() - 1);
-    for (int d = 0; d < nsn; ++d) {
-      const int w = Z.sn_first[d + 1] - Z.sn_first[d];
-      const auto& Rd = R[d];
-      size_t i = w;
-      while (i < Rd.size()) {
-        const int t = Z.sn_of_col[Rd[i]];
-        size_t e = i;
-        while (e < Rd.size() && Z.sn_of_col[Rd[e]] == t) ++e;
-        const int64_t q = fp[t]++;
-        Z.upd[3 * q] = d;
-        Z.upd[3 * q + 1] = static_cast<int>(i);
-        Z.upd[3 * q + 2] = static_cast<int>(e);
-        i = e;
-      }
+  Z.cb_storage = Z.cb_off[nsn];
+  // 4. relative positions of every child row below the child's columns in
+  //    its parent's row list (extend-add maps of the multifrontal scheme)
+  Z.relp.assign(Z.rows.size(), -1);
+  for (int c = 0; c < nsn; ++c) {
+    const int p = Z.sn_parent[c];
+    if (p < 0) continue;
+    const int wc = Z.sn_first[c + 1] - Z.sn_first[c];
+    const auto& Rp = R[p];
+    size_t q = 0;
+    for (size_t k = wc; k < R[c].size(); ++k) {
+      const int r = R[c][k];
+      while (Rp[q] < r) ++q;  // both ascending
+      if (Rp[q] != r) fail(NCL_E_INTERNAL, "child row missing from parent structure");
+      Z.relp[Z.sn_rptr[c] + k] = static_cast<int>(q);
     }
   }
   // 5. heights and ticket order (leaves first)
@@ -391,12 +436,22 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
   Z.max_height = 0;
   for (int s = 0; s < nsn; ++s) Z.max_height = std::max(Z.max_height, Z.height[s]);
   Z.order.resize(nsn);
+  std::vector<int> hc(Z.max_height + 2, 0);
+  for (int s = 0; s < nsn; ++s) hc[Z.height[s] + 1]++;
+  for (int h = 0; h <= Z.max_height; ++h) hc[h + 1] += hc[h];
   {
-    std::vector<int> hc(Z.max_height + 2, 0);
-    for (int s = 0; s < nsn; ++s) hc[Z.height[s] + 1]++;
-    for (int h = 0; h <= Z.max_height; ++h) hc[h + 1] += hc[h];
-    for (int s = 0; s < nsn; ++s) Z.order[hc[Z.height[s]]++] = s;
+    std::vector<int> fp(hc.begin(), hc.end() - 1);
+    for (int s = 0; s < nsn; ++s) Z.order[fp[Z.height[s]]++] = s;
   }
+  // phase split: the narrow top of the tree (at most kTopTasks supernodes)
+  // runs with a whole CTA per supernode, everything below with a warp each.
+  constexpr int kTopTasks = 2048;
+  Z.nsplit = nsn;
+  for (int h = Z.max_height; h >= 0; --h) {
+    if (nsn - hc[h] > kTopTasks) break;
+    Z.nsplit = hc[h];
+  }
+  Z.nleaf = hc[1] - hc[0];
   // 6. A -> panel map, diagonal positions
   const int nnz = cp[n];
   Z.amap.resize(nnz);

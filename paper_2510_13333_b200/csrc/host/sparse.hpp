@@ -92,17 +92,16 @@ struct Supernodal {
   std::vector<int> sn_parent;  // [nsn] parent supernode or -1
   std::vector<int64_t> sn_rptr;  // [nsn+1] offsets into rows
   std::vector<int> rows;         // row structure R_s (permuted, ascending; starts with the s columns)
+  std::vector<int> relp;         // [rows] position of a child row (k >= w) in the parent's R
   std::vector<int64_t> sn_loff;  // [nsn+1] offsets of dense column-major panels (nr x w)
-  int64_t l_storage = 0;
-  // update lists: for target s, entries [uptr[s], uptr[s+1]) of (d, p0, p1)
-  std::vector<int64_t> uptr;
-  std::vector<int> upd;  // triples
+  std::vector<int64_t> cb_off;   // [nsn+1] offsets of contribution blocks ((nr-w)^2)
+  int64_t l_storage = 0, cb_storage = 0;
   // children lists (supernode etree)
   std::vector<int> cptr, child;
-  // ticket order (leaves first by height) and heights
+  // ticket order (leaves first by height), heights, phase split, leaf count
   std::vector<int> order;
   std::vector<int> height;
-  int max_height = 0;
+  int max_height = 0, nsplit = 0, nleaf = 0;
   // A -> panel offsets for every entry of the source lower CSC
   std::vector<int64_t> amap;
   // diagonal entry positions of the source CSC (for max|diag|)
@@ -111,7 +110,12 @@ struct Supernodal {
   double flops = 0.0;  // sum_j (c_j^2 + 2 c_j) over reference column counts
 };
 
+// relax = 1: CHOLMOD-style relaxed amalgamation of adjacent parent/child
+// supernodes (does not change perm, etree or the reference fill pattern).
 Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& colptr,
-                            const std::vector<int>& rowind, int relax_small = 0);
+                            const std::vector<int>& rowind, int relax = 1);
+
+// True column structure of L in the reference layout (lp[n+1], li[l_nnz]).
+void true_L_structure(const SymbolicCore& S, std::vector<int64_t>& lp, std::vector<int>& li);
 
 }  // namespace nclb

@@ -153,6 +153,8 @@ class SymbolicInfo:
     max_rows: int
     l_storage: int
     flops: float
+    cb_storage: int = 0
+    nsplit: int = 0
 
 
 class SymbolicFactor:
@@ -203,7 +205,7 @@ class SymbolicFactor:
         s = SymbInfo()
         check(lib.ncl_symb_info_get(self._h, C.byref(s)))
         return SymbolicInfo(s.n, s.l_nnz, s.nsupernodes, s.max_height, s.max_width, s.max_rows, s.l_storage,
-                            s.flops)
+                            s.flops, s.cb_storage, s.nsplit)
 
 
 def analyze(M: SparseSym, perm=None) -> SymbolicFactor:

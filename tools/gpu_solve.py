@@ -1,0 +1,20 @@
+"""GPU NCL/IPM solve of one SCOPF config vs (optionally) the CPU oracle."""
+import json, sys, time
+sys.path.insert(0, __file__.rsplit('/tools/', 1)[0])
+from paper_2510_13333_b200 import _lib
+from paper_2510_13333_b200.scopf import Scopf
+from paper_2510_13333_b200.ipm import NclSolver, default_options
+grid, K = sys.argv[1], int(sys.argv[2])
+_lib.check(_lib.lib.ncl_init(0))
+t0 = time.time(); s = Scopf(grid, K); M = s.build_model(); S = NclSolver(M, s.bounds()); t_build = time.time() - t0
+out = S.solve(default_options())
+r = out.result
+print(json.dumps({"grid": grid, "K": K, "n": s.n, "m": s.m, "status": out.status, "build_s": t_build,
+                  **{k: r[k] for k in ["outer_iters", "inner_iters", "factorizations", "objective", "r_inf", "inf_pr",
+                                       "inf_du", "t_total", "t_init", "t_eval", "t_factor", "t_solve", "t_linesearch", "t_other"]}}))
+if len(sys.argv) > 3:
+    from oracle.ref import RefModel, ref_ncl_solve
+    R = RefModel.from_families(s.n, s.m, s.families())
+    t0 = time.time(); ref = ref_ncl_solve(R, s.bounds()); rr = ref["result"]
+    print(json.dumps({"oracle": True, "status": ref["status"], "wall": time.time() - t0,
+                      **{k: rr[k] for k in ["outer_iters", "inner_iters", "factorizations", "objective", "r_inf", "t_factor", "t_solve", "t_eval"]}}))
