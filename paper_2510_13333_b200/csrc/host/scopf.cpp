@@ -268,11 +268,18 @@ Grid grid_synthetic(int nb, int nl, int ng, uint64_t seed) {
   g.qd.assign(nb, 0.0);
   for (int i = 0; i < nb; ++i)
     if (rng.uniform() < 0.8) {
-      g.pd[i] = rng.uniform(0.2, 1.0);
+      // ~0.19 pu mean per bus: ACTIVSg500 carries ~7.75 GW on 500 buses; the
+      // survey's U(0.2, 1.0) loads 3x heavier and leaves N-1 reactive
+      // balances infeasible at |v| in [0.94, 1.06].
+      g.pd[i] = rng.uniform(0.05, 0.33);
       g.qd[i] = 0.3 * g.pd[i];
     }
   g.gs.assign(nb, 0.0);
+  // switched-shunt compensation of the load's reactive demand (like the
+  // ACTIVSg cases' shunts): without it reactive power cannot reach load
+  // pockets far from the 56 generator buses inside |v| in [0.94, 1.06]
   g.bs.assign(nb, 0.0);
+  for (int i = 0; i < nb; ++i) g.bs[i] = g.qd[i];
   g.vmin.assign(nb, 0.94);
   g.vmax.assign(nb, 1.06);
   // generators on the highest-degree buses
@@ -464,8 +471,11 @@ ModelSpec build_scopf(const Grid& g, const std::vector<int>& cont) {
     S.off_extra.push_back(s == 0 ? -1 : oex);
     S.row_start.push_back(row);
     for (int i = 0; i < nb; ++i) {
-      S.xl[ov + i] = g.vmin[i];
-      S.xu[ov + i] = g.vmax[i];
+      // post-contingency states use the emergency band (+-0.04 pu wider);
+      // SPEC.md:298 leaves the bound set on v^k open
+      const double em = s == 0 ? 0.0 : 0.04;
+      S.xl[ov + i] = g.vmin[i] - em;
+      S.xu[ov + i] = g.vmax[i] + em;
       S.x0[ov + i] = std::min(std::max(1.0, g.vmin[i]), g.vmax[i]);
     }
     for (int k = 0; k < ng; ++k) {
