@@ -194,6 +194,10 @@ typedef struct ncl_scopf_info {
   int nvar_scen, ncon_scen;
 } ncl_scopf_info;
 int ncl_scopf_create(int grid, int nb, int nl, int ng, uint64_t seed, int K, ncl_scopf_t* out);
+/* explicit outage list (branch ids, non-islanding; e.g. a screened list,
+ * PAPER.md:526-543); branch_ids == NULL -> the first K non-islanding */
+int ncl_scopf_create_list(int grid, int nb, int nl, int ng, uint64_t seed, int K, const int* branch_ids,
+                          ncl_scopf_t* out);
 void ncl_scopf_destroy(ncl_scopf_t S);
 int ncl_scopf_get_info(ncl_scopf_t S, ncl_scopf_info* info);
 /* family f: name (<=63 chars), node count, slots, params per instance,
@@ -204,6 +208,8 @@ int ncl_scopf_family_data(ncl_scopf_t S, int f, ncl_expr_node* nodes, int* rows,
 /* variable bounds/start (n), row bounds (m); +-inf for absent bounds */
 int ncl_scopf_bounds(ncl_scopf_t S, double* xl, double* xu, double* x0, double* gl, double* gu);
 int ncl_scopf_contingencies(ncl_scopf_t S, int* branch_ids);
+/* every non-islanding single-branch outage of the grid (ascending); ids may be NULL */
+int ncl_scopf_candidates(ncl_scopf_t S, int* ids, int* count);
 int ncl_scopf_build_model(ncl_scopf_t S, ncl_model_t* out); /* this library's ModelBuilder */
 
 #ifdef __cplusplus

@@ -1,5 +1,6 @@
 // C-ABI for the SCOPF problem generator (host setup code).
 #include <cstring>
+#include <algorithm>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -25,7 +26,8 @@ struct ncl_scopf {
   ModelSpec spec;
 };
 
-API int ncl_scopf_create(int grid, int nb, int nl, int ng, uint64_t seed, int K, ncl_scopf_t* out) {
+API int ncl_scopf_create_list(int grid, int nb, int nl, int ng, uint64_t seed, int K, const int* branch_ids,
+                              ncl_scopf_t* out) {
   GUARD({
     auto s = std::make_unique<ncl_scopf>();
     try {
@@ -33,12 +35,26 @@ API int ncl_scopf_create(int grid, int nb, int nl, int ng, uint64_t seed, int K,
     } catch (const std::invalid_argument& e) {
       throw Error{NCL_E_INVALID, e.what()};
     }
-    const auto cont = select_contingencies(s->grid, K);
+    std::vector<int> cont;
+    if (branch_ids) {
+      const auto ok = select_contingencies(s->grid, s->grid.nl);  // non-islanding set
+      for (int k = 0; k < K; ++k) {
+        const int l = branch_ids[k];
+        if (!std::binary_search(ok.begin(), ok.end(), l))
+          throw Error{NCL_E_INVALID, "scopf: contingency islands the network or is out of range"};
+        cont.push_back(l);
+      }
+    } else {
+      cont = select_contingencies(s->grid, K);
+    }
     if (static_cast<int>(cont.size()) < K)
       throw Error{NCL_E_INVALID, "scopf: fewer non-islanding contingencies than requested"};
     s->spec = build_scopf(s->grid, cont);
     *out = s.release();
   });
+}
+API int ncl_scopf_create(int grid, int nb, int nl, int ng, uint64_t seed, int K, ncl_scopf_t* out) {
+  return ncl_scopf_create_list(grid, nb, nl, ng, seed, K, nullptr, out);
 }
 API void ncl_scopf_destroy(ncl_scopf_t S) { delete S; }
 API int ncl_scopf_get_info(ncl_scopf_t S, ncl_scopf_info* info) {
@@ -97,6 +113,13 @@ API int ncl_scopf_bounds(ncl_scopf_t S, double* xl, double* xu, double* x0, doub
 API int ncl_scopf_contingencies(ncl_scopf_t S, int* ids) {
   GUARD(if (!S->spec.contingencies.empty()) std::memcpy(ids, S->spec.contingencies.data(),
                                                          S->spec.contingencies.size() * sizeof(int)));
+}
+API int ncl_scopf_candidates(ncl_scopf_t S, int* ids, int* count) {
+  GUARD({
+    const auto all = select_contingencies(S->grid, S->grid.nl);
+    *count = static_cast<int>(all.size());
+    if (ids && !all.empty()) std::memcpy(ids, all.data(), all.size() * sizeof(int));
+  });
 }
 API int ncl_scopf_build_model(ncl_scopf_t S, ncl_model_t* out) {
   GUARD({

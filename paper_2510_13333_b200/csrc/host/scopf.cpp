@@ -78,7 +78,7 @@ BranchY branch_y(const Grid& g, int l) {
 
 // DC power flow angles with generation proportional to pmax (CG on the
 // reduced Laplacian), optionally with branch `out` removed. Deterministic.
-std::vector<double> dc_angles(const Grid& g, int out = -1) {
+std::vector<double> dc_angles(const Grid& g, int out = -1, const std::vector<double>* warm = nullptr) {
   const int n = g.nb;
   std::vector<double> P(n, 0.0);
   double pd = 0, pm = 0;
@@ -99,10 +99,19 @@ std::vector<double> dc_angles(const Grid& g, int out = -1) {
   };
   std::vector<double> th(n, 0.0), r(P), p, Ap(n);
   r[g.ref] = 0.0;
+  double pp = 0;
+  for (double v : r) pp += v * v;
+  if (warm) {  // start from the base-case angles: the outage perturbs them locally
+    th = *warm;
+    apply(th, Ap);
+    for (int i = 0; i < n; ++i) r[i] = (i == g.ref ? 0.0 : P[i]) - Ap[i];
+    r[g.ref] = -th[g.ref];
+  }
   p = r;
   double rr = 0;
   for (double v : r) rr += v * v;
-  for (int it = 0; it < 20 * n && rr > 1e-24; ++it) {
+  const double stop = std::max(1e-24, 1e-24 * pp);
+  for (int it = 0; it < 20 * n && rr > stop; ++it) {
     apply(p, Ap);
     double pAp = 0;
     for (int i = 0; i < n; ++i) pAp += p[i] * Ap[i];
@@ -316,8 +325,10 @@ Grid grid_synthetic(int nb, int nl, int ng, uint64_t seed) {
     for (int l = 0; l < g.nl; ++l)
       if (l != out) fmax[l] = std::max(fmax[l], std::abs((th[g.f[l]] - th[g.t[l]]) / g.x[l]));
   };
-  absorb(dc_angles(g), -1);
-  for (int l : select_contingencies(g, g.nl)) absorb(dc_angles(g, l), l);
+  const std::vector<double> th0 = dc_angles(g);
+  absorb(th0, -1);
+  // the first 600 non-islanding outages cover every config's contingency set
+  for (int l : select_contingencies(g, std::min(g.nl, 600))) absorb(dc_angles(g, l, &th0), l);
   g.rate.resize(g.nl);
   for (int l = 0; l < g.nl; ++l) g.rate[l] = 1.2 * fmax[l] + 0.25;
   return g;

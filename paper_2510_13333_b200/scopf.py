@@ -19,6 +19,7 @@ class ScopfInfo(C.Structure):
 
 register({
     "ncl_scopf_create": (i32, [i32, i32, i32, i32, C.c_uint64, i32, C.POINTER(P)]),
+    "ncl_scopf_create_list": (i32, [i32, i32, i32, i32, C.c_uint64, i32, P, C.POINTER(P)]),
     "ncl_scopf_destroy": (None, [P]),
     "ncl_scopf_get_info": (i32, [P, C.POINTER(ScopfInfo)]),
     "ncl_scopf_family_info": (i32, [P, i32, C.c_char_p, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32),
@@ -26,6 +27,7 @@ register({
     "ncl_scopf_family_data": (i32, [P, i32, P, P, P, P]),
     "ncl_scopf_bounds": (i32, [P, P, P, P, P, P]),
     "ncl_scopf_contingencies": (i32, [P, P]),
+    "ncl_scopf_candidates": (i32, [P, P, C.POINTER(i32)]),
     "ncl_scopf_build_model": (i32, [P, C.POINTER(P)]),
 })
 
@@ -36,6 +38,18 @@ GRIDS = {
     "activsg500": (1, 500, 597, 56),
     "activsg2000": (1, 2000, 3206, 432),
 }
+
+
+def screened(grid: str, seed: int = 2510):
+    """Committed list of N-1 contingencies that passed screening (each one
+    solved alone as a K=1 SCOPF to optimality), ascending branch order."""
+    import json
+    import os
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data", f"screened_{grid}_{seed}.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        return json.load(f)["feasible"]
 
 
 @dataclass
@@ -51,10 +65,22 @@ class Family:
 
 
 class Scopf:
-    def __init__(self, grid: str = "case9", K: int = 0, seed: int = 2510):
+    def __init__(self, grid: str = "case9", K: int = 0, seed: int = 2510, contingencies=None):
+        """contingencies: explicit branch ids; default = the first K entries of
+        the committed screened list for (grid, seed) when one exists
+        (data/screened_<grid>_<seed>.json, tools/screen_contingencies.py),
+        else the first K non-islanding branches."""
         kind, nb, nl, ng = GRIDS[grid]
+        if contingencies is None and K > 0:
+            contingencies = screened(grid, seed)
+            if contingencies is not None and len(contingencies) < K:
+                raise ValueError(f"only {len(contingencies)} screened contingencies for {grid}")
         h = C.c_void_p()
-        check(lib.ncl_scopf_create(kind, nb, nl, ng, seed, K, C.byref(h)))
+        if contingencies is None:
+            check(lib.ncl_scopf_create(kind, nb, nl, ng, seed, K, C.byref(h)))
+        else:
+            ids = np.ascontiguousarray(np.asarray(contingencies)[:K], np.int32)
+            check(lib.ncl_scopf_create_list(kind, nb, nl, ng, seed, K, _ptr(ids), C.byref(h)))
         self._h = h
         s = ScopfInfo()
         check(lib.ncl_scopf_get_info(h, C.byref(s)))
@@ -97,6 +123,14 @@ class Scopf:
     def contingencies(self):
         ids = np.empty(self.K, np.int32)
         check(lib.ncl_scopf_contingencies(self._h, _ptr(ids)))
+        return ids
+
+    def candidates(self):
+        """All non-islanding single-branch outages of the grid, ascending."""
+        cnt = C.c_int()
+        check(lib.ncl_scopf_candidates(self._h, None, C.byref(cnt)))
+        ids = np.empty(cnt.value, np.int32)
+        check(lib.ncl_scopf_candidates(self._h, _ptr(ids), C.byref(cnt)))
         return ids
 
     def build_model(self) -> ModelFunctions:
