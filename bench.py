@@ -48,6 +48,7 @@ def _args():
     ap.add_argument("--grid", default=GRID)
     ap.add_argument("--K", type=int, default=K_CONT)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-solve", action="store_true", help="skip the end-to-end NCL solve (time to solve)")
     return ap.parse_args()
 
 
@@ -285,6 +286,34 @@ def main():
         with open(tp) as f:
             prof_traffic = json.load(f).get("bytes_per_launch")
 
+    # ---- time to solve: the whole NCL/IPM solve of the same SCOPF on this GPU
+    tts = None
+    if not a.no_solve:
+        from paper_2510_13333_b200.ipm import NclSolver, default_options
+
+        del F  # free the bench factor before the solver allocates its own
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        sol = NclSolver(P["model"], P["scopf"].bounds())
+        out = sol.solve(default_options(verbose=0))
+        t_solve = time.perf_counter() - t0
+        r = out.result
+        its = max(1, r["inner_iters"])
+        if dist:
+            t = torch.tensor([t_solve], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            t_solve = float(t.item())
+        tts = {"seconds": t_solve, "status": out.status, "outer_iters": r["outer_iters"],
+               "inner_iters": r["inner_iters"], "factorizations": r["factorizations"],
+               "objective": r["objective"], "r_inf": r["r_inf"], "inf_pr": r["inf_pr"], "inf_du": r["inf_du"],
+               "analyze_s": r["t_init"],
+               "kkt_factor_solve_ms_per_iter": 1e3 * (r["t_factor"] + r["t_solve"]) / its,
+               "split_s": {k: r[k] for k in ("t_init", "t_eval", "t_factor", "t_solve", "t_linesearch", "t_other")},
+               "paper_gpu_s": 170.75, "paper_ref": "PAPER.md:611 (A30 + cuDSS, real ACTIVSg500)"}
+        del sol
+
     cpu = None
     if rank == 0 and not a.no_cpu_baseline and os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libnclopf_ref.so")):
         from oracle.ref import RefFactorization, RefSparseSym, RefSymbolic
@@ -324,6 +353,7 @@ def main():
                          "kernel": "factor (supernodal LDL^T, maxdiag+thresh+factor_kernel)",
                          "algorithmic_bytes": B_fact},
             "cpu_baseline": cpu,
+            "time_to_solve": tts,
         }
         print(json.dumps(line), flush=True)
     if dist:

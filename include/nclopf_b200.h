@@ -91,6 +91,9 @@ typedef struct ncl_symb_info {
   int nsplit;             /* supernodes below this ticket run warp-per-task, above CTA-per-task */
 } ncl_symb_info;
 int ncl_symb_info_get(ncl_symb_t S, ncl_symb_info* info);
+/* inspection: supernode partition (nsn+1 firsts, nsn+1 row offsets), parent
+ * supernodes, heights, ticket order (nsn each); any may be NULL */
+int ncl_symb_supernodes(ncl_symb_t S, int* sn_first, int64_t* sn_rptr, int* sn_parent, int* height, int* order);
 int ncl_symb_get(ncl_symb_t S, int* perm, int* iperm, int* parent, int* up_colptr, int* up_rowind,
                  int* entry_map, int* l_colcount);
 

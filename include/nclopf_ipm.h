@@ -47,6 +47,7 @@ typedef struct ncl_options {
   double dw_decrease;   /* 1/3: next iteration starts from dw_last / 3 */
   double dw_max;        /* 1e40 -> RegularizationExhausted */
   double dc_base, kappa_c;  /* dc = dc_base * mu^kappa_c on a zero pivot: 1e-8, 0.25 */
+  int dw_reuse;         /* 1: start from dw_last/3 when the last iteration needed dw > 0 */
   double pivot_tol;     /* 1e-14 for the condensed K (sparse_sym.hpp:125 default 1e-12 is for O(1) diagonals) */
   /* linear solve (sparse_sym.hpp:136-139) */
   double refine_target; /* 1e-8 */

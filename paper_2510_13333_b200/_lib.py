@@ -64,6 +64,7 @@ _SIGS = {
     "ncl_analyze": (i32, [P, P, C.POINTER(P)]),
     "ncl_symb_destroy": (None, [P]),
     "ncl_symb_info_get": (i32, [P, C.POINTER(SymbInfo)]),
+    "ncl_symb_supernodes": (i32, [P, P, P, P, P, P]),
     "ncl_symb_get": (i32, [P, P, P, P, P, P, P, P]),
     "ncl_factorize": (i32, [P, P, f64, C.POINTER(P)]),
     "ncl_refactorize": (i32, [P, P, f64]),

@@ -474,6 +474,20 @@ API int ncl_symb_info_get(ncl_symb_t S, ncl_symb_info* info) {
     info->nsplit = S->Z.nsplit;
   });
 }
+API int ncl_symb_supernodes(ncl_symb_t S, int* sn_first, int64_t* sn_rptr, int* sn_parent, int* height,
+                            int* order) {
+  GUARD({
+    const Supernodal& Z = S->Z;
+    auto cp = [](auto* dst, const auto& v) {
+      if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(v[0]));
+    };
+    cp(sn_first, Z.sn_first);
+    cp(sn_rptr, Z.sn_rptr);
+    cp(sn_parent, Z.sn_parent);
+    cp(height, Z.height);
+    cp(order, Z.order);
+  });
+}
 API int ncl_symb_get(ncl_symb_t S, int* perm, int* iperm, int* parent, int* up_colptr, int* up_rowind,
                      int* entry_map, int* l_colcount) {
   GUARD({

@@ -2,6 +2,9 @@
 #include <cstring>
 #include <algorithm>
 #include <memory>
+#include <mutex>
+#include <tuple>
+#include <vector>
 #include <stdexcept>
 #include <string>
 
@@ -21,6 +24,26 @@ using namespace nclb;
   }                   \
   return NCL_OK;
 
+namespace {
+// grid generation (N-1 DC ratings) is deterministic and the costliest part of
+// instance creation; keep the last few grids
+Grid cached_synthetic(int nb, int nl, int ng, uint64_t seed) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::tuple<int, int, int, uint64_t>, Grid>> cache;
+  const auto key = std::make_tuple(nb, nl, ng, seed);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (const auto& e : cache)
+      if (e.first == key) return e.second;
+  }
+  Grid g = grid_synthetic(nb, nl, ng, seed);
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache.size() >= 4) cache.erase(cache.begin());
+  cache.emplace_back(key, g);
+  return g;
+}
+}  // namespace
+
 struct ncl_scopf {
   Grid grid;
   ModelSpec spec;
@@ -31,7 +54,7 @@ API int ncl_scopf_create_list(int grid, int nb, int nl, int ng, uint64_t seed, i
   GUARD({
     auto s = std::make_unique<ncl_scopf>();
     try {
-      s->grid = grid == 0 ? grid_case9() : grid_synthetic(nb, nl, ng, seed);
+      s->grid = grid == 0 ? grid_case9() : cached_synthetic(nb, nl, ng, seed);
     } catch (const std::invalid_argument& e) {
       throw Error{NCL_E_INVALID, e.what()};
     }

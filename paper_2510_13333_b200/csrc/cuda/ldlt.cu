@@ -189,16 +189,109 @@ __device__ __forceinline__ void factor_task(const FactorArgs& a, int s, int tid,
   }
 }
 
+// Front held entirely in shared memory (nr <= cap): one global read of the
+// A entries and children's CBs, factor + Schur update fused into one
+// right-looking sweep over the w pivot columns in smem, one write of the
+// panel and the lower CB. The warp version (nr <= 32) keeps lane i on row i
+// and broadcasts L(c2, c) with shuffles.
+template <int NT>
+__device__ __forceinline__ void factor_task_smem(const FactorArgs& a, int s, int tid, double thresh, double* F) {
+  const DevSymb& S = a.S;
+  if (tid == 0)
+    for (int q = __ldg(S.cptr + s); q < __ldg(S.cptr + s + 1); ++q) wait_flag(a.flags + __ldg(S.child + q), a.epoch);
+  const int f = __ldg(S.sn_first + s);
+  const int w = __ldg(S.sn_first + s + 1) - f;
+  const int64_t rb = __ldg(S.sn_rptr + s);
+  const int nr = static_cast<int>(__ldg(S.sn_rptr + s + 1) - rb);
+  const int m2 = nr - w;
+  for (int k = tid; k < nr * nr; k += NT) F[k] = 0.0;
+  team_sync<NT>();
+  for (int64_t e = __ldg(S.aptr + s) + tid; e < __ldg(S.aptr + s + 1); e += NT)
+    F[__ldg(S.aoff + e)] = __ldg(a.kvals + __ldg(S.asrc + e));  // panel offset c*nr + r == front offset
+  team_sync<NT>();
+  for (int q = __ldg(S.cptr + s); q < __ldg(S.cptr + s + 1); ++q) {
+    const int c = __ldg(S.child + q);
+    const int wc = __ldg(S.sn_first + c + 1) - __ldg(S.sn_first + c);
+    const int64_t rbc = __ldg(S.sn_rptr + c);
+    const int m2c = static_cast<int>(__ldg(S.sn_rptr + c + 1) - rbc) - wc;
+    const int* rel = S.relp + rbc + wc;
+    const double* Cc = a.CB + __ldg(S.cb_off + c);
+    for (int e = tid; e < m2c * m2c; e += NT) {
+      const int i = e % m2c, j = e / m2c;
+      if (i >= j) F[__ldg(rel + j) * nr + __ldg(rel + i)] += __ldcg(Cc + e);
+    }
+    team_sync<NT>();
+  }
+  if constexpr (NT == 32) {
+    const int i = tid;
+    for (int c = 0; c < w; ++c) {
+      const double d = F[c * nr + c];
+      if (i == 0) {
+        a.D[f + c] = d;
+        if (fabs(d) <= thresh) atomicMin(a.zp, f + c);
+      }
+      double l = 0.0;
+      if (i > c && i < nr) {
+        l = F[c * nr + i] / d;
+        F[c * nr + i] = l;
+      }
+      const double dl = d * l;
+      for (int c2 = c + 1; c2 < nr; ++c2) {
+        const double lc2 = __shfl_sync(kFull, dl, c2);  // d * L(c2, c)
+        if (i >= c2 && i < nr) F[c2 * nr + i] -= l * lc2;
+      }
+      __syncwarp();
+    }
+  } else {
+    for (int c = 0; c < w; ++c) {
+      double* Fc = F + c * nr;
+      const double d = Fc[c];
+      if (tid == 0) {
+        a.D[f + c] = d;
+        if (fabs(d) <= thresh) atomicMin(a.zp, f + c);
+      }
+      for (int i = c + 1 + tid; i < nr; i += NT) Fc[i] = Fc[i] / d;
+      __syncthreads();
+      const int rem = nr - c - 1;
+      for (int e = tid; e < rem * rem; e += NT) {
+        const int i = c + 1 + e % rem, c2 = c + 1 + e / rem;
+        if (i >= c2) F[c2 * nr + i] -= Fc[i] * (d * Fc[c2]);
+      }
+      __syncthreads();
+    }
+  }
+  double* P = a.L + __ldg(S.sn_loff + s);
+  double* C = a.CB + __ldg(S.cb_off + s);
+  for (int k = tid; k < w * nr; k += NT) P[k] = F[k];
+  for (int e = tid; e < m2 * m2; e += NT) {
+    const int i = e % m2, j = e / m2;
+    if (i >= j) C[e] = F[(w + j) * nr + (w + i)];
+  }
+  team_sync<NT>();
+  if (tid == 0) {
+    __threadfence();
+    st_release(a.flags + s, a.epoch);
+  }
+}
+
+constexpr int kWarpFront = 32;    // nr cap of the warp smem path
+constexpr int kCtaFront = 160;    // nr cap of the CTA smem path (160^2 doubles = 200 KB)
+
 template <int NT>
 __global__ void __launch_bounds__(NT == 32 ? 128 : NT) factor_kernel(FactorArgs a) {
   __shared__ int s_ticket;
+  extern __shared__ double s_front[];
   const int tid = NT == 32 ? (threadIdx.x & 31) : threadIdx.x;
+  double* F = NT == 32 ? s_front + (threadIdx.x >> 5) * kWarpFront * kWarpFront : s_front;
   const double thresh = __ldcg(a.thresh);
   Claim<NT> cl;
   for (;;) {
     const int t = cl.next(a.ticket, a.t0, a.t1, a.S.nleaf, tid, &s_ticket);
     if (t < 0) break;
-    factor_task<NT>(a, __ldg(a.S.order + t), tid, thresh);
+    const int s = __ldg(a.S.order + t);
+    const int nr = static_cast<int>(__ldg(a.S.sn_rptr + s + 1) - __ldg(a.S.sn_rptr + s));
+    if (nr <= (NT == 32 ? kWarpFront : kCtaFront)) factor_task_smem<NT>(a, s, tid, thresh, F);
+    else factor_task<NT>(a, s, tid, thresh);
   }
 }
 
@@ -486,9 +579,9 @@ void dev_max_abs_diag(const DevPattern& P, const double* kvals, double* out, cud
 }
 
 template <class K>
-int persistent_grid(K fn, int threads, int ntasks) {
+int persistent_grid(K fn, int threads, int ntasks, int smem = 0) {
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
   if (per_sm <= 0) per_sm = 1;
   const int g = num_sms() * per_sm;
   return std::max(1, std::min(g, ntasks));
@@ -503,20 +596,25 @@ void dev_factor(const DevSymb& S0, const DevPattern& P, DevFactor& F, const doub
   S.epoch++;
   cudaMemsetAsync(S.tickets, 0, 4 * sizeof(int), st);
   FactorArgs a{S, F.L, F.CB, F.D, kvals, F.scal, F.istat, S.flags, S.tickets + 0, S.epoch, 0, S.nsplit};
+  constexpr int smem1 = 4 * kWarpFront * kWarpFront * sizeof(double);
+  constexpr int smem2 = kCtaFront * kCtaFront * sizeof(double);
+  static int g = 0, g2 = 0;
+  if (!g) {
+    cudaFuncSetAttribute(factor_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1);
+    cudaFuncSetAttribute(factor_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+    g = persistent_grid(factor_kernel<32>, 128, 1 << 30, smem1);
+    g2 = persistent_grid(factor_kernel<256>, 256, 1 << 30, smem2);
+  }
   if (S.nsplit > 0) {
-    static int g = 0;
-    if (!g) g = persistent_grid(factor_kernel<32>, 128, 1 << 30);
     COUNT(1);
-    factor_kernel<32><<<g, 128, 0, st>>>(a);
+    factor_kernel<32><<<g, 128, smem1, st>>>(a);
   }
   if (S.nsplit < S.nsn) {
-    static int g2 = 0;
-    if (!g2) g2 = persistent_grid(factor_kernel<256>, 256, 1 << 30);
     a.ticket = S.tickets + 1;
     a.t0 = S.nsplit;
     a.t1 = S.nsn;
     COUNT(1);
-    factor_kernel<256><<<std::min(g2, S.nsn - S.nsplit), 256, 0, st>>>(a);
+    factor_kernel<256><<<std::min(g2, S.nsn - S.nsplit), 256, smem2, st>>>(a);
   }
 }
 

@@ -60,6 +60,7 @@ ncl_options default_options() {
   o.dw_max = 1e40;
   o.dc_base = 1e-8;
   o.kappa_c = 0.25;
+  o.dw_reuse = 1;
   o.pivot_tol = 1e-14;
   o.refine_target = 1e-8;
   o.refine_max_sweeps = 5;
@@ -132,7 +133,12 @@ int Solver::subproblem(double tol, int outer) {
     t0 = clk::now();
     S_.dc = 0.0;
     be_.form_newton(S_);
-    double dw = 0.0;
+    // dw_reuse: when the previous iteration needed dw > 0, skip the dw = 0
+    // trial and start at dw_last / 3 (one factorization saved per
+    // iteration in the non-convex phase; Ipopt always tries 0 first)
+    double dw = (o_.dw_reuse && dw_last_ > 0.0)
+                    ? std::max(o_.dw_first_rel * std::max(1.0, be_.hess_absmax()), o_.dw_decrease * dw_last_)
+                    : 0.0;
     double hnorm = -1.0;
     int tries = 0;
     for (;;) {

@@ -26,7 +26,7 @@ _OPT_FIELDS = [
     ("gamma_theta", f64), ("gamma_phi", f64), ("eta_phi", f64), ("delta", f64), ("s_theta", f64), ("s_phi", f64),
     ("alpha_min_frac", f64), ("max_backtrack", i32),
     ("dw_first_rel", f64), ("dw_growth", f64), ("dw_decrease", f64), ("dw_max", f64), ("dc_base", f64),
-    ("kappa_c", f64), ("pivot_tol", f64), ("refine_target", f64), ("refine_max_sweeps", i32),
+    ("kappa_c", f64), ("dw_reuse", i32), ("pivot_tol", f64), ("refine_target", f64), ("refine_max_sweeps", i32),
     ("mu_warm_frac", f64), ("acceptable_factor", f64), ("acceptable_iter", i32), ("verbose", i32),
 ]
 

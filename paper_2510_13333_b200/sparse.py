@@ -208,6 +208,17 @@ class SymbolicFactor:
                             s.flops, s.cb_storage, s.nsplit)
 
 
+def supernodes(S: "SymbolicFactor"):
+    """Supernode partition / parents / heights / ticket order (inspection)."""
+    info = S.info()
+    ns = info.nsupernodes
+    first = np.empty(ns + 1, np.int32)
+    rptr = np.empty(ns + 1, np.int64)
+    par, h, order = (np.empty(ns, np.int32) for _ in range(3))
+    check(lib.ncl_symb_supernodes(S.handle, _ptr(first), _ptr(rptr), _ptr(par), _ptr(h), _ptr(order)))
+    return dict(first=first, rptr=rptr, parent=par, height=h, order=order)
+
+
 def analyze(M: SparseSym, perm=None) -> SymbolicFactor:
     """analyze(M) / analyze(M, perm) (sparse_sym.hpp:87-88), bit-exact."""
     h = C.c_void_p()
