@@ -138,37 +138,97 @@ std::vector<int> symbolic_order(int n, const std::vector<int>& cp, const std::ve
   std::vector<char> dead(n, 0);
   std::vector<int> perm;
   perm.reserve(n);
+  // Hybrid adjacency: sorted vectors, switched to a bitmap once a node's
+  // degree exceeds kBig (the SCOPF's base-case nodes touch every
+  // contingency: a vector merge would cost O(degree) per neighbouring
+  // elimination, the bitmap costs O(|clique|)). Only the SET of neighbours is
+  // observable (degrees and clique membership), so the representation does
+  // not change the ordering.
+  constexpr int kBig = 256;
+  const int64_t nwords = (static_cast<int64_t>(n) + 63) / 64;
+  std::vector<int> bmap(n, -1), bdeg(n, 0);  // bitmap slot per node, degree in bitmap mode
+  std::vector<std::vector<uint64_t>> pool;
+  std::vector<int> free_slots;
+  auto degree = [&](int u) { return bmap[u] >= 0 ? bdeg[u] : static_cast<int>(adj[u].size()); };
+  auto to_bitmap = [&](int u) {
+    int slot;
+    if (!free_slots.empty()) {
+      slot = free_slots.back();
+      free_slots.pop_back();
+    } else {
+      slot = static_cast<int>(pool.size());
+      pool.emplace_back(nwords, 0ull);
+    }
+    auto& bm = pool[slot];
+    for (int x : adj[u]) bm[x >> 6] |= 1ull << (x & 63);
+    bdeg[u] = static_cast<int>(adj[u].size());
+    bmap[u] = slot;
+    std::vector<int>().swap(adj[u]);
+  };
   std::vector<int> clique, merged;
   while (!heap.empty()) {
     const Key k = heap.top();
     heap.pop();
     const int v = static_cast<int>(k & 0xffffffffu);
     const int deg = static_cast<int>(k >> 32);
-    if (dead[v] || deg != static_cast<int>(adj[v].size())) continue;
+    if (dead[v] || deg != degree(v)) continue;
     perm.push_back(v);
     dead[v] = 1;
-    clique.swap(adj[v]);
-    for (int u : clique) {
-      std::vector<int>& au = adj[u];
-      const int old = static_cast<int>(au.size());
-      merged.clear();
-      merged.reserve(au.size() + clique.size());
-      size_t i = 0, j = 0;
-      const size_t na = au.size(), nc = clique.size();
-      while (i < na || j < nc) {
-        int x;
-        if (j >= nc || (i < na && au[i] < clique[j])) {
-          x = au[i++];
-        } else if (i >= na || clique[j] < au[i]) {
-          x = clique[j++];
-        } else {
-          x = au[i++];
-          ++j;
+    if (bmap[v] >= 0) {  // enumerate the bitmap ascending, release it
+      auto& bm = pool[bmap[v]];
+      clique.clear();
+      clique.reserve(bdeg[v]);
+      for (int64_t wd = 0; wd < nwords; ++wd) {
+        uint64_t bits = bm[wd];
+        while (bits) {
+          const int t = __builtin_ctzll(bits);
+          clique.push_back(static_cast<int>(wd * 64 + t));
+          bits &= bits - 1;
         }
-        if (x != v && x != u) merged.push_back(x);
+        bm[wd] = 0;
       }
-      au.swap(merged);
-      if (static_cast<int>(au.size()) != old) heap.push(key(static_cast<int>(au.size()), u));
+      free_slots.push_back(bmap[v]);
+      bmap[v] = -1;
+    } else {
+      clique.swap(adj[v]);
+    }
+    for (int u : clique) {
+      const int old = degree(u);
+      if (bmap[u] >= 0) {
+        auto& bm = pool[bmap[u]];
+        int d = bdeg[u];
+        for (int x : clique)
+          if (x != u) {
+            uint64_t& wd = bm[x >> 6];
+            const uint64_t bit = 1ull << (x & 63);
+            if (!(wd & bit)) wd |= bit, ++d;
+          }
+        uint64_t& wv = bm[v >> 6];
+        const uint64_t bv = 1ull << (v & 63);
+        if (wv & bv) wv &= ~bv, --d;
+        bdeg[u] = d;
+      } else {
+        std::vector<int>& au = adj[u];
+        merged.clear();
+        merged.reserve(au.size() + clique.size());
+        size_t i = 0, j = 0;
+        const size_t na = au.size(), nc = clique.size();
+        while (i < na || j < nc) {
+          int x;
+          if (j >= nc || (i < na && au[i] < clique[j])) {
+            x = au[i++];
+          } else if (i >= na || clique[j] < au[i]) {
+            x = clique[j++];
+          } else {
+            x = au[i++];
+            ++j;
+          }
+          if (x != v && x != u) merged.push_back(x);
+        }
+        au.swap(merged);
+        if (static_cast<int>(au.size()) > kBig) to_bitmap(u);
+      }
+      if (degree(u) != old) heap.push(key(degree(u), u));
     }
     clique.clear();
     std::vector<int>().swap(clique);

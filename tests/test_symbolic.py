@@ -101,3 +101,27 @@ def test_matrix_market_matches_reference():
     r, c, v = matgen.kkt_like(10, 4, rng)
     A, B = both(14, r, c, v)
     assert A.write_matrix_market() == B.write_matrix_market()
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_high_degree_nodes_bit_exact(seed):
+    """Nodes above the ordering's bitmap threshold (degree > 1024), like the
+    SCOPF base-case variables that couple every contingency block."""
+    rng = np.random.default_rng(77 + seed)
+    n = 2600
+    r, c = [], []
+    for i in range(1, n):  # sparse backbone: random tree + chords
+        j = int(rng.integers(0, i))
+        r.append(i), c.append(j)
+    for _ in range(2 * n):
+        i, j = sorted(rng.integers(0, n, 2))[::-1]
+        if i != j:
+            r.append(int(i)), c.append(int(j))
+    for hub in rng.choice(n, 4, replace=False):  # hubs of degree ~1100-1300
+        for j in rng.choice(n, int(rng.integers(1100, 1300)), replace=False):
+            if j != hub:
+                r.append(int(max(hub, j))), c.append(int(min(hub, j)))
+    r += list(range(n)); c += list(range(n))
+    v = rng.standard_normal(len(r))
+    A, B = both(n, np.array(r), np.array(c), v)
+    assert_symbolic_equal(A, B)
