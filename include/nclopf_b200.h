@@ -211,6 +211,9 @@ int ncl_scopf_family_data(ncl_scopf_t S, int f, ncl_expr_node* nodes, int* rows,
 /* variable bounds/start (n), row bounds (m); +-inf for absent bounds */
 int ncl_scopf_bounds(ncl_scopf_t S, double* xl, double* xu, double* x0, double* gl, double* gu);
 int ncl_scopf_contingencies(ncl_scopf_t S, int* branch_ids);
+/* scenario of every variable (n): 0 = base case, k = contingency k — the
+ * var_group input of the sharded factorization (nclopf_dist.h) */
+int ncl_scopf_var_groups(ncl_scopf_t S, int* groups);
 /* every non-islanding single-branch outage of the grid (ascending); ids may be NULL */
 int ncl_scopf_candidates(ncl_scopf_t S, int* ids, int* count);
 int ncl_scopf_build_model(ncl_scopf_t S, ncl_model_t* out); /* this library's ModelBuilder */

@@ -405,7 +405,7 @@ void upload_symb(ncl_symb* S) {
   S->aoff.upload(aoff);
   S->flags.alloc(3 * std::max(1, nsn));
   ck(cudaMemsetAsync(S->flags.p, 0, 3 * std::max(1, nsn) * sizeof(int), g_stream), "memset");
-  S->tickets.alloc(4);
+  S->tickets.alloc(kTickets);
   DevSymb& d = S->d;
   d.n = S->core.n;
   d.nsn = nsn;
@@ -707,5 +707,256 @@ API int ncl_fact_get_L(ncl_fact_t F, int* lp, int* li, double* lx) {
         if (lx) lx[p] = Lh[Z.sn_loff[s] + static_cast<int64_t>(j - f) * nr + q];
       }
     }
+  });
+}
+
+// ---------------------------------------------------------------------------
+// Multi-GPU: NCCL (dlopen'd, so the library shares the process's libnccl.so.2
+// with torch) and the contingency-sharded factor / solve (csrc/host/shard.hpp)
+// ---------------------------------------------------------------------------
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include "../../include/nclopf_dist.h"
+#include "host/shard.hpp"
+
+namespace {
+struct Nccl {
+  void* h = nullptr;
+  decltype(&ncclGetUniqueId) get_id = nullptr;
+  decltype(&ncclCommInitRank) init_rank = nullptr;
+  decltype(&ncclAllGather) all_gather = nullptr;
+  decltype(&ncclAllReduce) all_reduce = nullptr;
+  decltype(&ncclCommDestroy) destroy = nullptr;
+  decltype(&ncclGetErrorString) err = nullptr;
+  ncclComm_t comm = nullptr;
+  int world = 1, rank = 0;
+};
+Nccl g_nccl;
+void nccl_load() {
+  if (g_nccl.h) return;
+  g_nccl.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!g_nccl.h) throw Error{NCL_E_CUDA, std::string("NCCL not loadable: ") + dlerror()};
+  auto sym = [](const char* n) {
+    void* p = dlsym(g_nccl.h, n);
+    if (!p) throw Error{NCL_E_CUDA, std::string("NCCL symbol missing: ") + n};
+    return p;
+  };
+  g_nccl.get_id = reinterpret_cast<decltype(g_nccl.get_id)>(sym("ncclGetUniqueId"));
+  g_nccl.init_rank = reinterpret_cast<decltype(g_nccl.init_rank)>(sym("ncclCommInitRank"));
+  g_nccl.all_gather = reinterpret_cast<decltype(g_nccl.all_gather)>(sym("ncclAllGather"));
+  g_nccl.all_reduce = reinterpret_cast<decltype(g_nccl.all_reduce)>(sym("ncclAllReduce"));
+  g_nccl.destroy = reinterpret_cast<decltype(g_nccl.destroy)>(sym("ncclCommDestroy"));
+  g_nccl.err = reinterpret_cast<decltype(g_nccl.err)>(sym("ncclGetErrorString"));
+}
+void nck(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw Error{NCL_E_CUDA, std::string(what) + ": " + g_nccl.err(r)};
+}
+}  // namespace
+
+API int ncl_dist_get_unique_id(char* id) {
+  GUARD({
+    nccl_load();
+    ncclUniqueId u;
+    nck(g_nccl.get_id(&u), "ncclGetUniqueId");
+    std::memcpy(id, u.internal, NCCL_UNIQUE_ID_BYTES);
+  });
+}
+API int ncl_dist_init(int world, int rank, const char* id) {
+  GUARD({
+    ensure_init();
+    nccl_load();
+    if (g_nccl.comm) throw Error{NCL_E_LOGIC, "ncl_dist_init: already initialised"};
+    ncclUniqueId u;
+    std::memcpy(u.internal, id, NCCL_UNIQUE_ID_BYTES);
+    nck(g_nccl.init_rank(&g_nccl.comm, world, u, rank), "ncclCommInitRank");
+    g_nccl.world = world;
+    g_nccl.rank = rank;
+  });
+}
+API int ncl_dist_finalize(void) {
+  GUARD({
+    if (g_nccl.comm) g_nccl.destroy(g_nccl.comm);
+    g_nccl.comm = nullptr;
+    g_nccl.world = 1;
+    g_nccl.rank = 0;
+  });
+}
+
+struct ncl_shard {
+  ShardPlan P;
+  ncl_symb* S = nullptr;
+  bool dev_ready = false;
+  DevBuf<int> listA, listB, bids, bowner;
+  DevBuf<int64_t> cb_off, cv_off;
+  DevBuf<uint8_t> report;
+  DevBuf<double> send, recv;
+  DevBuf<int> unrep;  // original indices this rank does not report (zeroed before the x all-reduce)
+  int64_t nunrep = 0;
+};
+
+namespace {
+void shard_upload(ncl_shard* sh) {
+  if (sh->dev_ready) return;
+  ensure_init();
+  upload_symb(sh->S);
+  sh->listA.upload(sh->P.listA);
+  sh->listB.upload(sh->P.listB);
+  sh->bids.upload(sh->P.boundary);
+  sh->bowner.upload(sh->P.bowner);
+  sh->cb_off.upload(sh->P.cb_pack_off);
+  sh->cv_off.upload(sh->P.cv_pack_off);
+  sh->report.upload(sh->P.col_report);
+  {
+    std::vector<int> u;
+    const auto& perm = sh->S->core.perm;
+    for (size_t j = 0; j < sh->P.col_report.size(); ++j)
+      if (!sh->P.col_report[j]) u.push_back(perm[j]);
+    sh->nunrep = static_cast<int64_t>(u.size());
+    sh->unrep.upload(u);
+  }
+  const int64_t chunk = std::max(sh->P.cb_chunk, sh->P.cv_chunk);
+  sh->send.alloc(std::max<int64_t>(1, chunk));
+  sh->recv.alloc(std::max<int64_t>(1, chunk * sh->P.world));
+  sh->dev_ready = true;
+}
+DevTasks tasks_A(ncl_shard* sh) {
+  return DevTasks{sh->listA.p, static_cast<int>(sh->P.listA.size()), sh->P.nleafA, sh->P.splitA};
+}
+DevTasks tasks_B(ncl_shard* sh) {
+  return DevTasks{sh->listB.p, static_cast<int>(sh->P.listB.size()), sh->P.nleafB, sh->P.splitB};
+}
+void need_comm(const ncl_shard* sh) {
+  if (sh->P.world == 1) return;
+  if (!g_nccl.comm || g_nccl.world != sh->P.world || g_nccl.rank != sh->P.rank)
+    throw Error{NCL_E_LOGIC, "sharded call needs ncl_dist_init with the plan's world/rank"};
+}
+void allgather_blocks(ncl_shard* sh, double* base, int cv, int* flags, int epoch) {
+  const ShardPlan& P = sh->P;
+  const int nb = static_cast<int>(P.boundary.size());
+  const int64_t chunk = cv ? P.cv_chunk : P.cb_chunk;
+  if (nb == 0 || chunk == 0) return;
+  const int64_t* off = cv ? sh->cv_off.p : sh->cb_off.p;
+  dev_shard_pack(sh->S->d, base, sh->bids.p, sh->bowner.p, off, nb, P.rank, cv, sh->send.p, g_stream);
+  nck(g_nccl.all_gather(sh->send.p, sh->recv.p, chunk, ncclFloat64, g_nccl.comm, g_stream), "ncclAllGather");
+  dev_shard_unpack(sh->S->d, base, sh->bids.p, sh->bowner.p, off, nb, P.rank, cv, sh->recv.p, chunk, flags, epoch,
+                   g_stream);
+}
+}  // namespace
+
+API int ncl_shard_create(ncl_symb_t S, const int* var_group, int ngroups, int world, int rank, ncl_shard_t* out) {
+  GUARD({
+    auto sh = std::make_unique<ncl_shard>();
+    sh->S = S;
+    std::vector<int> g(var_group, var_group + S->core.n);
+    sh->P = build_shard_plan(S->Z, S->core, g, ngroups, world, rank);
+    *out = sh.release();
+  });
+}
+API void ncl_shard_destroy(ncl_shard_t P) { delete P; }
+API int ncl_shard_info_get(ncl_shard_t sh, ncl_shard_info* info) {
+  GUARD({
+    const ShardPlan& P = sh->P;
+    info->world = P.world;
+    info->rank = P.rank;
+    info->owned_supernodes = P.owned_supernodes;
+    info->shared_supernodes = P.shared_supernodes;
+    info->n_phase_a = static_cast<int>(P.listA.size());
+    info->n_phase_b = static_cast<int>(P.listB.size());
+    info->n_boundary = static_cast<int>(P.boundary.size());
+    info->cb_chunk = P.cb_chunk;
+    info->cv_chunk = P.cv_chunk;
+    int64_t rc = 0;
+    for (uint8_t v : P.col_report) rc += v;
+    info->report_cols = rc;
+  });
+}
+API int ncl_shard_owners(ncl_shard_t sh, int* owner) {
+  GUARD(std::memcpy(owner, sh->P.owner.data(), sh->P.owner.size() * sizeof(int)));
+}
+API int ncl_shard_boundary(ncl_shard_t sh, int* ids, int* owner, int64_t* cb_off, int64_t* cv_off) {
+  GUARD({
+    const ShardPlan& P = sh->P;
+    const size_t nb = P.boundary.size();
+    if (ids) std::memcpy(ids, P.boundary.data(), nb * sizeof(int));
+    if (owner) std::memcpy(owner, P.bowner.data(), nb * sizeof(int));
+    if (cb_off) std::memcpy(cb_off, P.cb_pack_off.data(), nb * sizeof(int64_t));
+    if (cv_off) std::memcpy(cv_off, P.cv_pack_off.data(), nb * sizeof(int64_t));
+  });
+}
+
+API int ncl_shard_refactorize(ncl_fact_t F, ncl_sym_t M, ncl_shard_t sh, double tol) {
+  GUARD({
+    if (sh->S != F->S) throw Error{NCL_E_INVALID, "shard plan built for another symbolic factor"};
+    need_comm(sh);
+    check_match(M, F->S);
+    ensure_dev(M, "factorize");
+    shard_upload(sh);
+    DevSymb& d = F->S->d;
+    dev_factor_begin(d, M->dp, F->F, M->vals.p, tol, g_stream);
+    dev_factor_list(d, F->F, M->vals.p, tasks_A(sh), 0, g_stream);
+    if (sh->P.world > 1) allgather_blocks(sh, F->F.CB, 0, d.flags, d.epoch);
+    dev_factor_list(d, F->F, M->vals.p, tasks_B(sh), 1, g_stream);
+    if (sh->P.world > 1) {
+      dev_inertia(d, F->F, g_stream, sh->report.p);
+      // istat = [zero-pivot position (min), npos, nneg, nzero (sums)]
+      nck(g_nccl.all_reduce(F->F.istat, F->F.istat, 1, ncclInt32, ncclMin, g_nccl.comm, g_stream), "allreduce");
+      nck(g_nccl.all_reduce(F->F.istat + 1, F->F.istat + 1, 3, ncclInt32, ncclSum, g_nccl.comm, g_stream),
+          "allreduce");
+    } else {
+      dev_inertia(d, F->F, g_stream);
+    }
+    check_launch("shard factorize");
+  });
+}
+
+// Single-GPU emulation of a world-G run: every rank's phase A on one device
+// (they write disjoint CBs, so no exchange is needed), then phase B once.
+API int ncl_shard_refactorize_emulated(ncl_fact_t F, ncl_sym_t M, ncl_shard_t* plans, int G, double tol) {
+  GUARD({
+    if (G < 1 || 2 * (G + 1) > kTickets) throw Error{NCL_E_INVALID, "emulated shards: bad G"};
+    check_match(M, F->S);
+    ensure_dev(M, "factorize");
+    for (int r = 0; r < G; ++r) {
+      if (plans[r]->S != F->S || plans[r]->P.world != G || plans[r]->P.rank != r)
+        throw Error{NCL_E_INVALID, "emulated shards: plans must be ranks 0..G-1 of one world"};
+      shard_upload(plans[r]);
+    }
+    DevSymb& d = F->S->d;
+    dev_factor_begin(d, M->dp, F->F, M->vals.p, tol, g_stream);
+    for (int r = 0; r < G; ++r) dev_factor_list(d, F->F, M->vals.p, tasks_A(plans[r]), r, g_stream);
+    dev_factor_list(d, F->F, M->vals.p, tasks_B(plans[0]), G, g_stream);
+    dev_inertia(d, F->F, g_stream);
+    check_launch("emulated shard factorize");
+  });
+}
+
+
+API int ncl_shard_solve(ncl_fact_t F, ncl_shard_t sh, double* x, int where) {
+  GUARD({
+    need_comm(sh);
+    shard_upload(sh);
+    const int n = F->S->core.n;
+    double* dx = x;
+    if (where == NCL_HOST) {
+      ck(cudaMemcpyAsync(F->work1.p, x, n * sizeof(double), cudaMemcpyHostToDevice, g_stream), "H2D");
+      dx = F->work1.p;
+    }
+    DevSymb& d = F->S->d;
+    dev_solve_begin(d, g_stream);
+    dev_solve_fwd_list(d, F->F, dx, tasks_A(sh), 0, g_stream);
+    if (sh->P.world > 1) allgather_blocks(sh, F->F.CV, 1, d.flags + d.nsn, d.epoch);
+    dev_solve_fwd_list(d, F->F, dx, tasks_B(sh), 1, g_stream);
+    dev_solve_bwd_list(d, F->F, dx, tasks_B(sh), 2, g_stream);
+    dev_solve_bwd_list(d, F->F, dx, tasks_A(sh), 3, g_stream);
+    if (sh->P.world > 1) {
+      dev_zero_indexed(dx, sh->unrep.p, sh->nunrep, g_stream);
+      nck(g_nccl.all_reduce(dx, dx, n, ncclFloat64, ncclSum, g_nccl.comm, g_stream), "allreduce x");
+    }
+    if (where == NCL_HOST) {
+      ck(cudaMemcpyAsync(x, dx, n * sizeof(double), cudaMemcpyDeviceToHost, g_stream), "D2H");
+      ck(cudaStreamSynchronize(g_stream), "sync");
+    }
+    check_launch("shard solve");
   });
 }

@@ -137,6 +137,16 @@ API int ncl_scopf_contingencies(ncl_scopf_t S, int* ids) {
   GUARD(if (!S->spec.contingencies.empty()) std::memcpy(ids, S->spec.contingencies.data(),
                                                          S->spec.contingencies.size() * sizeof(int)));
 }
+API int ncl_scopf_var_groups(ncl_scopf_t S, int* groups) {
+  GUARD({
+    const ModelSpec& p = S->spec;
+    const int ns = static_cast<int>(p.off_v.size());
+    for (int s = 0; s < ns; ++s) {
+      const int b = p.off_v[s], e = s + 1 < ns ? p.off_v[s + 1] : p.n;
+      for (int i = b; i < e; ++i) groups[i] = s;
+    }
+  });
+}
 API int ncl_scopf_candidates(ncl_scopf_t S, int* ids, int* count) {
   GUARD({
     const auto all = select_contingencies(S->grid, S->grid.nl);

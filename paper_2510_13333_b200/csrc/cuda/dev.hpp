@@ -60,10 +60,35 @@ struct DevFactor {
   int* istat = nullptr;    // [4]: zp position, npos, nneg, nzero
 };
 
+// A task list: supernode ids in leaves-first height order; the first
+// `nleaf` are leaves, tasks from `split` on run CTA-per-task.
+struct DevTasks {
+  const int* ids = nullptr;
+  int n = 0, nleaf = 0, split = 0;
+};
+constexpr int kTickets = 40;  // ticket counters per symbolic handle
+
 // all launches are asynchronous on `st`
+// sharded pieces: begin (threshold, epoch, tickets) -> list(s) -> inertia
+void dev_factor_begin(const DevSymb& S, const DevPattern& P, DevFactor& F, const double* kvals, double pivot_tol,
+                      cudaStream_t st);
+void dev_factor_list(const DevSymb& S, DevFactor& F, const double* kvals, const DevTasks& T, int slot,
+                     cudaStream_t st);
+void dev_solve_begin(const DevSymb& S, cudaStream_t st);
+void dev_solve_fwd_list(const DevSymb& S, DevFactor& F, const double* b, const DevTasks& T, int slot,
+                        cudaStream_t st);
+void dev_solve_bwd_list(const DevSymb& S, DevFactor& F, double* x, const DevTasks& T, int slot, cudaStream_t st);
+// exchange helpers (csrc/cuda/shard.cu): pack my boundary CBs (or CVs) into
+// send; unpack the others' from recv (G chunks) and publish their flags
+void dev_shard_pack(const DevSymb& S, const double* src, const int* bids, const int* bowner, const int64_t* pack_off,
+                    int nb, int rank, int cv, double* send, cudaStream_t st);
+void dev_shard_unpack(const DevSymb& S, double* dst, const int* bids, const int* bowner, const int64_t* pack_off,
+                      int nb, int rank, int cv, const double* recv, int64_t chunk, int* flags, int epoch,
+                      cudaStream_t st);
+void dev_zero_indexed(double* x, const int* idx, int64_t n, cudaStream_t st);
 void dev_factor(const DevSymb& S, const DevPattern& P, DevFactor& F, const double* kvals, double pivot_tol,
                 cudaStream_t st);
-void dev_inertia(const DevSymb& S, DevFactor& F, cudaStream_t st);
+void dev_inertia(const DevSymb& S, DevFactor& F, cudaStream_t st, const uint8_t* report = nullptr);
 // x := M^{-1} b (in place allowed: x may alias b)
 void dev_solve(const DevSymb& S, DevFactor& F, const double* b, double* x, cudaStream_t st);
 void dev_spmv(const DevPattern& P, const double* kvals, const double* x, double* y, cudaStream_t st);

@@ -111,7 +111,9 @@ struct FactorArgs {
   int* flags;
   int* ticket;
   int epoch;
-  int t0, t1;  // ticket range of this launch
+  int t0, t1;          // ticket range of this launch (indices into tasks)
+  const int* tasks;    // supernode ids, leaves-first height order
+  int nleaf;           // leaf tasks at the head of `tasks`
 };
 
 template <int NT>
@@ -286,9 +288,9 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT) factor_kernel(FactorArgs 
   const double thresh = __ldcg(a.thresh);
   Claim<NT> cl;
   for (;;) {
-    const int t = cl.next(a.ticket, a.t0, a.t1, a.S.nleaf, tid, &s_ticket);
+    const int t = cl.next(a.ticket, a.t0, a.t1, a.nleaf, tid, &s_ticket);
     if (t < 0) break;
-    const int s = __ldg(a.S.order + t);
+    const int s = __ldg(a.tasks + t);
     const int nr = static_cast<int>(__ldg(a.S.sn_rptr + s + 1) - __ldg(a.S.sn_rptr + s));
     if (nr <= (NT == 32 ? kWarpFront : kCtaFront)) factor_task_smem<NT>(a, s, tid, thresh, F);
     else factor_task<NT>(a, s, tid, thresh);
@@ -310,10 +312,12 @@ __global__ void thresh_kernel(double* scal, double tol, int* istat, int n) {
   istat[1] = istat[2] = istat[3] = 0;
 }
 
-__global__ void inertia_kernel(const double* __restrict__ D, int n, const double* scal, int* istat) {
+__global__ void inertia_kernel(const double* __restrict__ D, int n, const double* scal, int* istat,
+                               const uint8_t* __restrict__ report) {
   const double th = scal[0];
   int np = 0, nn = 0, nz = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (report && !report[i]) continue;  // sharded: every column counted by exactly one rank
     const double d = D[i];
     if (fabs(d) <= th) nz++;
     else if (d > 0.0) np++;
@@ -353,6 +357,8 @@ struct SolveArgs {
   int* ticket;
   int epoch;
   int t0, t1;
+  const int* tasks;
+  int nleaf;
 };
 
 template <int NT>
@@ -448,9 +454,9 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT) fwd_kernel(SolveArgs a) {
   const int tid = NT == 32 ? (threadIdx.x & 31) : threadIdx.x;
   Claim<NT> cl;
   for (;;) {
-    const int t = cl.next(a.ticket, a.t0, a.t1, a.S.nleaf, tid, &s_ticket);
+    const int t = cl.next(a.ticket, a.t0, a.t1, a.nleaf, tid, &s_ticket);
     if (t < 0) break;
-    fwd_task<NT>(a, __ldg(a.S.order + t), tid);
+    fwd_task<NT>(a, __ldg(a.tasks + t), tid);
   }
 }
 
@@ -473,7 +479,7 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT) bwd_kernel(SolveArgs a) {
     }
     const int k = a.t1 - 1 - t;
     if (k < a.t0) break;
-    bwd_task<NT>(a, __ldg(a.S.order + k), tid);
+    bwd_task<NT>(a, __ldg(a.tasks + k), tid);
   }
 }
 
@@ -587,73 +593,104 @@ int persistent_grid(K fn, int threads, int ntasks, int smem = 0) {
   return std::max(1, std::min(g, ntasks));
 }
 
-void dev_factor(const DevSymb& S0, const DevPattern& P, DevFactor& F, const double* kvals, double pivot_tol,
-                cudaStream_t st) {
+static int g_fg = 0, g_fg2 = 0, g_sf = 0, g_sf2 = 0, g_sb = 0, g_sb2 = 0;
+constexpr int kFacSmem1 = 4 * kWarpFront * kWarpFront * sizeof(double);
+constexpr int kFacSmem2 = kCtaFront * kCtaFront * sizeof(double);
+static void init_grids() {
+  if (g_fg) return;
+  cudaFuncSetAttribute(factor_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFacSmem1);
+  cudaFuncSetAttribute(factor_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFacSmem2);
+  g_fg = persistent_grid(factor_kernel<32>, 128, 1 << 30, kFacSmem1);
+  g_fg2 = persistent_grid(factor_kernel<256>, 256, 1 << 30, kFacSmem2);
+  g_sf = persistent_grid(fwd_kernel<32>, 128, 1 << 30);
+  g_sf2 = persistent_grid(fwd_kernel<256>, 256, 1 << 30);
+  g_sb = persistent_grid(bwd_kernel<32>, 128, 1 << 30);
+  g_sb2 = persistent_grid(bwd_kernel<256>, 256, 1 << 30);
+}
+
+void dev_factor_begin(const DevSymb& S0, const DevPattern& P, DevFactor& F, const double* kvals, double pivot_tol,
+                      cudaStream_t st) {
   DevSymb& S = const_cast<DevSymb&>(S0);
+  init_grids();
   dev_max_abs_diag(P, kvals, F.scal + 1, st);
   COUNT(1);
   thresh_kernel<<<1, 1, 0, st>>>(F.scal, pivot_tol, F.istat, S.n);
   S.epoch++;
-  cudaMemsetAsync(S.tickets, 0, 4 * sizeof(int), st);
-  FactorArgs a{S, F.L, F.CB, F.D, kvals, F.scal, F.istat, S.flags, S.tickets + 0, S.epoch, 0, S.nsplit};
-  constexpr int smem1 = 4 * kWarpFront * kWarpFront * sizeof(double);
-  constexpr int smem2 = kCtaFront * kCtaFront * sizeof(double);
-  static int g = 0, g2 = 0;
-  if (!g) {
-    cudaFuncSetAttribute(factor_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1);
-    cudaFuncSetAttribute(factor_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
-    g = persistent_grid(factor_kernel<32>, 128, 1 << 30, smem1);
-    g2 = persistent_grid(factor_kernel<256>, 256, 1 << 30, smem2);
-  }
-  if (S.nsplit > 0) {
+  cudaMemsetAsync(S.tickets, 0, kTickets * sizeof(int), st);
+}
+
+void dev_factor_list(const DevSymb& S, DevFactor& F, const double* kvals, const DevTasks& T, int slot,
+                     cudaStream_t st) {
+  if (T.n == 0) return;
+  FactorArgs a{S, F.L, F.CB, F.D, kvals, F.scal, F.istat, S.flags, S.tickets + 2 * slot, S.epoch, 0, T.split,
+               T.ids, T.nleaf};
+  if (T.split > 0) {
     COUNT(1);
-    factor_kernel<32><<<g, 128, smem1, st>>>(a);
+    factor_kernel<32><<<g_fg, 128, kFacSmem1, st>>>(a);
   }
-  if (S.nsplit < S.nsn) {
-    a.ticket = S.tickets + 1;
-    a.t0 = S.nsplit;
-    a.t1 = S.nsn;
+  if (T.split < T.n) {
+    a.ticket = S.tickets + 2 * slot + 1;
+    a.t0 = T.split;
+    a.t1 = T.n;
     COUNT(1);
-    factor_kernel<256><<<std::min(g2, S.nsn - S.nsplit), 256, smem2, st>>>(a);
+    factor_kernel<256><<<std::min(g_fg2, T.n - T.split), 256, kFacSmem2, st>>>(a);
   }
 }
 
-void dev_inertia(const DevSymb& S, DevFactor& F, cudaStream_t st) {
+void dev_factor(const DevSymb& S, const DevPattern& P, DevFactor& F, const double* kvals, double pivot_tol,
+                cudaStream_t st) {
+  dev_factor_begin(S, P, F, kvals, pivot_tol, st);
+  dev_factor_list(S, F, kvals, DevTasks{S.order, S.nsn, S.nleaf, S.nsplit}, 0, st);
+}
+
+void dev_inertia(const DevSymb& S, DevFactor& F, cudaStream_t st, const uint8_t* report) {
   COUNT(1);
-  inertia_kernel<<<grid_for(S.n, 256), 256, 0, st>>>(F.D, S.n, F.scal, F.istat);
+  inertia_kernel<<<grid_for(S.n, 256), 256, 0, st>>>(F.D, S.n, F.scal, F.istat, report);
 }
 
-void dev_solve(const DevSymb& S0, DevFactor& F, const double* b, double* x, cudaStream_t st) {
+void dev_solve_begin(const DevSymb& S0, cudaStream_t st) {
   DevSymb& S = const_cast<DevSymb&>(S0);
-  if (S.n == 0) return;
+  init_grids();
   S.epoch++;
-  cudaMemsetAsync(S.tickets, 0, 4 * sizeof(int), st);
-  static int gf = 0, gf2 = 0, gb = 0, gb2 = 0;
-  if (!gf) {
-    gf = persistent_grid(fwd_kernel<32>, 128, 1 << 30);
-    gf2 = persistent_grid(fwd_kernel<256>, 256, 1 << 30);
-    gb = persistent_grid(bwd_kernel<32>, 128, 1 << 30);
-    gb2 = persistent_grid(bwd_kernel<256>, 256, 1 << 30);
-  }
-  const int ntop = S.nsn - S.nsplit;
-  SolveArgs fa{S, F.L, F.D, F.CV, F.xp, b, x, S.flags + S.nsn, S.tickets + 0, S.epoch, 0, S.nsplit};
-  if (S.nsplit > 0) COUNT(1), fwd_kernel<32><<<gf, 128, 0, st>>>(fa);
-  if (ntop > 0) {
-    fa.ticket = S.tickets + 1;
-    fa.t0 = S.nsplit;
-    fa.t1 = S.nsn;
+  cudaMemsetAsync(S.tickets, 0, kTickets * sizeof(int), st);
+}
+
+void dev_solve_fwd_list(const DevSymb& S, DevFactor& F, const double* b, const DevTasks& T, int slot,
+                        cudaStream_t st) {
+  if (T.n == 0) return;
+  SolveArgs fa{S, F.L, F.D, F.CV, F.xp, b, nullptr, S.flags + S.nsn, S.tickets + 2 * slot, S.epoch, 0, T.split,
+               T.ids, T.nleaf};
+  if (T.split > 0) COUNT(1), fwd_kernel<32><<<g_sf, 128, 0, st>>>(fa);
+  if (T.split < T.n) {
+    fa.ticket = S.tickets + 2 * slot + 1;
+    fa.t0 = T.split;
+    fa.t1 = T.n;
     COUNT(1);
-    fwd_kernel<256><<<std::min(gf2, ntop), 256, 0, st>>>(fa);
+    fwd_kernel<256><<<std::min(g_sf2, T.n - T.split), 256, 0, st>>>(fa);
   }
-  SolveArgs ba{S, F.L, F.D, F.CV, F.xp, b, x, S.flags + 2 * S.nsn, S.tickets + 2, S.epoch, S.nsplit, S.nsn};
-  if (ntop > 0) COUNT(1), bwd_kernel<256><<<std::min(gb2, ntop), 256, 0, st>>>(ba);
-  if (S.nsplit > 0) {
-    ba.ticket = S.tickets + 3;
+}
+
+// backward over one list, roots first (the CTA part first, then the warp part)
+void dev_solve_bwd_list(const DevSymb& S, DevFactor& F, double* x, const DevTasks& T, int slot, cudaStream_t st) {
+  if (T.n == 0) return;
+  SolveArgs ba{S, F.L, F.D, F.CV, F.xp, nullptr, x, S.flags + 2 * S.nsn, S.tickets + 2 * slot, S.epoch, T.split,
+               T.n, T.ids, T.nleaf};
+  if (T.split < T.n) COUNT(1), bwd_kernel<256><<<std::min(g_sb2, T.n - T.split), 256, 0, st>>>(ba);
+  if (T.split > 0) {
+    ba.ticket = S.tickets + 2 * slot + 1;
     ba.t0 = 0;
-    ba.t1 = S.nsplit;
+    ba.t1 = T.split;
     COUNT(1);
-    bwd_kernel<32><<<gb, 128, 0, st>>>(ba);
+    bwd_kernel<32><<<g_sb, 128, 0, st>>>(ba);
   }
+}
+
+void dev_solve(const DevSymb& S, DevFactor& F, const double* b, double* x, cudaStream_t st) {
+  if (S.n == 0) return;
+  dev_solve_begin(S, st);
+  const DevTasks all{S.order, S.nsn, S.nleaf, S.nsplit};
+  dev_solve_fwd_list(S, F, b, all, 0, st);
+  dev_solve_bwd_list(S, F, x, all, 2, st);
 }
 
 void dev_spmv(const DevPattern& P, const double* kvals, const double* x, double* y, cudaStream_t st) {
