@@ -13,10 +13,12 @@ timed region). `--impl reference` times the reference's own CPU
 factorize + solve (oracle/_ref, compiled from /root/reference/proj/src) on
 the same matrix — rank 0 only.
 
-Multi-GPU: the contingency blocks shard, but the sharded factorization is
-not built yet; until then N>1 runs N independent
-replicas ("scaling": "weak", one matrix per GPU) and reports the max-over-
-ranks time.
+Multi-GPU (torchrun, one rank per GPU): the same KKT is factored and solved
+contingency-sharded (include/nclopf_dist.h): each rank factors its block of
+contingency subtrees, the subtree-root contribution blocks are all-gathered
+over NVLink by the library's NCCL communicator, the separator is factored
+redundantly ("scaling": "strong", time = max over ranks). The end-to-end NCL
+solve (time_to_solve) runs on rank 0 only; the IPM itself is not sharded.
 """
 from __future__ import annotations
 
@@ -162,7 +164,7 @@ def run_reference(a, world):
     ms = 1e3 * sum(times) / len(times)
     line = {"metric": METRIC, "impl": "reference", "value": ms, "unit": "ms/IPM-iter (KKT factor+solve)",
             "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{a.grid}x{a.K} condensed KKT factor+solve", "N": n, "nnzK": A.nnz()},
             "cpu_baseline": {"value": ms, "unit": "ms/IPM-iter (KKT factor+solve)", "cores": 1,
                              "kind": "reference", "sample": f"{a.steps} factorize+solve of the {a.grid}x{a.K} KKT"},
@@ -206,11 +208,30 @@ def main():
     x_d = torch.empty_like(b_d)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
 
+    plan = None
+    if world > 1:
+        # contingency-sharded factor/solve over the library's NCCL communicator
+        from paper_2510_13333_b200.dist import ShardPlan, init_nccl, var_groups
+        init_nccl(world, rank, dist)
+        plan = ShardPlan(S, var_groups(P["scopf"]), a.K + 1, world, rank)
+
+    def refactor():
+        if plan is not None:
+            plan.refactorize(F, A)
+        else:
+            F.refactorize(A)
+
+    def solve(x, where):
+        if plan is not None:
+            plan.solve_in_place(F, x, where)
+        else:
+            F.solve_in_place(x, where=where)
+
     def step_device():
-        F.refactorize(A)
+        refactor()
         with torch.cuda.stream(stream):
             x_d.copy_(b_d)
-        F.solve_in_place(x_d, where=ps.DEVICE)
+        solve(x_d, ps.DEVICE)
 
     torch.cuda.synchronize()
     for _ in range(a.warmup):
@@ -229,11 +250,11 @@ def main():
             with torch.cuda.stream(stream):
                 flush.fill_(1.0)
                 e0.record(stream)
-            F.refactorize(A)
+            refactor()
             with torch.cuda.stream(stream):
                 e1.record(stream)
                 x_d.copy_(b_d)
-            F.solve_in_place(x_d, where=ps.DEVICE)
+            solve(x_d, ps.DEVICE)
             with torch.cuda.stream(stream):
                 e2.record(stream)
         torch.cuda.synchronize()
@@ -251,9 +272,9 @@ def main():
     x_h = torch.empty(n, dtype=torch.float64).pin_memory()
     for _ in range(2):
         A.set_values(vals_h, where=ps.HOST)
-        F.refactorize(A)
+        refactor()
         x_h.copy_(b_h)
-        F.solve_in_place(x_h, where=ps.HOST)
+        solve(x_h, ps.HOST)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -264,9 +285,9 @@ def main():
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         A.set_values(vals_h, where=ps.HOST)  # H2D of K's values
-        F.refactorize(A)
+        refactor()
         x_h.copy_(b_h)
-        F.solve_in_place(x_h, where=ps.HOST)  # H2D of b, D2H of x (synchronous)
+        solve(x_h, ps.HOST)  # H2D of b, D2H of x (synchronous)
         sp, zp, *_ = F._status()  # D2H of status + inertia
         e2e.append(time.perf_counter() - t0)
     e2e_ms = 1e3 * sum(e2e) / len(e2e)
@@ -288,7 +309,7 @@ def main():
 
     # ---- time to solve: the whole NCL/IPM solve of the same SCOPF on this GPU
     tts = None
-    if not a.no_solve:
+    if not a.no_solve and rank == 0:
         from paper_2510_13333_b200.ipm import NclSolver, default_options
 
         del F  # free the bench factor before the solver allocates its own
@@ -301,11 +322,7 @@ def main():
         t_solve = time.perf_counter() - t0
         r = out.result
         its = max(1, r["inner_iters"])
-        if dist:
-            t = torch.tensor([t_solve], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            t_solve = float(t.item())
-        tts = {"seconds": t_solve, "status": out.status, "outer_iters": r["outer_iters"],
+        tts = {"seconds": t_solve, "gpus": 1, "status": out.status, "outer_iters": r["outer_iters"],
                "inner_iters": r["inner_iters"], "factorizations": r["factorizations"],
                "objective": r["objective"], "r_inf": r["r_inf"], "inf_pr": r["inf_pr"], "inf_du": r["inf_du"],
                "analyze_s": r["t_init"],
@@ -335,11 +352,12 @@ def main():
         line = {
             "metric": METRIC, "value": step_ms, "unit": "ms/IPM-iter (KKT factor+solve)", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": step_ms, "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{a.grid}x{a.K} condensed KKT factor+solve (paper layout, seed {SEED})",
                        "N": n, "nnzK": nnzk, "l_nnz": info.l_nnz, "supernodes": info.nsupernodes,
                        "sn_height": info.max_height, "flops": info.flops, "l2": "flushed (256 MiB write) between steps",
-                       "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "parallelism": f"contingency-sharded x{world} (NCCL all-gather of subtree-root CBs)"
+                       if world > 1 else "single",
                        "factor_ms": sum(fact_ms) / a.steps, "solve_ms": sum(solve_ms) / a.steps,
                        "status": "ok" if st[0] == 0 else "zero_pivot",
                        "inertia": [st[2].n_pos, st[2].n_neg, st[2].n_zero],

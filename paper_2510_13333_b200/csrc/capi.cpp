@@ -355,6 +355,7 @@ API int ncl_sym_write_matrix_market(ncl_sym_t M, char* buf, int64_t cap, int64_t
 struct ncl_symb {
   SymbolicCore core;
   Supernodal Z;
+  TopSched top;  // level schedule of the CTA part (large fronts -> blocked DMMA path)
   uint64_t hash = 0;
   int nnz = 0;
   DevSymb d;
@@ -364,6 +365,31 @@ struct ncl_symb {
 };
 
 namespace {
+constexpr int kSmemFrontCap = 160;  // = kCtaFront in csrc/cuda/ldlt.cu
+TopSched build_top(const Supernodal& Z, const std::vector<int>& ids, int split) {
+  TopSched t;
+  for (int i = split; i < static_cast<int>(ids.size());) {
+    const int h = Z.height[ids[i]];
+    int e = i;
+    std::vector<int> big;
+    while (e < static_cast<int>(ids.size()) && Z.height[ids[e]] == h) {
+      const int s = ids[e];
+      const int nr = static_cast<int>(Z.sn_rptr[s + 1] - Z.sn_rptr[s]);
+      if (nr > kSmemFrontCap) {
+        big.insert(big.end(), {s, Z.sn_first[s], Z.sn_first[s + 1] - Z.sn_first[s], nr});
+        t.any_big = true;
+        t.max_nr = std::max(t.max_nr, nr);
+      }
+      ++e;
+    }
+    t.lvl_begin.push_back(i);
+    t.lvl_end.push_back(e);
+    t.big.push_back(std::move(big));
+    i = e;
+  }
+  return t;
+}
+
 void upload_symb(ncl_symb* S) {
   if (S->dev_ready) return;
   ensure_init();
@@ -453,6 +479,7 @@ ncl_symb* analyze_impl(ncl_sym_t M, const int* perm) {
   auto S = std::make_unique<ncl_symb>();
   S->core = analyze_core(n, M->pat.col_ptr(), M->pat.row_ind(), std::move(p));
   S->Z = build_supernodes(S->core, M->pat.col_ptr(), M->pat.row_ind());
+  S->top = build_top(S->Z, S->Z.order, S->Z.nsplit);
   S->hash = M->hash;
   S->nnz = M->pat.nnz();
   return S.release();
@@ -511,7 +538,7 @@ struct ncl_fact {
   ncl_symb* S = nullptr;
   std::unique_ptr<ncl_symb> owned;
   DevFactor F;
-  DevBuf<double> L, CB, CV, D, xp, scal, work1, work2, work3;
+  DevBuf<double> L, CB, CV, D, xp, scal, work1, work2, work3, bigF, bigW;
   DevBuf<int> istat;
 };
 
@@ -536,13 +563,20 @@ void alloc_fact(ncl_fact* f) {
   f->F.L = f->L.p;
   f->F.CB = f->CB.p;
   f->F.CV = f->CV.p;
+  if (f->S->Z.max_nr > kSmemFrontCap) {  // scratch of the blocked large-front path
+    const int64_t mx = f->S->Z.max_nr;
+    f->bigF.alloc(mx * mx);
+    f->bigW.alloc(mx * 32);
+    f->F.bigF = f->bigF.p;
+    f->F.bigW = f->bigW.p;
+  }
   f->F.D = f->D.p;
   f->F.xp = f->xp.p;
   f->F.scal = f->scal.p;
   f->F.istat = f->istat.p;
 }
 void run_factor(ncl_fact* f, ncl_sym_t M, double tol) {
-  dev_factor(f->S->d, M->dp, f->F, M->vals.p, tol, g_stream);
+  dev_factor(f->S->d, M->dp, f->F, M->vals.p, tol, g_stream, &f->S->top);
   dev_inertia(f->S->d, f->F, g_stream);
   check_launch("factorize");
 }
@@ -792,6 +826,7 @@ struct ncl_shard {
   DevBuf<uint8_t> report;
   DevBuf<double> send, recv;
   DevBuf<int> unrep;  // original indices this rank does not report (zeroed before the x all-reduce)
+  TopSched topA, topB;
   int64_t nunrep = 0;
 };
 
@@ -821,10 +856,10 @@ void shard_upload(ncl_shard* sh) {
   sh->dev_ready = true;
 }
 DevTasks tasks_A(ncl_shard* sh) {
-  return DevTasks{sh->listA.p, static_cast<int>(sh->P.listA.size()), sh->P.nleafA, sh->P.splitA};
+  return DevTasks{sh->listA.p, static_cast<int>(sh->P.listA.size()), sh->P.nleafA, sh->P.splitA, &sh->topA};
 }
 DevTasks tasks_B(ncl_shard* sh) {
-  return DevTasks{sh->listB.p, static_cast<int>(sh->P.listB.size()), sh->P.nleafB, sh->P.splitB};
+  return DevTasks{sh->listB.p, static_cast<int>(sh->P.listB.size()), sh->P.nleafB, sh->P.splitB, &sh->topB};
 }
 void need_comm(const ncl_shard* sh) {
   if (sh->P.world == 1) return;
@@ -850,6 +885,8 @@ API int ncl_shard_create(ncl_symb_t S, const int* var_group, int ngroups, int wo
     sh->S = S;
     std::vector<int> g(var_group, var_group + S->core.n);
     sh->P = build_shard_plan(S->Z, S->core, g, ngroups, world, rank);
+    sh->topA = build_top(S->Z, sh->P.listA, sh->P.splitA);
+    sh->topB = build_top(S->Z, sh->P.listB, sh->P.splitB);
     *out = sh.release();
   });
 }

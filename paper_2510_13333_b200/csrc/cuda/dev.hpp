@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 namespace nclb {
 
@@ -54,6 +55,8 @@ struct DevFactor {
   double* L = nullptr;  // panels
   double* CB = nullptr; // contribution blocks (multifrontal Schur updates)
   double* CV = nullptr; // [rows] forward-solve contribution vectors
+  double* bigF = nullptr;  // scratch front of the blocked large-front path (max_nr^2)
+  double* bigW = nullptr;  // scratch W = L21 D (max_nr x 32)
   double* D = nullptr;  // [n] by pivot position
   double* xp = nullptr;  // [n] permuted work vector
   double* scal = nullptr;  // [4]: thresh, maxdiag, scratch
@@ -62,9 +65,19 @@ struct DevFactor {
 
 // A task list: supernode ids in leaves-first height order; the first
 // `nleaf` are leaves, tasks from `split` on run CTA-per-task.
+// Host-side schedule of the CTA part of a list when it holds fronts too large
+// for shared memory: per height level the [begin, end) index range in the
+// list and the large supernodes (s, f, w, nr) that run the blocked DMMA path.
+struct TopSched {
+  std::vector<int> lvl_begin, lvl_end;
+  std::vector<std::vector<int>> big;  // per level: quadruples (s, f, w, nr)
+  bool any_big = false;
+  int max_nr = 0;
+};
 struct DevTasks {
   const int* ids = nullptr;
   int n = 0, nleaf = 0, split = 0;
+  const TopSched* top = nullptr;  // host pointer; nullptr or !any_big -> one persistent launch
 };
 constexpr int kTickets = 40;  // ticket counters per symbolic handle
 
@@ -85,9 +98,11 @@ void dev_shard_pack(const DevSymb& S, const double* src, const int* bids, const 
 void dev_shard_unpack(const DevSymb& S, double* dst, const int* bids, const int* bowner, const int64_t* pack_off,
                       int nb, int rank, int cv, const double* recv, int64_t chunk, int* flags, int epoch,
                       cudaStream_t st);
+void dev_factor_big(const DevSymb& S, DevFactor& F, const double* kvals, int s, int f, int w, int nr, double* Fs,
+                    double* Wb, cudaStream_t st);
 void dev_zero_indexed(double* x, const int* idx, int64_t n, cudaStream_t st);
 void dev_factor(const DevSymb& S, const DevPattern& P, DevFactor& F, const double* kvals, double pivot_tol,
-                cudaStream_t st);
+                cudaStream_t st, const TopSched* top = nullptr);
 void dev_inertia(const DevSymb& S, DevFactor& F, cudaStream_t st, const uint8_t* report = nullptr);
 // x := M^{-1} b (in place allowed: x may alias b)
 void dev_solve(const DevSymb& S, DevFactor& F, const double* b, double* x, cudaStream_t st);

@@ -114,6 +114,7 @@ struct FactorArgs {
   int t0, t1;          // ticket range of this launch (indices into tasks)
   const int* tasks;    // supernode ids, leaves-first height order
   int nleaf;           // leaf tasks at the head of `tasks`
+  int skip_big;        // leave nr > kCtaFront to the blocked DMMA path
 };
 
 template <int NT>
@@ -293,7 +294,7 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT) factor_kernel(FactorArgs 
     const int s = __ldg(a.tasks + t);
     const int nr = static_cast<int>(__ldg(a.S.sn_rptr + s + 1) - __ldg(a.S.sn_rptr + s));
     if (nr <= (NT == 32 ? kWarpFront : kCtaFront)) factor_task_smem<NT>(a, s, tid, thresh, F);
-    else factor_task<NT>(a, s, tid, thresh);
+    else if (!a.skip_big) factor_task<NT>(a, s, tid, thresh);
   }
 }
 
@@ -623,10 +624,33 @@ void dev_factor_list(const DevSymb& S, DevFactor& F, const double* kvals, const 
                      cudaStream_t st) {
   if (T.n == 0) return;
   FactorArgs a{S, F.L, F.CB, F.D, kvals, F.scal, F.istat, S.flags, S.tickets + 2 * slot, S.epoch, 0, T.split,
-               T.ids, T.nleaf};
+               T.ids, T.nleaf, 0};
   if (T.split > 0) {
     COUNT(1);
     factor_kernel<32><<<g_fg, 128, kFacSmem1, st>>>(a);
+  }
+  if (T.top && T.top->any_big) {
+    // level by level: small fronts of the level in one persistent launch,
+    // then its large fronts on the blocked DMMA path
+    const TopSched& ts = *T.top;
+    a.skip_big = 1;
+    a.nleaf = 0;
+    for (size_t L = 0; L < ts.lvl_begin.size(); ++L) {
+      const int b = ts.lvl_begin[L], e = ts.lvl_end[L];
+      const int nsmall = (e - b) - static_cast<int>(ts.big[L].size() / 4);
+      if (nsmall > 0) {
+        cudaMemsetAsync(S.tickets + kTickets - 1, 0, sizeof(int), st);
+        a.ticket = S.tickets + kTickets - 1;
+        a.t0 = b;
+        a.t1 = e;
+        COUNT(1);
+        factor_kernel<256><<<std::min(g_fg2, e - b), 256, kFacSmem2, st>>>(a);
+      }
+      for (size_t q = 0; q < ts.big[L].size(); q += 4)
+        dev_factor_big(S, F, kvals, ts.big[L][q], ts.big[L][q + 1], ts.big[L][q + 2], ts.big[L][q + 3], F.bigF,
+                       F.bigW, st);
+    }
+    return;
   }
   if (T.split < T.n) {
     a.ticket = S.tickets + 2 * slot + 1;
@@ -638,9 +662,9 @@ void dev_factor_list(const DevSymb& S, DevFactor& F, const double* kvals, const 
 }
 
 void dev_factor(const DevSymb& S, const DevPattern& P, DevFactor& F, const double* kvals, double pivot_tol,
-                cudaStream_t st) {
+                cudaStream_t st, const TopSched* top) {
   dev_factor_begin(S, P, F, kvals, pivot_tol, st);
-  dev_factor_list(S, F, kvals, DevTasks{S.order, S.nsn, S.nleaf, S.nsplit}, 0, st);
+  dev_factor_list(S, F, kvals, DevTasks{S.order, S.nsn, S.nleaf, S.nsplit, top}, 0, st);
 }
 
 void dev_inertia(const DevSymb& S, DevFactor& F, cudaStream_t st, const uint8_t* report) {

@@ -142,3 +142,30 @@ def test_supernodal_wide_fronts(gpu):
     assert relerr(Fa.diagonal(), Fb.diagonal()) < 1e-10
     b = rng.standard_normal(150)
     assert relerr(ps.solve_refined(Fa, A, b).x, Fb.solve_refined(b)[0]) < 1e-9
+
+
+@pytest.mark.parametrize("n1,n2,dens", [(240, 60, 0.5), (420, 130, 0.3)])
+def test_large_front_dmma_path(gpu, n1, n2, dens):
+    """Dense quasi-definite blocks give fronts wider than the 160-row shared-
+    memory cap: the blocked FP64-DMMA path (csrc/cuda/bigfront.cu)."""
+    rng = np.random.default_rng(n1)
+    (r, c, v), K = matgen.quasi_definite(n1, n2, dens, rng)
+    n = n1 + n2
+    A, B = both(n, r, c, v)
+    Sa = ps.analyze(A)
+    assert Sa.info().max_rows > 160
+    Fa = ps.factorize(A, Sa)
+    Fb = RefFactorization(B, RefSymbolic(B))
+    assert Fa.status == Fb.status == "ok"
+    ia = Fa.inertia
+    assert (ia.n_pos, ia.n_neg, ia.n_zero) == Fb.inertia == (n1, n2, 0)
+    assert relerr(Fa.diagonal(), Fb.diagonal()) < 1e-10
+    b = rng.standard_normal(n)
+    assert relerr(Fa.solve(b), Fb.solve(b)) < 1e-8
+    lp, li, lx = Fa.L_csc()
+    rp, ri, rx = Fb.L_csc(Sa.l_nnz)
+    np.testing.assert_array_equal(li, ri)
+    assert relerr(lx, rx) < 1e-8
+    D1 = Fa.diagonal()
+    Fa.refactorize(A)
+    assert np.array_equal(Fa.diagonal(), D1)  # deterministic run to run

@@ -23,9 +23,24 @@ grid, need = sys.argv[1], int(sys.argv[2])
 seed = int(sys.argv[3]) if len(sys.argv) > 3 else 2510
 _lib.check(_lib.lib.ncl_init(0))
 probe = [int(l) for l in Scopf(grid, 0, seed=seed).candidates()]  # non-islanding, ascending
+os.makedirs(os.path.join(ROOT, "paper_2510_13333_b200", "data"), exist_ok=True)
+dst = os.path.join(ROOT, "paper_2510_13333_b200", "data", f"screened_{grid}_{seed}.json")
+out_dir = os.path.join(ROOT, "gpurun_out", "data")
+os.makedirs(out_dir, exist_ok=True)
 feasible, rejected, log = [], [], []
 t0 = time.time()
 opts = default_options(verbose=0, max_inner=600)
+
+
+def save():
+    doc = {"grid": grid, "seed": seed, "rule": "K=1 SCOPF reaches NCL optimality (default options, max_inner 600)",
+           "screened": len(log), "feasible": feasible, "rejected": rejected, "seconds": time.time() - t0,
+           "complete": len(feasible) >= need or len(log) == len(probe), "log": log}
+    for d in (dst, os.path.join(out_dir, os.path.basename(dst))):
+        with open(d, "w") as f:
+            json.dump(doc, f)
+
+
 for l in probe:
     s = Scopf(grid, 1, seed=seed, contingencies=[l])
     out = NclSolver(s.build_model(), s.bounds()).solve(opts)
@@ -33,12 +48,9 @@ for l in probe:
     (feasible if ok else rejected).append(l)
     log.append({"branch": l, "status": out.status, "inner": out.result["inner_iters"], "r_inf": out.result["r_inf"]})
     print(json.dumps(log[-1]), flush=True)
+    if len(log) % 10 == 0:
+        save()
     if len(feasible) >= need:
         break
-os.makedirs(os.path.join(ROOT, "paper_2510_13333_b200", "data"), exist_ok=True)
-dst = os.path.join(ROOT, "paper_2510_13333_b200", "data", f"screened_{grid}_{seed}.json")
-with open(dst, "w") as f:
-    json.dump({"grid": grid, "seed": seed, "rule": "K=1 SCOPF reaches NCL optimality (default options, max_inner 600)",
-               "screened": len(log), "feasible": feasible, "rejected": rejected, "seconds": time.time() - t0,
-               "log": log}, f)
+save()
 print(f"{len(feasible)} feasible / {len(log)} screened in {time.time() - t0:.1f}s -> {dst}")
