@@ -11,7 +11,8 @@ timeout 900 python bench.py ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/
 if [ -n "$NCU" ]; then
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
   python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-solve > gpurun_out/ncu_launch_bench.log 2>&1
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"${NCU_KERNEL:-factor_kernel}" -s 2 -c 1 \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"${NCU_KERNEL:-factor_kernel}" -s 2 -c ${NCU_COUNT:-2} \
   -o gpurun_out/prof_${NCU_NAME:-factor} -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-solve > gpurun_out/ncu_full.log 2>&1
 tail -3 gpurun_out/ncu_full.log
 fi
+if [ -n "$EXTRA" ]; then eval "$EXTRA"; fi
