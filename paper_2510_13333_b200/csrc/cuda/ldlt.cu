@@ -212,18 +212,48 @@ __device__ __forceinline__ void factor_task_smem(const FactorArgs& a, int s, int
   for (int64_t e = __ldg(S.aptr + s) + tid; e < __ldg(S.aptr + s + 1); e += NT)
     F[__ldg(S.aoff + e)] = __ldg(a.kvals + __ldg(S.asrc + e));  // panel offset c*nr + r == front offset
   team_sync<NT>();
-  for (int q = __ldg(S.cptr + s); q < __ldg(S.cptr + s + 1); ++q) {
-    const int c = __ldg(S.child + q);
-    const int wc = __ldg(S.sn_first + c + 1) - __ldg(S.sn_first + c);
-    const int64_t rbc = __ldg(S.sn_rptr + c);
-    const int m2c = static_cast<int>(__ldg(S.sn_rptr + c + 1) - rbc) - wc;
-    const int* rel = S.relp + rbc + wc;
-    const double* Cc = a.CB + __ldg(S.cb_off + c);
-    for (int e = tid; e < m2c * m2c; e += NT) {
-      const int i = e % m2c, j = e / m2c;
-      if (i >= j) F[__ldg(rel + j) * nr + __ldg(rel + i)] += __ldcg(Cc + e);
+  if constexpr (NT == 32) {
+    for (int q = __ldg(S.cptr + s); q < __ldg(S.cptr + s + 1); ++q) {
+      const int c = __ldg(S.child + q);
+      const int wc = __ldg(S.sn_first + c + 1) - __ldg(S.sn_first + c);
+      const int64_t rbc = __ldg(S.sn_rptr + c);
+      const int m2c = static_cast<int>(__ldg(S.sn_rptr + c + 1) - rbc) - wc;
+      const int* rel = S.relp + rbc + wc;
+      const double* Cc = a.CB + __ldg(S.cb_off + c);
+      for (int j = 0; j < m2c; ++j) {
+        const int rj = __ldg(rel + j);
+        for (int i = j + tid; i < m2c; i += 32) F[rj * nr + __ldg(rel + i)] += __ldcg(Cc + j * m2c + i);
+      }
+      __syncwarp();
     }
-    team_sync<NT>();
+  } else {
+    // warp `warp` owns front columns [warp*nr/8, (warp+1)*nr/8): every entry
+    // has one owner and sees the children in ascending order (deterministic)
+    // without a CTA barrier per child
+    const int lane = tid & 31, warp = tid >> 5, nw = NT / 32;
+    const int cb0 = (warp * nr) / nw, cb1 = ((warp + 1) * nr) / nw;
+    for (int q = __ldg(S.cptr + s); q < __ldg(S.cptr + s + 1); ++q) {
+      const int c = __ldg(S.child + q);
+      const int wc = __ldg(S.sn_first + c + 1) - __ldg(S.sn_first + c);
+      const int64_t rbc = __ldg(S.sn_rptr + c);
+      const int m2c = static_cast<int>(__ldg(S.sn_rptr + c + 1) - rbc) - wc;
+      const int* rel = S.relp + rbc + wc;
+      const double* Cc = a.CB + __ldg(S.cb_off + c);
+      int lo = 0, hi = m2c;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(rel + mid) < cb0) lo = mid + 1;
+        else hi = mid;
+      }
+      for (int j = lo; j < m2c; ++j) {
+        const int rj = __ldg(rel + j);
+        if (rj >= cb1) break;
+        double* Fj = F + rj * nr;
+        const double* Cj = Cc + j * m2c;
+        for (int i = j + lane; i < m2c; i += 32) Fj[__ldg(rel + i)] += __ldcg(Cj + i);
+      }
+    }
+    __syncthreads();
   }
   if constexpr (NT == 32) {
     const int i = tid;
@@ -246,19 +276,46 @@ __device__ __forceinline__ void factor_task_smem(const FactorArgs& a, int s, int
       __syncwarp();
     }
   } else {
-    for (int c = 0; c < w; ++c) {
-      double* Fc = F + c * nr;
-      const double d = Fc[c];
-      if (tid == 0) {
-        a.D[f + c] = d;
-        if (fabs(d) <= thresh) atomicMin(a.zp, f + c);
+    // blocked right-looking LDLᵀ, panels of kPb columns:
+    //  (a) warp 0 factors the panel (rows c0..nr) with __syncwarp only,
+    //  (b) all warps apply the rank-kPb update to the trailing lower
+    //      triangle: warps own columns j, lanes rows i >= j.
+    constexpr int kPb = 8;
+    const int lane = tid & 31, warp = tid >> 5;
+    for (int c0 = 0; c0 < w; c0 += kPb) {
+      const int c1 = min(w, c0 + kPb);
+      if (warp == 0) {
+        for (int c = c0; c < c1; ++c) {
+          double* Fc = F + c * nr;
+          const double d = Fc[c];
+          if (lane == 0) {
+            a.D[f + c] = d;
+            if (fabs(d) <= thresh) atomicMin(a.zp, f + c);
+          }
+          for (int i = c + 1 + lane; i < nr; i += 32) Fc[i] = Fc[i] / d;
+          __syncwarp();
+          for (int c2 = c + 1; c2 < c1; ++c2) {
+            const double dl = d * Fc[c2];
+            double* F2 = F + c2 * nr;
+            for (int i = c2 + lane; i < nr; i += 32) F2[i] -= Fc[i] * dl;
+          }
+          __syncwarp();
+        }
       }
-      for (int i = c + 1 + tid; i < nr; i += NT) Fc[i] = Fc[i] / d;
       __syncthreads();
-      const int rem = nr - c - 1;
-      for (int e = tid; e < rem * rem; e += NT) {
-        const int i = c + 1 + e % rem, c2 = c + 1 + e / rem;
-        if (i >= c2) F[c2 * nr + i] -= Fc[i] * (d * Fc[c2]);
+      const int kb = c1 - c0;
+      for (int j = c1 + warp; j < nr; j += NT / 32) {
+        double dlj[kPb];
+#pragma unroll
+        for (int k = 0; k < kPb; ++k) dlj[k] = k < kb ? F[(c0 + k) * nr + (c0 + k)] * F[(c0 + k) * nr + j] : 0.0;
+        double* Fj = F + j * nr;
+        for (int i = j + lane; i < nr; i += 32) {
+          double acc = 0.0;
+#pragma unroll
+          for (int k = 0; k < kPb; ++k)
+            if (k < kb) acc += F[(c0 + k) * nr + i] * dlj[k];
+          Fj[i] -= acc;
+        }
       }
       __syncthreads();
     }
@@ -266,9 +323,13 @@ __device__ __forceinline__ void factor_task_smem(const FactorArgs& a, int s, int
   double* P = a.L + __ldg(S.sn_loff + s);
   double* C = a.CB + __ldg(S.cb_off + s);
   for (int k = tid; k < w * nr; k += NT) P[k] = F[k];
-  for (int e = tid; e < m2 * m2; e += NT) {
-    const int i = e % m2, j = e / m2;
-    if (i >= j) C[e] = F[(w + j) * nr + (w + i)];
+  {
+    const int lane = tid & 31, warp = tid >> 5;
+    for (int j = warp; j < m2; j += NT / 32) {
+      const double* Fj = F + (w + j) * nr + w;
+      double* Cj = C + j * m2;
+      for (int i = j + lane; i < m2; i += 32) Cj[i] = Fj[i];
+    }
   }
   team_sync<NT>();
   if (tid == 0) {
