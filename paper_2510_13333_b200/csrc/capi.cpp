@@ -360,7 +360,8 @@ struct ncl_symb {
   int nnz = 0;
   DevSymb d;
   DevBuf<int> perm, sn_first, sn_parent, rows, relp, cptr, child, order, asrc, aoff, flags, tickets;
-  DevBuf<int64_t> sn_rptr, sn_loff, cb_off, aptr;
+  DevBuf<int64_t> sn_rptr, sn_loff, cb_off, aptr, gm_ptr, gsp, gsrc;
+  DevBuf<int> gdst;
   bool dev_ready = false;
 };
 
@@ -405,6 +406,10 @@ void upload_symb(ncl_symb* S) {
   S->sn_rptr.upload(Z.sn_rptr);
   S->sn_loff.upload(Z.sn_loff);
   S->cb_off.upload(Z.cb_off);
+  S->gm_ptr.upload(Z.gm_ptr);
+  S->gdst.upload(Z.gdst);
+  S->gsp.upload(Z.gsp);
+  S->gsrc.upload(Z.gsrc);
   // A entries grouped by target supernode, sorted by panel offset
   const int nsn = Z.nsn;
   std::vector<int64_t> aptr(nsn + 1, 0);
@@ -448,6 +453,10 @@ void upload_symb(ncl_symb* S) {
   d.sn_loff = S->sn_loff.p;
   d.relp = S->relp.p;
   d.cb_off = S->cb_off.p;
+  d.gm_ptr = S->gm_ptr.p;
+  d.gdst = S->gdst.p;
+  d.gsp = S->gsp.p;
+  d.gsrc = S->gsrc.p;
   d.cptr = S->cptr.p;
   d.child = S->child.p;
   d.order = S->order.p;

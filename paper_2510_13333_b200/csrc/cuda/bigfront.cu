@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(256) bf_assemble(BigArgs a) {
     for (int j = lo; j < j1; ++j) {
       const int rj = __ldg(rel + j);
       double* Fj = a.F + static_cast<int64_t>(rj) * nr;
-      const double* Cj = Cc + static_cast<int64_t>(j) * m2c;
+      const double* Cj = Cc + cb_col(j, m2c);
       for (int i = j + threadIdx.x; i < m2c; i += blockDim.x) Fj[__ldg(rel + i)] += __ldcg(Cj + i);
     }
     __syncthreads();
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(256) bf_writeout(BigArgs a, int* flags, int ep
     } else {
       const int64_t k = e - np;
       const int i = static_cast<int>(k % m2), j = static_cast<int>(k / m2);
-      if (i >= j) C[k] = a.F[static_cast<int64_t>(w + j) * nr + (w + i)];
+      if (i >= j) C[cb_col(j, m2) + i] = a.F[static_cast<int64_t>(w + j) * nr + (w + i)];
     }
   }
 }

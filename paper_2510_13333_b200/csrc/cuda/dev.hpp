@@ -9,6 +9,13 @@
 
 namespace nclb {
 
+// Contribution blocks are packed lower-triangular, column-major: column j of
+// an m x m block holds rows j..m-1 contiguously; entry (i, j) is at
+// cb_col(j, m) + i.
+__host__ __device__ inline int64_t cb_col(int j, int m) {
+  return static_cast<int64_t>(j) * m - static_cast<int64_t>(j) * (j + 1) / 2;
+}
+
 // Number of library kernel launches issued so far (evidence for the bench's
 // gpu_launches key). Incremented by every dev_* wrapper.
 extern int64_t g_kernel_launches;
@@ -26,6 +33,10 @@ struct DevSymb {
   int* relp = nullptr;       // [rows] child row -> position in the parent's row list
   int64_t* cb_off = nullptr; // [nsn+1] contribution-block offsets ((nr-w)^2 each)
   int64_t cb_storage = 0;
+  int64_t* gm_ptr = nullptr;  // [nsn+1] gather-map entry ranges (CTA-part fronts)
+  int* gdst = nullptr;        // front position of each gather entry
+  int64_t* gsp = nullptr;     // [entries+1] source ranges
+  int64_t* gsrc = nullptr;    // ~A slot or global CB index
   int* cptr = nullptr;  // children CSR
   int* child = nullptr;
   int* order = nullptr;  // ticket order, leaves first

@@ -132,7 +132,7 @@ __device__ __forceinline__ void factor_task(const FactorArgs& a, int s, int tid,
   double* C = a.CB + __ldg(S.cb_off + s);
   // 2. clear, scatter A (each panel entry holds at most one A entry)
   for (int i = tid; i < w * nr; i += NT) P[i] = 0.0;
-  for (int i = tid; i < m2 * m2; i += NT) C[i] = 0.0;
+  for (int i = tid; i < m2 * (m2 + 1) / 2; i += NT) C[i] = 0.0;
   team_sync<NT>();
   for (int64_t e = __ldg(S.aptr + s) + tid; e < __ldg(S.aptr + s + 1); e += NT)
     P[__ldg(S.aoff + e)] = __ldg(a.kvals + __ldg(S.asrc + e));
@@ -150,9 +150,9 @@ __device__ __forceinline__ void factor_task(const FactorArgs& a, int s, int tid,
       const int rj = __ldg(rel + j);
       for (int i = j + tid; i < m2c; i += NT) {
         const int ri = __ldg(rel + i);
-        const double v = __ldcg(Cc + static_cast<int64_t>(j) * m2c + i);
+        const double v = __ldcg(Cc + cb_col(j, m2c) + i);
         if (rj < w) P[static_cast<int64_t>(rj) * nr + ri] += v;
-        else C[static_cast<int64_t>(rj - w) * m2 + (ri - w)] += v;
+        else C[cb_col(rj - w, m2) + (ri - w)] += v;
       }
     }
     team_sync<NT>();
@@ -183,7 +183,7 @@ __device__ __forceinline__ void factor_task(const FactorArgs& a, int s, int tid,
       const double* Pc = P + static_cast<int64_t>(c) * nr;
       acc += Pc[w + i] * (Pc[c] * Pc[w + j]);
     }
-    C[e] -= acc;
+    C[cb_col(j, m2) + i] -= acc;
   }
   team_sync<NT>();
   if (tid == 0) {
@@ -209,6 +209,20 @@ __device__ __forceinline__ void factor_task_smem(const FactorArgs& a, int s, int
   const int m2 = nr - w;
   for (int k = tid; k < nr * nr; k += NT) F[k] = 0.0;
   team_sync<NT>();
+  const int64_t g0 = NT == 32 ? 0 : __ldg(S.gm_ptr + s), g1 = NT == 32 ? 0 : __ldg(S.gm_ptr + s + 1);
+  if (g1 > g0) {
+    // gather-sum per front entry: A value first, then the children's CB
+    // entries in ascending child order (the extend-add order)
+    for (int64_t k = g0 + tid; k < g1; k += NT) {
+      double acc = 0.0;
+      for (int64_t q = __ldg(S.gsp + k); q < __ldg(S.gsp + k + 1); ++q) {
+        const int64_t src = __ldg(S.gsrc + q);
+        acc += src < 0 ? __ldg(a.kvals + ~src) : __ldcg(a.CB + src);
+      }
+      F[__ldg(S.gdst + k)] = acc;
+    }
+    team_sync<NT>();
+  } else {
   for (int64_t e = __ldg(S.aptr + s) + tid; e < __ldg(S.aptr + s + 1); e += NT)
     F[__ldg(S.aoff + e)] = __ldg(a.kvals + __ldg(S.asrc + e));  // panel offset c*nr + r == front offset
   team_sync<NT>();
@@ -222,7 +236,7 @@ __device__ __forceinline__ void factor_task_smem(const FactorArgs& a, int s, int
       const double* Cc = a.CB + __ldg(S.cb_off + c);
       for (int j = 0; j < m2c; ++j) {
         const int rj = __ldg(rel + j);
-        for (int i = j + tid; i < m2c; i += 32) F[rj * nr + __ldg(rel + i)] += __ldcg(Cc + j * m2c + i);
+        for (int i = j + tid; i < m2c; i += 32) F[rj * nr + __ldg(rel + i)] += __ldcg(Cc + cb_col(j, m2c) + i);
       }
       __syncwarp();
     }
@@ -249,12 +263,13 @@ __device__ __forceinline__ void factor_task_smem(const FactorArgs& a, int s, int
         const int rj = __ldg(rel + j);
         if (rj >= cb1) break;
         double* Fj = F + rj * nr;
-        const double* Cj = Cc + j * m2c;
+        const double* Cj = Cc + cb_col(j, m2c);
         for (int i = j + lane; i < m2c; i += 32) Fj[__ldg(rel + i)] += __ldcg(Cj + i);
       }
     }
     __syncthreads();
   }
+  }  // scatter / extend-add path
   if constexpr (NT == 32) {
     const int i = tid;
     for (int c = 0; c < w; ++c) {
@@ -327,7 +342,7 @@ __device__ __forceinline__ void factor_task_smem(const FactorArgs& a, int s, int
     const int lane = tid & 31, warp = tid >> 5;
     for (int j = warp; j < m2; j += NT / 32) {
       const double* Fj = F + (w + j) * nr + w;
-      double* Cj = C + j * m2;
+      double* Cj = C + cb_col(j, m2);
       for (int i = j + lane; i < m2; i += 32) Cj[i] = Fj[i];
     }
   }

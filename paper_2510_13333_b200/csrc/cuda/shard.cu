@@ -17,7 +17,7 @@ namespace {
 __device__ __forceinline__ int64_t blk_size(const DevSymb& S, int s, int cv) {
   const int w = __ldg(S.sn_first + s + 1) - __ldg(S.sn_first + s);
   const int64_t m2 = (__ldg(S.sn_rptr + s + 1) - __ldg(S.sn_rptr + s)) - w;
-  return cv ? m2 : m2 * m2;
+  return cv ? m2 : m2 * (m2 + 1) / 2;
 }
 __device__ __forceinline__ int64_t blk_off(const DevSymb& S, int s, int cv) {
   if (!cv) return __ldg(S.cb_off + s);

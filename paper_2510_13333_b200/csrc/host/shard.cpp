@@ -9,22 +9,14 @@ namespace nclb {
 
 namespace {
 constexpr int kMixed = -2;
-constexpr int kTopTasks = 2048;  // same narrow-top rule as build_supernodes
 
-// index in `list` (height-sorted) where the CTA-per-task part starts
-int split_of(const std::vector<int>& list, const std::vector<int>& height) {
-  if (list.empty()) return 0;
-  const int hmax = height[list.back()];
-  std::vector<int> cnt(hmax + 2, 0);
-  for (int s : list) cnt[height[s]]++;
-  int tail = 0, hs = hmax + 1;
-  for (int h = hmax; h >= 0; --h) {
-    if (tail + cnt[h] > kTopTasks) break;
-    tail += cnt[h];
-    hs = h;
-  }
+// index in `list` (height-sorted) where the CTA-per-task part starts: the
+// GLOBAL split height of the unsharded schedule, so every supernode is
+// processed by the same team kind — hence the same arithmetic — for every
+// number of ranks (bitwise G-independence)
+int split_of(const std::vector<int>& list, const std::vector<int>& height, int hsplit) {
   int i = 0;
-  while (i < static_cast<int>(list.size()) && height[list[i]] < hs) ++i;
+  while (i < static_cast<int>(list.size()) && height[list[i]] < hsplit) ++i;
   return i;
 }
 int leaves_of(const std::vector<int>& list, const std::vector<int>& height) {
@@ -75,8 +67,9 @@ ShardPlan build_shard_plan(const Supernodal& Z, const SymbolicCore& S, const std
   }
   P.nleafA = leaves_of(P.listA, Z.height);
   P.nleafB = leaves_of(P.listB, Z.height);
-  P.splitA = split_of(P.listA, Z.height);
-  P.splitB = split_of(P.listB, Z.height);
+  const int hsplit = Z.nsplit < nsn ? Z.height[Z.order[Z.nsplit]] : Z.max_height + 1;
+  P.splitA = split_of(P.listA, Z.height, hsplit);
+  P.splitB = split_of(P.listB, Z.height, hsplit);
   // boundary children and packing offsets per owning rank
   std::vector<int64_t> cbfill(world, 0), cvfill(world, 0);
   for (int s = 0; s < nsn; ++s) {
@@ -89,7 +82,7 @@ ShardPlan build_shard_plan(const Supernodal& Z, const SymbolicCore& S, const std
     P.bowner.push_back(q);
     P.cb_pack_off.push_back(cbfill[q]);
     P.cv_pack_off.push_back(cvfill[q]);
-    cbfill[q] += m2 * m2;
+    cbfill[q] += m2 * (m2 + 1) / 2;
     cvfill[q] += m2;
   }
   for (int q = 0; q < world; ++q) {

@@ -467,7 +467,7 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
     const int64_t w = Z.sn_first[s + 1] - Z.sn_first[s];
     const int64_t nr = static_cast<int64_t>(R[s].size());
     Z.sn_loff[s + 1] = Z.sn_loff[s] + w * nr;
-    Z.cb_off[s + 1] = Z.cb_off[s] + (nr - w) * (nr - w);
+    Z.cb_off[s + 1] = Z.cb_off[s] + (nr - w) * (nr - w + 1) / 2;  // packed lower, column-major
     Z.max_w = std::max<int>(Z.max_w, static_cast<int>(w));
     Z.max_nr = std::max<int>(Z.max_nr, static_cast<int>(nr));
   }
@@ -529,6 +529,73 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
       const int pos = static_cast<int>(std::lower_bound(rb, rb + nr, hi) - rb);
       Z.amap[p] = Z.sn_loff[s] + static_cast<int64_t>(lo - f) * nr + pos;
     }
+  // 7. gather maps of the CTA-part shared-memory fronts (order >= nsplit,
+  //    nr <= kGatherFront): for every front entry that receives anything,
+  //    its sources in assembly order — the A value (encoded ~slot) first, then
+  //    the children's packed CB entries in ascending child order — so the
+  //    assembly is one independent gather-sum per entry (no per-child
+  //    barriers; same summation order as the scatter/extend-add path).
+  {
+    constexpr int kGatherFront = 160;
+    Z.gm_ptr.assign(nsn + 1, 0);
+    std::vector<std::vector<int64_t>> asrc_of(nsn);
+    std::vector<std::vector<int>> adst_of(nsn);
+    std::vector<uint8_t> want(nsn, 0);
+    for (int t = Z.nsplit; t < nsn; ++t) {
+      const int sn = Z.order[t];
+      if (Z.sn_rptr[sn + 1] - Z.sn_rptr[sn] <= kGatherFront) want[sn] = 1;
+    }
+    for (int64_t p = 0; p < static_cast<int64_t>(Z.amap.size()); ++p) {
+      const int64_t off = Z.amap[p];
+      const int sn = static_cast<int>(std::upper_bound(Z.sn_loff.begin(), Z.sn_loff.end(), off) - Z.sn_loff.begin()) - 1;
+      if (!want[sn]) continue;
+      adst_of[sn].push_back(static_cast<int>(off - Z.sn_loff[sn]));
+      asrc_of[sn].push_back(p);
+    }
+    std::vector<int> cnt;
+    for (int sn = 0; sn < nsn; ++sn) {
+      if (!want[sn]) {
+        Z.gm_ptr[sn + 1] = Z.gm_ptr[sn];
+        continue;
+      }
+      const int nr = static_cast<int>(Z.sn_rptr[sn + 1] - Z.sn_rptr[sn]);
+      cnt.assign(static_cast<size_t>(nr) * nr + 1, 0);
+      for (int d : adst_of[sn]) cnt[d + 1]++;
+      for (int q = Z.cptr[sn]; q < Z.cptr[sn + 1]; ++q) {
+        const int c = Z.child[q];
+        const int wc = Z.sn_first[c + 1] - Z.sn_first[c];
+        const int m2c = static_cast<int>(Z.sn_rptr[c + 1] - Z.sn_rptr[c]) - wc;
+        const int* rel = Z.relp.data() + Z.sn_rptr[c] + wc;
+        for (int j = 0; j < m2c; ++j)
+          for (int i = j; i < m2c; ++i) cnt[static_cast<size_t>(rel[j]) * nr + rel[i] + 1]++;
+      }
+      // CSR over the entries that receive something, in front order
+      std::vector<int64_t> start(static_cast<size_t>(nr) * nr + 1, 0);
+      for (size_t d = 0; d < static_cast<size_t>(nr) * nr; ++d) start[d + 1] = start[d] + cnt[d + 1];
+      const int64_t nsrc = start.back();
+      const int64_t base = static_cast<int64_t>(Z.gsrc.size());
+      Z.gsrc.resize(base + nsrc);
+      std::vector<int64_t> fill(start.begin(), start.end() - 1);
+      for (size_t k = 0; k < adst_of[sn].size(); ++k) Z.gsrc[base + fill[adst_of[sn][k]]++] = ~asrc_of[sn][k];
+      for (int q = Z.cptr[sn]; q < Z.cptr[sn + 1]; ++q) {
+        const int c = Z.child[q];
+        const int wc = Z.sn_first[c + 1] - Z.sn_first[c];
+        const int m2c = static_cast<int>(Z.sn_rptr[c + 1] - Z.sn_rptr[c]) - wc;
+        const int* rel = Z.relp.data() + Z.sn_rptr[c] + wc;
+        for (int j = 0; j < m2c; ++j) {
+          const int64_t colb = Z.cb_off[c] + static_cast<int64_t>(j) * m2c - static_cast<int64_t>(j) * (j + 1) / 2;
+          for (int i = j; i < m2c; ++i) Z.gsrc[base + fill[static_cast<size_t>(rel[j]) * nr + rel[i]]++] = colb + i;
+        }
+      }
+      for (size_t d = 0; d < static_cast<size_t>(nr) * nr; ++d)
+        if (cnt[d + 1]) {
+          Z.gdst.push_back(static_cast<int>(d));
+          Z.gsp.push_back(base + start[d]);
+        }
+      Z.gm_ptr[sn + 1] = static_cast<int64_t>(Z.gdst.size());
+    }
+    Z.gsp.push_back(static_cast<int64_t>(Z.gsrc.size()));
+  }
   double fl = 0.0;
   for (int j = 0; j < n; ++j) {
     const double c = S.l_colcount[j];

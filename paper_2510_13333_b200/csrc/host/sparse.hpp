@@ -94,7 +94,7 @@ struct Supernodal {
   std::vector<int> rows;         // row structure R_s (permuted, ascending; starts with the s columns)
   std::vector<int> relp;         // [rows] position of a child row (k >= w) in the parent's R
   std::vector<int64_t> sn_loff;  // [nsn+1] offsets of dense column-major panels (nr x w)
-  std::vector<int64_t> cb_off;   // [nsn+1] offsets of contribution blocks ((nr-w)^2)
+  std::vector<int64_t> cb_off;   // [nsn+1] offsets of packed-lower contribution blocks (m2 (m2+1)/2)
   int64_t l_storage = 0, cb_storage = 0;
   // children lists (supernode etree)
   std::vector<int> cptr, child;
@@ -106,6 +106,11 @@ struct Supernodal {
   std::vector<int64_t> amap;
   // diagonal entry positions of the source CSC (for max|diag|)
   std::vector<int> diag_pos;
+  // gather maps of the CTA-part shared-memory fronts (see build_supernodes §7):
+  // supernode s owns front entries gdst[gm_ptr[s] .. gm_ptr[s+1]); entry k sums
+  // gsrc[gsp[k] .. gsp[k+1]) (~slot = A value, else a global CB index)
+  std::vector<int64_t> gm_ptr, gsp, gsrc;
+  std::vector<int> gdst;
   int max_w = 0, max_nr = 0;
   double flops = 0.0;  // sum_j (c_j^2 + 2 c_j) over reference column counts
 };

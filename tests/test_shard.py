@@ -29,7 +29,7 @@ def _cb_layout(S):
     d = ps.supernodes(S)
     w = np.diff(d["first"]).astype(np.int64)
     m2 = np.diff(d["rptr"]) - w
-    cb_off = np.concatenate([[0], np.cumsum(m2 * m2)])
+    cb_off = np.concatenate([[0], np.cumsum(m2 * (m2 + 1) // 2)])
     return d, w, m2, cb_off
 
 
@@ -82,17 +82,17 @@ def _exchange_worker(rank, world, port, q):
         truth = np.zeros(cb_off[-1])
         for sn in range(len(w)):  # the CB every rank would compute, tagged by supernode
             truth[cb_off[sn]:cb_off[sn + 1]] = sn + np.arange(cb_off[sn + 1] - cb_off[sn]) * 1e-6
-        local = np.where(np.repeat(own, m2 * m2) == rank, truth, np.nan)  # only my own blocks are valid
+        local = np.where(np.repeat(own, m2 * (m2 + 1) // 2) == rank, truth, np.nan)  # only my own blocks are valid
         send = np.zeros(info.cb_chunk)
         for sn, o, off in zip(b.ids, b.owner, b.cb_off):
             if o == rank:
-                n = m2[sn] * m2[sn]
+                n = m2[sn] * (m2[sn] + 1) // 2
                 send[off:off + n] = local[cb_off[sn]:cb_off[sn] + n]
         parts = [torch.zeros(info.cb_chunk, dtype=torch.float64) for _ in range(world)]
         dist.all_gather(parts, torch.from_numpy(send))
         for sn, o, off in zip(b.ids, b.owner, b.cb_off):
             if o != rank:
-                n = m2[sn] * m2[sn]
+                n = m2[sn] * (m2[sn] + 1) // 2
                 local[cb_off[sn]:cb_off[sn] + n] = parts[o].numpy()[off:off + n]
         ok = all(np.array_equal(local[cb_off[sn]:cb_off[sn + 1]], truth[cb_off[sn]:cb_off[sn + 1]]) for sn in b.ids)
         q.put((rank, ok, int(info.n_boundary), int(info.cb_chunk)))
