@@ -362,22 +362,22 @@ struct ncl_symb {
   DevBuf<int> perm, sn_first, sn_parent, rows, relp, cptr, child, order, asrc, aoff, flags, tickets;
   DevBuf<int64_t> sn_rptr, sn_loff, cb_off, aptr, gm_ptr, gsp, gsrc;
   DevBuf<int> gdst;
+  DevBuf<uint8_t> big;
   bool dev_ready = false;
 };
 
 namespace {
-constexpr int kSmemFrontCap = 160;  // = kCtaFront in csrc/cuda/ldlt.cu
 TopSched build_top(const Supernodal& Z, const std::vector<int>& ids, int split) {
   TopSched t;
   for (int i = split; i < static_cast<int>(ids.size());) {
     const int h = Z.height[ids[i]];
     int e = i;
-    std::vector<int> big;
+    std::vector<int64_t> big;
     while (e < static_cast<int>(ids.size()) && Z.height[ids[e]] == h) {
       const int s = ids[e];
       const int nr = static_cast<int>(Z.sn_rptr[s + 1] - Z.sn_rptr[s]);
-      if (nr > kSmemFrontCap) {
-        big.insert(big.end(), {s, Z.sn_first[s], Z.sn_first[s + 1] - Z.sn_first[s], nr});
+      if (Z.big[s]) {
+        big.insert(big.end(), {s, Z.sn_first[s], Z.sn_first[s + 1] - Z.sn_first[s], nr, Z.gm_ptr[s], Z.gm_ptr[s + 1]});
         t.any_big = true;
         t.max_nr = std::max(t.max_nr, nr);
       }
@@ -410,6 +410,7 @@ void upload_symb(ncl_symb* S) {
   S->gdst.upload(Z.gdst);
   S->gsp.upload(Z.gsp);
   S->gsrc.upload(Z.gsrc);
+  S->big.upload(Z.big);
   // A entries grouped by target supernode, sorted by panel offset
   const int nsn = Z.nsn;
   std::vector<int64_t> aptr(nsn + 1, 0);
@@ -457,6 +458,7 @@ void upload_symb(ncl_symb* S) {
   d.gdst = S->gdst.p;
   d.gsp = S->gsp.p;
   d.gsrc = S->gsrc.p;
+  d.big = S->big.p;
   d.cptr = S->cptr.p;
   d.child = S->child.p;
   d.order = S->order.p;
@@ -572,8 +574,8 @@ void alloc_fact(ncl_fact* f) {
   f->F.L = f->L.p;
   f->F.CB = f->CB.p;
   f->F.CV = f->CV.p;
-  if (f->S->Z.max_nr > kSmemFrontCap) {  // scratch of the blocked large-front path
-    const int64_t mx = f->S->Z.max_nr;
+  if (f->S->top.any_big) {  // scratch of the blocked large-front path
+    const int64_t mx = f->S->top.max_nr;
     f->bigF.alloc(mx * mx);
     f->bigW.alloc(mx * 32);
     f->F.bigF = f->bigF.p;

@@ -21,7 +21,6 @@ namespace {
 
 constexpr int kBs = 32;      // panel width
 constexpr int kTile = 64;    // DMMA tile (64 x 64 per CTA, 4 warps x 32 x 32)
-constexpr int kColBlk = 32;  // assembly: target columns per CTA
 constexpr unsigned kFullMask = 0xffffffffu;
 
 struct BigArgs {
@@ -37,48 +36,33 @@ struct BigArgs {
   int* zp;
 };
 
-// --- assembly: CTA b owns target columns [b*kColBlk, (b+1)*kColBlk) -------
-__global__ void __launch_bounds__(256) bf_assemble(BigArgs a) {
+// --- assembly: one thread per front entry that receives anything, summing
+// its sources (A value, then children's CB entries in ascending child order)
+// from the gather map — spread over the whole GPU
+__global__ void __launch_bounds__(256) bf_gather(BigArgs a, int64_t g0, int64_t g1) {
   const DevSymb& S = a.S;
-  const int nr = a.nr;
-  const int c0 = blockIdx.x * kColBlk, c1 = min(nr, c0 + kColBlk);
-  for (int64_t e = threadIdx.x; e < static_cast<int64_t>(c1 - c0) * nr; e += blockDim.x)
-    a.F[static_cast<int64_t>(c0) * nr + e] = 0.0;
-  __syncthreads();
-  const int64_t a0 = __ldg(S.aptr + a.s), a1 = __ldg(S.aptr + a.s + 1);
-  for (int64_t e = a0 + threadIdx.x; e < a1; e += blockDim.x) {
-    const int off = __ldg(S.aoff + e);  // c * nr + r (panel layout == front layout for c < w)
-    const int c = off / nr;
-    if (c >= c0 && c < c1) a.F[off] = __ldg(a.kvals + __ldg(S.asrc + e));
-  }
-  __syncthreads();
-  for (int q = __ldg(S.cptr + a.s); q < __ldg(S.cptr + a.s + 1); ++q) {
-    const int ch = __ldg(S.child + q);
-    const int wc = __ldg(S.sn_first + ch + 1) - __ldg(S.sn_first + ch);
-    const int64_t rbc = __ldg(S.sn_rptr + ch);
-    const int m2c = static_cast<int>(__ldg(S.sn_rptr + ch + 1) - rbc) - wc;
-    const int* rel = S.relp + rbc + wc;
-    const double* Cc = a.CB + __ldg(S.cb_off + ch);
-    // child columns j with rel[j] in [c0, c1): a contiguous range (rel ascending)
-    int lo = 0, hi = m2c;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (__ldg(rel + mid) < c0) lo = mid + 1;
-      else hi = mid;
+  for (int64_t k = g0 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < g1;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t q = __ldg(S.gsp + k);
+    const int64_t q1 = __ldg(S.gsp + k + 1);
+    double acc = 0.0;
+    for (; q + 4 <= q1; q += 4) {
+      const int64_t s0 = __ldg(S.gsrc + q), s1 = __ldg(S.gsrc + q + 1), s2 = __ldg(S.gsrc + q + 2),
+                    s3 = __ldg(S.gsrc + q + 3);
+      const double v0 = s0 < 0 ? __ldg(a.kvals + ~s0) : __ldcg(a.CB + s0);
+      const double v1 = s1 < 0 ? __ldg(a.kvals + ~s1) : __ldcg(a.CB + s1);
+      const double v2 = s2 < 0 ? __ldg(a.kvals + ~s2) : __ldcg(a.CB + s2);
+      const double v3 = s3 < 0 ? __ldg(a.kvals + ~s3) : __ldcg(a.CB + s3);
+      acc += v0;
+      acc += v1;
+      acc += v2;
+      acc += v3;
     }
-    int j1 = lo, hi2 = m2c;
-    while (j1 < hi2) {
-      const int mid = (j1 + hi2) >> 1;
-      if (__ldg(rel + mid) < c1) j1 = mid + 1;
-      else hi2 = mid;
+    for (; q < q1; ++q) {
+      const int64_t src = __ldg(S.gsrc + q);
+      acc += src < 0 ? __ldg(a.kvals + ~src) : __ldcg(a.CB + src);
     }
-    for (int j = lo; j < j1; ++j) {
-      const int rj = __ldg(rel + j);
-      double* Fj = a.F + static_cast<int64_t>(rj) * nr;
-      const double* Cj = Cc + cb_col(j, m2c);
-      for (int i = j + threadIdx.x; i < m2c; i += blockDim.x) Fj[__ldg(rel + i)] += __ldcg(Cj + i);
-    }
-    __syncthreads();
+    a.F[__ldg(S.gdst + k)] = acc;
   }
 }
 
@@ -195,12 +179,15 @@ __global__ void bf_publish(int* flags, int s, int epoch) {
 
 // Factor one large supernode (all launches on st, in order). F / Wb: scratch
 // of nr*nr and nr*kBs doubles.
-void dev_factor_big(const DevSymb& S, DevFactor& Fa, const double* kvals, int s, int f, int w, int nr, double* F,
-                    double* Wb, cudaStream_t st) {
+void dev_factor_big(const DevSymb& S, DevFactor& Fa, const double* kvals, int s, int f, int w, int nr, int64_t g0,
+                    int64_t g1, double* F, double* Wb, cudaStream_t st) {
   BigArgs a{S, s, f, w, nr, nr - w, F, Wb, Fa.L, Fa.CB, Fa.D, kvals, Fa.scal, Fa.istat};
-  const int ncb = (nr + kColBlk - 1) / kColBlk;
-  bf_assemble<<<ncb, 256, 0, st>>>(a);
-  g_kernel_launches += 1;
+  cudaMemsetAsync(F, 0, static_cast<size_t>(nr) * nr * sizeof(double), st);
+  const int64_t ne = g1 - g0;
+  if (ne > 0) {
+    bf_gather<<<static_cast<int>(std::min<int64_t>((ne + 255) / 256, 4 * 148)), 256, 0, st>>>(a, g0, g1);
+    g_kernel_launches += 1;
+  }
   for (int k0 = 0; k0 < w; k0 += kBs) {
     const int k1 = std::min(w, k0 + kBs);
     bf_panel<<<1, 256, 0, st>>>(a, k0, k1);

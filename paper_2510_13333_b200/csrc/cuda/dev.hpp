@@ -37,6 +37,7 @@ struct DevSymb {
   int* gdst = nullptr;        // front position of each gather entry
   int64_t* gsp = nullptr;     // [entries+1] source ranges
   int64_t* gsrc = nullptr;    // ~A slot or global CB index
+  uint8_t* big = nullptr;     // [nsn] 1 = large-front path
   int* cptr = nullptr;  // children CSR
   int* child = nullptr;
   int* order = nullptr;  // ticket order, leaves first
@@ -81,7 +82,7 @@ struct DevFactor {
 // list and the large supernodes (s, f, w, nr) that run the blocked DMMA path.
 struct TopSched {
   std::vector<int> lvl_begin, lvl_end;
-  std::vector<std::vector<int>> big;  // per level: quadruples (s, f, w, nr)
+  std::vector<std::vector<int64_t>> big;  // per level: (s, f, w, nr, gather begin, gather end) sextuples
   bool any_big = false;
   int max_nr = 0;
 };
@@ -109,8 +110,8 @@ void dev_shard_pack(const DevSymb& S, const double* src, const int* bids, const 
 void dev_shard_unpack(const DevSymb& S, double* dst, const int* bids, const int* bowner, const int64_t* pack_off,
                       int nb, int rank, int cv, const double* recv, int64_t chunk, int* flags, int epoch,
                       cudaStream_t st);
-void dev_factor_big(const DevSymb& S, DevFactor& F, const double* kvals, int s, int f, int w, int nr, double* Fs,
-                    double* Wb, cudaStream_t st);
+void dev_factor_big(const DevSymb& S, DevFactor& F, const double* kvals, int s, int f, int w, int nr, int64_t g0,
+                    int64_t g1, double* Fs, double* Wb, cudaStream_t st);
 void dev_zero_indexed(double* x, const int* idx, int64_t n, cudaStream_t st);
 void dev_factor(const DevSymb& S, const DevPattern& P, DevFactor& F, const double* kvals, double pivot_tol,
                 cudaStream_t st, const TopSched* top = nullptr);

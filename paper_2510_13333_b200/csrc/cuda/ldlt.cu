@@ -197,6 +197,31 @@ __device__ __forceinline__ void factor_task(const FactorArgs& a, int s, int tid,
 // right-looking sweep over the w pivot columns in smem, one write of the
 // panel and the lower CB. The warp version (nr <= 32) keeps lane i on row i
 // and broadcasts L(c2, c) with shuffles.
+// sum of gather entry k's sources in list order; loads issued 4 at a time
+__device__ __forceinline__ double gather_sum(const DevSymb& S, const double* __restrict__ kvals,
+                                             const double* __restrict__ CB, int64_t k) {
+  int64_t q = __ldg(S.gsp + k);
+  const int64_t q1 = __ldg(S.gsp + k + 1);
+  double acc = 0.0;
+  for (; q + 4 <= q1; q += 4) {
+    const int64_t s0 = __ldg(S.gsrc + q), s1 = __ldg(S.gsrc + q + 1), s2 = __ldg(S.gsrc + q + 2),
+                  s3 = __ldg(S.gsrc + q + 3);
+    const double v0 = s0 < 0 ? __ldg(kvals + ~s0) : __ldcg(CB + s0);
+    const double v1 = s1 < 0 ? __ldg(kvals + ~s1) : __ldcg(CB + s1);
+    const double v2 = s2 < 0 ? __ldg(kvals + ~s2) : __ldcg(CB + s2);
+    const double v3 = s3 < 0 ? __ldg(kvals + ~s3) : __ldcg(CB + s3);
+    acc += v0;
+    acc += v1;
+    acc += v2;
+    acc += v3;
+  }
+  for (; q < q1; ++q) {
+    const int64_t src = __ldg(S.gsrc + q);
+    acc += src < 0 ? __ldg(kvals + ~src) : __ldcg(CB + src);
+  }
+  return acc;
+}
+
 template <int NT>
 __device__ __forceinline__ void factor_task_smem(const FactorArgs& a, int s, int tid, double thresh, double* F) {
   const DevSymb& S = a.S;
@@ -213,14 +238,7 @@ __device__ __forceinline__ void factor_task_smem(const FactorArgs& a, int s, int
   if (g1 > g0) {
     // gather-sum per front entry: A value first, then the children's CB
     // entries in ascending child order (the extend-add order)
-    for (int64_t k = g0 + tid; k < g1; k += NT) {
-      double acc = 0.0;
-      for (int64_t q = __ldg(S.gsp + k); q < __ldg(S.gsp + k + 1); ++q) {
-        const int64_t src = __ldg(S.gsrc + q);
-        acc += src < 0 ? __ldg(a.kvals + ~src) : __ldcg(a.CB + src);
-      }
-      F[__ldg(S.gdst + k)] = acc;
-    }
+    for (int64_t k = g0 + tid; k < g1; k += NT) F[__ldg(S.gdst + k)] = gather_sum(S, a.kvals, a.CB, k);
     team_sync<NT>();
   } else {
   for (int64_t e = __ldg(S.aptr + s) + tid; e < __ldg(S.aptr + s + 1); e += NT)
@@ -369,8 +387,9 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT) factor_kernel(FactorArgs 
     if (t < 0) break;
     const int s = __ldg(a.tasks + t);
     const int nr = static_cast<int>(__ldg(a.S.sn_rptr + s + 1) - __ldg(a.S.sn_rptr + s));
+    if (a.skip_big && __ldg(a.S.big + s)) continue;  // runs on the large-front path
     if (nr <= (NT == 32 ? kWarpFront : kCtaFront)) factor_task_smem<NT>(a, s, tid, thresh, F);
-    else if (!a.skip_big) factor_task<NT>(a, s, tid, thresh);
+    else factor_task<NT>(a, s, tid, thresh);
   }
 }
 
@@ -713,7 +732,7 @@ void dev_factor_list(const DevSymb& S, DevFactor& F, const double* kvals, const 
     a.nleaf = 0;
     for (size_t L = 0; L < ts.lvl_begin.size(); ++L) {
       const int b = ts.lvl_begin[L], e = ts.lvl_end[L];
-      const int nsmall = (e - b) - static_cast<int>(ts.big[L].size() / 4);
+      const int nsmall = (e - b) - static_cast<int>(ts.big[L].size() / 6);
       if (nsmall > 0) {
         cudaMemsetAsync(S.tickets + kTickets - 1, 0, sizeof(int), st);
         a.ticket = S.tickets + kTickets - 1;
@@ -722,9 +741,11 @@ void dev_factor_list(const DevSymb& S, DevFactor& F, const double* kvals, const 
         COUNT(1);
         factor_kernel<256><<<std::min(g_fg2, e - b), 256, kFacSmem2, st>>>(a);
       }
-      for (size_t q = 0; q < ts.big[L].size(); q += 4)
-        dev_factor_big(S, F, kvals, ts.big[L][q], ts.big[L][q + 1], ts.big[L][q + 2], ts.big[L][q + 3], F.bigF,
-                       F.bigW, st);
+      for (size_t q = 0; q < ts.big[L].size(); q += 6) {
+        const int64_t* bq = ts.big[L].data() + q;
+        dev_factor_big(S, F, kvals, static_cast<int>(bq[0]), static_cast<int>(bq[1]), static_cast<int>(bq[2]),
+                       static_cast<int>(bq[3]), bq[4], bq[5], F.bigF, F.bigW, st);
+      }
     }
     return;
   }

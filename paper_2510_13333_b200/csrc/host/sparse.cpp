@@ -334,6 +334,8 @@ void true_L_structure(const SymbolicCore& S, std::vector<int64_t>& lp, std::vect
 
 Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
                             const std::vector<int>& ri, int relax) {
+  constexpr int64_t kSmemFront = 160;       // = kCtaFront (csrc/cuda/ldlt.cu)
+  constexpr int64_t kHeavyGather = 400000;  // child entries one CTA assembles comfortably
   const int n = S.n;
   Supernodal Z;
   // 1a. fundamental partition: j+1 joins j's supernode iff parent[j]==j+1 and
@@ -529,21 +531,19 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
       const int pos = static_cast<int>(std::lower_bound(rb, rb + nr, hi) - rb);
       Z.amap[p] = Z.sn_loff[s] + static_cast<int64_t>(lo - f) * nr + pos;
     }
-  // 7. gather maps of the CTA-part shared-memory fronts (order >= nsplit,
-  //    nr <= kGatherFront): for every front entry that receives anything,
+  // 7. gather maps of the CTA-part fronts (order >= nsplit): for every front entry that receives anything,
   //    its sources in assembly order — the A value (encoded ~slot) first, then
   //    the children's packed CB entries in ascending child order — so the
   //    assembly is one independent gather-sum per entry (no per-child
   //    barriers; same summation order as the scatter/extend-add path).
   {
-    constexpr int kGatherFront = 160;
     Z.gm_ptr.assign(nsn + 1, 0);
     std::vector<std::vector<int64_t>> asrc_of(nsn);
     std::vector<std::vector<int>> adst_of(nsn);
     std::vector<uint8_t> want(nsn, 0);
     for (int t = Z.nsplit; t < nsn; ++t) {
       const int sn = Z.order[t];
-      if (Z.sn_rptr[sn + 1] - Z.sn_rptr[sn] <= kGatherFront) want[sn] = 1;
+      want[sn] = 1;
     }
     for (int64_t p = 0; p < static_cast<int64_t>(Z.amap.size()); ++p) {
       const int64_t off = Z.amap[p];
@@ -595,6 +595,15 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
       Z.gm_ptr[sn + 1] = static_cast<int64_t>(Z.gdst.size());
     }
     Z.gsp.push_back(static_cast<int64_t>(Z.gsrc.size()));
+    // large-front path: fronts beyond the 200 KB shared-memory cap, and fronts
+    // whose assembly gathers too many child entries for one CTA (e.g. the
+    // separator root under every contingency subtree)
+    Z.big.assign(nsn, 0);
+    for (int sn = 0; sn < nsn; ++sn) {
+      if (!want[sn]) continue;
+      const int64_t nsrc = Z.gsp[Z.gm_ptr[sn + 1]] - Z.gsp[Z.gm_ptr[sn]];
+      if (Z.sn_rptr[sn + 1] - Z.sn_rptr[sn] > kSmemFront || nsrc > kHeavyGather) Z.big[sn] = 1;
+    }
   }
   double fl = 0.0;
   for (int j = 0; j < n; ++j) {

@@ -111,6 +111,7 @@ struct Supernodal {
   // gsrc[gsp[k] .. gsp[k+1]) (~slot = A value, else a global CB index)
   std::vector<int64_t> gm_ptr, gsp, gsrc;
   std::vector<int> gdst;
+  std::vector<uint8_t> big;  // [nsn] large-front path (multi-CTA gather + blocked DMMA factor)
   int max_w = 0, max_nr = 0;
   double flops = 0.0;  // sum_j (c_j^2 + 2 c_j) over reference column counts
 };
