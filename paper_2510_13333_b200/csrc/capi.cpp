@@ -355,7 +355,7 @@ API int ncl_sym_write_matrix_market(ncl_sym_t M, char* buf, int64_t cap, int64_t
 struct ncl_symb {
   SymbolicCore core;
   Supernodal Z;
-  TopSched top;  // level schedule of the CTA part (large fronts -> blocked DMMA path)
+  TaskLayout lay;  // default task layout (subtree groups + singles) and its level schedule
   uint64_t hash = 0;
   int nnz = 0;
   DevSymb d;
@@ -363,18 +363,66 @@ struct ncl_symb {
   DevBuf<int64_t> sn_rptr, sn_loff, cb_off, aptr, gm_ptr, gsp, gsrc;
   DevBuf<int> gdst;
   DevBuf<uint8_t> big;
+  DevBuf<int> lay_nodes, lay_tptr;
   bool dev_ready = false;
 };
 
 namespace {
-TopSched build_top(const Supernodal& Z, const std::vector<int>& ids, int split) {
-  TopSched t;
-  for (int i = split; i < static_cast<int>(ids.size());) {
-    const int h = Z.height[ids[i]];
+// Task layout of a list (leaves-first height order, CTA part from `split`):
+// every warp-part supernode whose subtree has <= kGroup supernodes and whose
+// parent does not qualify roots a GROUP task (its subtree in postorder,
+// processed by one warp without scheduling between nodes); the remaining
+// warp-part supernodes and the CTA part are single-node tasks. Order: groups
+// (dependency-free), warp singles by height, CTA singles by height.
+constexpr int kGroup = 64;
+TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int split) {
+  const int nsn = Z.nsn;
+  TaskLayout L;
+  std::vector<uint8_t> warp(nsn, 0);
+  for (int i = 0; i < split; ++i) warp[list[i]] = 1;
+  std::vector<int> size(nsn, 1);
+  for (int i = 0; i < split; ++i) {
+    const int s = list[i], p = Z.sn_parent[s];
+    if (p >= 0 && warp[p]) size[p] += size[s];
+  }
+  L.tptr.push_back(0);
+  std::vector<std::pair<int, int>> st;  // (node, next child cursor)
+  for (int i = 0; i < split; ++i) {
+    const int r = list[i], p = Z.sn_parent[r];
+    if (size[r] > kGroup || (p >= 0 && warp[p] && size[p] <= kGroup)) continue;
+    st.emplace_back(r, Z.cptr[r]);  // postorder DFS, children ascending
+    while (!st.empty()) {
+      auto& top = st.back();
+      if (top.second < Z.cptr[top.first + 1]) {
+        const int c = Z.child[top.second++];
+        st.emplace_back(c, Z.cptr[c]);
+      } else {
+        L.nodes.push_back(top.first);
+        st.pop_back();
+      }
+    }
+    L.tptr.push_back(static_cast<int>(L.nodes.size()));
+  }
+  L.nleaf = static_cast<int>(L.tptr.size()) - 1;
+  for (int i = 0; i < split; ++i)
+    if (size[list[i]] > kGroup) {
+      L.nodes.push_back(list[i]);
+      L.tptr.push_back(static_cast<int>(L.nodes.size()));
+    }
+  L.split = static_cast<int>(L.tptr.size()) - 1;
+  for (int i = split; i < static_cast<int>(list.size()); ++i) {
+    L.nodes.push_back(list[i]);
+    L.tptr.push_back(static_cast<int>(L.nodes.size()));
+  }
+  // level schedule of the CTA part (task indices), large fronts per level
+  TopSched& t = L.top;
+  const int ntask = static_cast<int>(L.tptr.size()) - 1;
+  for (int i = L.split; i < ntask;) {
+    const int h = Z.height[L.nodes[i]];
     int e = i;
     std::vector<int64_t> big;
-    while (e < static_cast<int>(ids.size()) && Z.height[ids[e]] == h) {
-      const int s = ids[e];
+    while (e < ntask && Z.height[L.nodes[e]] == h) {
+      const int s = L.nodes[e];
       const int nr = static_cast<int>(Z.sn_rptr[s + 1] - Z.sn_rptr[s]);
       if (Z.big[s]) {
         big.insert(big.end(), {s, Z.sn_first[s], Z.sn_first[s + 1] - Z.sn_first[s], nr, Z.gm_ptr[s], Z.gm_ptr[s + 1]});
@@ -388,7 +436,7 @@ TopSched build_top(const Supernodal& Z, const std::vector<int>& ids, int split) 
     t.big.push_back(std::move(big));
     i = e;
   }
-  return t;
+  return L;
 }
 
 void upload_symb(ncl_symb* S) {
@@ -411,6 +459,8 @@ void upload_symb(ncl_symb* S) {
   S->gsp.upload(Z.gsp);
   S->gsrc.upload(Z.gsrc);
   S->big.upload(Z.big);
+  S->lay_nodes.upload(S->lay.nodes);
+  S->lay_tptr.upload(S->lay.tptr);
   // A entries grouped by target supernode, sorted by panel offset
   const int nsn = Z.nsn;
   std::vector<int64_t> aptr(nsn + 1, 0);
@@ -459,6 +509,8 @@ void upload_symb(ncl_symb* S) {
   d.gsp = S->gsp.p;
   d.gsrc = S->gsrc.p;
   d.big = S->big.p;
+  d.tasks = DevTasks{S->lay_nodes.p, S->lay_tptr.p, static_cast<int>(S->lay.tptr.size()) - 1, S->lay.nleaf,
+                     S->lay.split, &S->lay.top};
   d.cptr = S->cptr.p;
   d.child = S->child.p;
   d.order = S->order.p;
@@ -490,7 +542,7 @@ ncl_symb* analyze_impl(ncl_sym_t M, const int* perm) {
   auto S = std::make_unique<ncl_symb>();
   S->core = analyze_core(n, M->pat.col_ptr(), M->pat.row_ind(), std::move(p));
   S->Z = build_supernodes(S->core, M->pat.col_ptr(), M->pat.row_ind());
-  S->top = build_top(S->Z, S->Z.order, S->Z.nsplit);
+  S->lay = build_layout(S->Z, S->Z.order, S->Z.nsplit);
   S->hash = M->hash;
   S->nnz = M->pat.nnz();
   return S.release();
@@ -574,8 +626,8 @@ void alloc_fact(ncl_fact* f) {
   f->F.L = f->L.p;
   f->F.CB = f->CB.p;
   f->F.CV = f->CV.p;
-  if (f->S->top.any_big) {  // scratch of the blocked large-front path
-    const int64_t mx = f->S->top.max_nr;
+  if (f->S->lay.top.any_big) {  // scratch of the blocked large-front path
+    const int64_t mx = f->S->lay.top.max_nr;
     f->bigF.alloc(mx * mx);
     f->bigW.alloc(mx * 32);
     f->F.bigF = f->bigF.p;
@@ -587,7 +639,7 @@ void alloc_fact(ncl_fact* f) {
   f->F.istat = f->istat.p;
 }
 void run_factor(ncl_fact* f, ncl_sym_t M, double tol) {
-  dev_factor(f->S->d, M->dp, f->F, M->vals.p, tol, g_stream, &f->S->top);
+  dev_factor(f->S->d, M->dp, f->F, M->vals.p, tol, g_stream, nullptr);
   dev_inertia(f->S->d, f->F, g_stream);
   check_launch("factorize");
 }
@@ -837,7 +889,8 @@ struct ncl_shard {
   DevBuf<uint8_t> report;
   DevBuf<double> send, recv;
   DevBuf<int> unrep;  // original indices this rank does not report (zeroed before the x all-reduce)
-  TopSched topA, topB;
+  TaskLayout layA, layB;
+  DevBuf<int> tA, tB;  // task pointers
   int64_t nunrep = 0;
 };
 
@@ -846,8 +899,10 @@ void shard_upload(ncl_shard* sh) {
   if (sh->dev_ready) return;
   ensure_init();
   upload_symb(sh->S);
-  sh->listA.upload(sh->P.listA);
-  sh->listB.upload(sh->P.listB);
+  sh->listA.upload(sh->layA.nodes);
+  sh->listB.upload(sh->layB.nodes);
+  sh->tA.upload(sh->layA.tptr);
+  sh->tB.upload(sh->layB.tptr);
   sh->bids.upload(sh->P.boundary);
   sh->bowner.upload(sh->P.bowner);
   sh->cb_off.upload(sh->P.cb_pack_off);
@@ -867,10 +922,12 @@ void shard_upload(ncl_shard* sh) {
   sh->dev_ready = true;
 }
 DevTasks tasks_A(ncl_shard* sh) {
-  return DevTasks{sh->listA.p, static_cast<int>(sh->P.listA.size()), sh->P.nleafA, sh->P.splitA, &sh->topA};
+  return DevTasks{sh->listA.p, sh->tA.p, static_cast<int>(sh->layA.tptr.size()) - 1, sh->layA.nleaf, sh->layA.split,
+                  &sh->layA.top};
 }
 DevTasks tasks_B(ncl_shard* sh) {
-  return DevTasks{sh->listB.p, static_cast<int>(sh->P.listB.size()), sh->P.nleafB, sh->P.splitB, &sh->topB};
+  return DevTasks{sh->listB.p, sh->tB.p, static_cast<int>(sh->layB.tptr.size()) - 1, sh->layB.nleaf, sh->layB.split,
+                  &sh->layB.top};
 }
 void need_comm(const ncl_shard* sh) {
   if (sh->P.world == 1) return;
@@ -896,8 +953,8 @@ API int ncl_shard_create(ncl_symb_t S, const int* var_group, int ngroups, int wo
     sh->S = S;
     std::vector<int> g(var_group, var_group + S->core.n);
     sh->P = build_shard_plan(S->Z, S->core, g, ngroups, world, rank);
-    sh->topA = build_top(S->Z, sh->P.listA, sh->P.splitA);
-    sh->topB = build_top(S->Z, sh->P.listB, sh->P.splitB);
+    sh->layA = build_layout(S->Z, sh->P.listA, sh->P.splitA);
+    sh->layB = build_layout(S->Z, sh->P.listB, sh->P.splitB);
     *out = sh.release();
   });
 }

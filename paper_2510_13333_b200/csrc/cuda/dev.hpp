@@ -20,6 +20,26 @@ __host__ __device__ inline int64_t cb_col(int j, int m) {
 // gpu_launches key). Incremented by every dev_* wrapper.
 extern int64_t g_kernel_launches;
 
+// Host-side schedule of the CTA part of a list when it holds fronts too large
+// for shared memory: per height level the [begin, end) index range in the
+// list and the large supernodes (s, f, w, nr) that run the blocked DMMA path.
+struct TopSched {
+  std::vector<int> lvl_begin, lvl_end;
+  std::vector<std::vector<int64_t>> big;  // per level: (s, f, w, nr, gather begin, gather end) sextuples
+  bool any_big = false;
+  int max_nr = 0;
+};
+// A task list: `ids` holds supernodes, task t covers ids[tptr[t] .. tptr[t+1])
+// (a whole small subtree in postorder, or one supernode). Tasks are in
+// dependency order; the first `nleaf` have no external dependencies, tasks
+// from `split` on are single supernodes run CTA-per-task.
+struct DevTasks {
+  const int* ids = nullptr;
+  const int* tptr = nullptr;
+  int n = 0, nleaf = 0, split = 0;  // counts / indices in TASKS
+  const TopSched* top = nullptr;    // host pointer; nullptr or !any_big -> one persistent launch
+};
+
 // Symbolic schedule resident in HBM (built once from host Supernodal).
 struct DevSymb {
   int n = 0, nsn = 0, nleaf = 0, nsplit = 0;
@@ -45,6 +65,7 @@ struct DevSymb {
   int* asrc = nullptr;       // source value slot
   int* aoff = nullptr;       // offset inside panel
   // scheduling state
+  DevTasks tasks;           // default (unsharded) task list
   int* flags = nullptr;     // [3*nsn] epoch flags: factor, fwd, bwd
   int* tickets = nullptr;   // [4]
   int epoch = 0;
@@ -77,20 +98,13 @@ struct DevFactor {
 
 // A task list: supernode ids in leaves-first height order; the first
 // `nleaf` are leaves, tasks from `split` on run CTA-per-task.
-// Host-side schedule of the CTA part of a list when it holds fronts too large
-// for shared memory: per height level the [begin, end) index range in the
-// list and the large supernodes (s, f, w, nr) that run the blocked DMMA path.
-struct TopSched {
-  std::vector<int> lvl_begin, lvl_end;
-  std::vector<std::vector<int64_t>> big;  // per level: (s, f, w, nr, gather begin, gather end) sextuples
-  bool any_big = false;
-  int max_nr = 0;
+// Host copy of a task layout (see build_layout in capi.cpp)
+struct TaskLayout {
+  std::vector<int> nodes, tptr;
+  int nleaf = 0, split = 0;
+  TopSched top;
 };
-struct DevTasks {
-  const int* ids = nullptr;
-  int n = 0, nleaf = 0, split = 0;
-  const TopSched* top = nullptr;  // host pointer; nullptr or !any_big -> one persistent launch
-};
+
 constexpr int kTickets = 40;  // ticket counters per symbolic handle
 
 // all launches are asynchronous on `st`

@@ -60,7 +60,7 @@ __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
 // Team = one warp (NT = 32) for the wide bottom of the tree, one CTA
 // (NT = 256) for the narrow top (tickets >= Z.nsplit), two launches.
 // ---------------------------------------------------------------------------
-constexpr int kLeafChunk = 8;
+constexpr int kLeafChunk = 2;  // dependency-free tasks (whole subtrees) per claim
 
 template <int NT>
 __device__ __forceinline__ void team_sync() {
@@ -112,8 +112,9 @@ struct FactorArgs {
   int* ticket;
   int epoch;
   int t0, t1;          // ticket range of this launch (indices into tasks)
-  const int* tasks;    // supernode ids, leaves-first height order
-  int nleaf;           // leaf tasks at the head of `tasks`
+  const int* tasks;    // supernode ids: tasks are ranges tptr[t]..tptr[t+1] (postorder subtrees)
+  const int* tptr;     // task -> node range
+  int nleaf;           // dependency-free tasks at the head
   int skip_big;        // leave nr > kCtaFront to the blocked DMMA path
 };
 
@@ -385,11 +386,15 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT) factor_kernel(FactorArgs 
   for (;;) {
     const int t = cl.next(a.ticket, a.t0, a.t1, a.nleaf, tid, &s_ticket);
     if (t < 0) break;
-    const int s = __ldg(a.tasks + t);
-    const int nr = static_cast<int>(__ldg(a.S.sn_rptr + s + 1) - __ldg(a.S.sn_rptr + s));
-    if (a.skip_big && __ldg(a.S.big + s)) continue;  // runs on the large-front path
-    if (nr <= (NT == 32 ? kWarpFront : kCtaFront)) factor_task_smem<NT>(a, s, tid, thresh, F);
-    else factor_task<NT>(a, s, tid, thresh);
+    // a task is a whole small subtree in postorder (one warp, no scheduling
+    // between its nodes) or a single supernode
+    for (int k = __ldg(a.tptr + t); k < __ldg(a.tptr + t + 1); ++k) {
+      const int s = __ldg(a.tasks + k);
+      const int nr = static_cast<int>(__ldg(a.S.sn_rptr + s + 1) - __ldg(a.S.sn_rptr + s));
+      if (a.skip_big && __ldg(a.S.big + s)) continue;  // runs on the large-front path
+      if (nr <= (NT == 32 ? kWarpFront : kCtaFront)) factor_task_smem<NT>(a, s, tid, thresh, F);
+      else factor_task<NT>(a, s, tid, thresh);
+    }
   }
 }
 
@@ -454,6 +459,7 @@ struct SolveArgs {
   int epoch;
   int t0, t1;
   const int* tasks;
+  const int* tptr;
   int nleaf;
 };
 
@@ -552,7 +558,7 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT) fwd_kernel(SolveArgs a) {
   for (;;) {
     const int t = cl.next(a.ticket, a.t0, a.t1, a.nleaf, tid, &s_ticket);
     if (t < 0) break;
-    fwd_task<NT>(a, __ldg(a.tasks + t), tid);
+    for (int k = __ldg(a.tptr + t); k < __ldg(a.tptr + t + 1); ++k) fwd_task<NT>(a, __ldg(a.tasks + k), tid);
   }
 }
 
@@ -575,7 +581,7 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT) bwd_kernel(SolveArgs a) {
     }
     const int k = a.t1 - 1 - t;
     if (k < a.t0) break;
-    bwd_task<NT>(a, __ldg(a.tasks + k), tid);
+    for (int j = __ldg(a.tptr + k + 1) - 1; j >= __ldg(a.tptr + k); --j) bwd_task<NT>(a, __ldg(a.tasks + j), tid);
   }
 }
 
@@ -719,7 +725,7 @@ void dev_factor_list(const DevSymb& S, DevFactor& F, const double* kvals, const 
                      cudaStream_t st) {
   if (T.n == 0) return;
   FactorArgs a{S, F.L, F.CB, F.D, kvals, F.scal, F.istat, S.flags, S.tickets + 2 * slot, S.epoch, 0, T.split,
-               T.ids, T.nleaf, 0};
+               T.ids, T.tptr, T.nleaf, 0};
   if (T.split > 0) {
     COUNT(1);
     factor_kernel<32><<<g_fg, 128, kFacSmem1, st>>>(a);
@@ -761,7 +767,9 @@ void dev_factor_list(const DevSymb& S, DevFactor& F, const double* kvals, const 
 void dev_factor(const DevSymb& S, const DevPattern& P, DevFactor& F, const double* kvals, double pivot_tol,
                 cudaStream_t st, const TopSched* top) {
   dev_factor_begin(S, P, F, kvals, pivot_tol, st);
-  dev_factor_list(S, F, kvals, DevTasks{S.order, S.nsn, S.nleaf, S.nsplit, top}, 0, st);
+  DevTasks T = S.tasks;
+  if (top) T.top = top;
+  dev_factor_list(S, F, kvals, T, 0, st);
 }
 
 void dev_inertia(const DevSymb& S, DevFactor& F, cudaStream_t st, const uint8_t* report) {
@@ -780,7 +788,7 @@ void dev_solve_fwd_list(const DevSymb& S, DevFactor& F, const double* b, const D
                         cudaStream_t st) {
   if (T.n == 0) return;
   SolveArgs fa{S, F.L, F.D, F.CV, F.xp, b, nullptr, S.flags + S.nsn, S.tickets + 2 * slot, S.epoch, 0, T.split,
-               T.ids, T.nleaf};
+               T.ids, T.tptr, T.nleaf};
   if (T.split > 0) COUNT(1), fwd_kernel<32><<<g_sf, 128, 0, st>>>(fa);
   if (T.split < T.n) {
     fa.ticket = S.tickets + 2 * slot + 1;
@@ -795,7 +803,7 @@ void dev_solve_fwd_list(const DevSymb& S, DevFactor& F, const double* b, const D
 void dev_solve_bwd_list(const DevSymb& S, DevFactor& F, double* x, const DevTasks& T, int slot, cudaStream_t st) {
   if (T.n == 0) return;
   SolveArgs ba{S, F.L, F.D, F.CV, F.xp, nullptr, x, S.flags + 2 * S.nsn, S.tickets + 2 * slot, S.epoch, T.split,
-               T.n, T.ids, T.nleaf};
+               T.n, T.ids, T.tptr, T.nleaf};
   if (T.split < T.n) COUNT(1), bwd_kernel<256><<<std::min(g_sb2, T.n - T.split), 256, 0, st>>>(ba);
   if (T.split > 0) {
     ba.ticket = S.tickets + 2 * slot + 1;
@@ -809,9 +817,8 @@ void dev_solve_bwd_list(const DevSymb& S, DevFactor& F, double* x, const DevTask
 void dev_solve(const DevSymb& S, DevFactor& F, const double* b, double* x, cudaStream_t st) {
   if (S.n == 0) return;
   dev_solve_begin(S, st);
-  const DevTasks all{S.order, S.nsn, S.nleaf, S.nsplit};
-  dev_solve_fwd_list(S, F, b, all, 0, st);
-  dev_solve_bwd_list(S, F, x, all, 2, st);
+  dev_solve_fwd_list(S, F, b, S.tasks, 0, st);
+  dev_solve_bwd_list(S, F, x, S.tasks, 2, st);
 }
 
 void dev_spmv(const DevPattern& P, const double* kvals, const double* x, double* y, cudaStream_t st) {
