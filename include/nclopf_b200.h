@@ -89,6 +89,8 @@ typedef struct ncl_symb_info {
   double flops;           /* sum_j (c_j^2 + 2 c_j) */
   int64_t cb_storage;     /* doubles in the multifrontal contribution blocks */
   int nsplit;             /* supernodes below this ticket run warp-per-task, above CTA-per-task */
+  int n_big;              /* fronts on the multi-CTA gather + blocked DMMA path */
+  int n_tasks;            /* scheduled tasks (subtree groups + single supernodes) */
 } ncl_symb_info;
 int ncl_symb_info_get(ncl_symb_t S, ncl_symb_info* info);
 /* inspection: supernode partition (nsn+1 firsts, nsn+1 row offsets), parent

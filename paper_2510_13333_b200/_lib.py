@@ -28,7 +28,7 @@ pf64 = C.POINTER(C.c_double)
 class SymbInfo(C.Structure):
     _fields_ = [("n", i32), ("l_nnz", i64), ("nsupernodes", i32), ("max_height", i32),
                 ("max_width", i32), ("max_rows", i32), ("l_storage", i64), ("flops", f64),
-                ("cb_storage", i64), ("nsplit", i32)]
+                ("cb_storage", i64), ("nsplit", i32), ("n_big", i32), ("n_tasks", i32)]
 
 
 _SIGS = {

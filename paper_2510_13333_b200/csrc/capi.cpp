@@ -417,12 +417,13 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
   // level schedule of the CTA part (task indices), large fronts per level
   TopSched& t = L.top;
   const int ntask = static_cast<int>(L.tptr.size()) - 1;
+  auto node_of = [&](int task) { return L.nodes[L.tptr[task]]; };  // CTA-part tasks are single nodes
   for (int i = L.split; i < ntask;) {
-    const int h = Z.height[L.nodes[i]];
+    const int h = Z.height[node_of(i)];
     int e = i;
     std::vector<int64_t> big;
-    while (e < ntask && Z.height[L.nodes[e]] == h) {
-      const int s = L.nodes[e];
+    while (e < ntask && Z.height[node_of(e)] == h) {
+      const int s = node_of(e);
       const int nr = static_cast<int>(Z.sn_rptr[s + 1] - Z.sn_rptr[s]);
       if (Z.big[s]) {
         big.insert(big.end(), {s, Z.sn_first[s], Z.sn_first[s + 1] - Z.sn_first[s], nr, Z.gm_ptr[s], Z.gm_ptr[s + 1]});
@@ -562,6 +563,10 @@ API int ncl_symb_info_get(ncl_symb_t S, ncl_symb_info* info) {
     info->flops = S->Z.flops;
     info->cb_storage = S->Z.cb_storage;
     info->nsplit = S->Z.nsplit;
+    int nb = 0;
+    for (const auto& lv : S->lay.top.big) nb += static_cast<int>(lv.size() / 6);
+    info->n_big = nb;
+    info->n_tasks = static_cast<int>(S->lay.tptr.size()) - 1;
   });
 }
 API int ncl_symb_supernodes(ncl_symb_t S, int* sn_first, int64_t* sn_rptr, int* sn_parent, int* height,

@@ -155,6 +155,8 @@ class SymbolicInfo:
     flops: float
     cb_storage: int = 0
     nsplit: int = 0
+    n_big: int = 0
+    n_tasks: int = 0
 
 
 class SymbolicFactor:
@@ -205,7 +207,7 @@ class SymbolicFactor:
         s = SymbInfo()
         check(lib.ncl_symb_info_get(self._h, C.byref(s)))
         return SymbolicInfo(s.n, s.l_nnz, s.nsupernodes, s.max_height, s.max_width, s.max_rows, s.l_storage,
-                            s.flops, s.cb_storage, s.nsplit)
+                            s.flops, s.cb_storage, s.nsplit, s.n_big, s.n_tasks)
 
 
 def supernodes(S: "SymbolicFactor"):
