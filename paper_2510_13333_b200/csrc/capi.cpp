@@ -364,6 +364,7 @@ struct ncl_symb {
   DevBuf<int> gdst;
   DevBuf<uint8_t> big;
   DevBuf<int> lay_nodes, lay_tptr;
+  DevBuf<SnMeta> meta;
   bool dev_ready = false;
 };
 
@@ -486,6 +487,25 @@ void upload_symb(ncl_symb* S) {
   S->aptr.upload(aptr);
   S->asrc.upload(asrc);
   S->aoff.upload(aoff);
+  {
+    std::vector<SnMeta> mv(nsn);
+    for (int s = 0; s < nsn; ++s) {
+      SnMeta& m = mv[s];
+      m.loff = Z.sn_loff[s];
+      m.cboff = Z.cb_off[s];
+      m.rptr = Z.sn_rptr[s];
+      m.a0 = aptr[s];
+      m.na = static_cast<int>(aptr[s + 1] - aptr[s]);
+      m.f = Z.sn_first[s];
+      m.w = Z.sn_first[s + 1] - Z.sn_first[s];
+      m.nr = static_cast<int>(Z.sn_rptr[s + 1] - Z.sn_rptr[s]);
+      m.c0 = Z.cptr[s];
+      m.c1 = Z.cptr[s + 1];
+      m.parent = Z.sn_parent[s];
+      m.pad = 0;
+    }
+    S->meta.upload(mv);
+  }
   S->flags.alloc(3 * std::max(1, nsn));
   ck(cudaMemsetAsync(S->flags.p, 0, 3 * std::max(1, nsn) * sizeof(int), g_stream), "memset");
   S->tickets.alloc(kTickets);
@@ -510,6 +530,7 @@ void upload_symb(ncl_symb* S) {
   d.gsp = S->gsp.p;
   d.gsrc = S->gsrc.p;
   d.big = S->big.p;
+  d.meta = S->meta.p;
   d.tasks = DevTasks{S->lay_nodes.p, S->lay_tptr.p, static_cast<int>(S->lay.tptr.size()) - 1, S->lay.nleaf,
                      S->lay.split, &S->lay.top};
   d.cptr = S->cptr.p;

@@ -29,6 +29,20 @@ struct TopSched {
   bool any_big = false;
   int max_nr = 0;
 };
+// Packed per-supernode metadata (one 64-byte record, four 16-byte loads):
+// everything a small-front task needs before touching the numbers.
+struct alignas(16) SnMeta {
+  int64_t loff;   // panel offset (L)
+  int64_t cboff;  // contribution-block offset (CB)
+  int64_t rptr;   // row-list offset (rows / relp / CV)
+  int64_t a0;     // first A entry (aptr)
+  int na;         // number of A entries
+  int f, w, nr;   // first column, width, rows
+  int c0, c1;     // children range in child[]
+  int parent, pad;
+};
+static_assert(sizeof(SnMeta) == 64, "SnMeta must stay one 64-byte record");
+
 // A task list: `ids` holds supernodes, task t covers ids[tptr[t] .. tptr[t+1])
 // (a whole small subtree in postorder, or one supernode). Tasks are in
 // dependency order; the first `nleaf` have no external dependencies, tasks
@@ -66,6 +80,7 @@ struct DevSymb {
   int* aoff = nullptr;       // offset inside panel
   // scheduling state
   DevTasks tasks;           // default (unsharded) task list
+  const SnMeta* meta = nullptr;  // [nsn]
   int* flags = nullptr;     // [3*nsn] epoch flags: factor, fwd, bwd
   int* tickets = nullptr;   // [4]
   int epoch = 0;

@@ -372,6 +372,79 @@ __device__ __forceinline__ void factor_task_smem(const FactorArgs& a, int s, int
   }
 }
 
+// Small front (nr <= 32) by one warp from the packed metadata: lane i owns
+// row i; children's metadata is fetched lane-parallel; the relative row map
+// of a child sits in registers (lane i holds rel[i]) and its CB columns are
+// read contiguously. Inside a subtree group the children were produced by
+// this very warp, so there is no flag wait, and only the group's root
+// publishes (fence + release). Arithmetic is identical to factor_task_smem<32>.
+__device__ __forceinline__ void small_task(const FactorArgs& a, int s, int lane, double thresh, double* F,
+                                           bool wait_children, bool publish) {
+  const DevSymb& S = a.S;
+  const SnMeta m = S.meta[s];
+  const int nr = m.nr, w = m.w, f = m.f, m2 = nr - w;
+  if (wait_children)
+    for (int q = m.c0 + lane; q < m.c1; q += 32) wait_flag(a.flags + __ldg(S.child + q), a.epoch);
+  for (int k = lane; k < nr * nr; k += 32) F[k] = 0.0;
+  __syncwarp();
+  for (int e = lane; e < m.na; e += 32)
+    F[__ldg(S.aoff + m.a0 + e)] = __ldg(a.kvals + __ldg(S.asrc + m.a0 + e));
+  __syncwarp();
+  for (int q0 = m.c0; q0 < m.c1; q0 += 32) {
+    // lane k fetches child q0+k's metadata; then children in order
+    int cm2 = 0;
+    int64_t ccb = 0, crel = 0;
+    if (q0 + lane < m.c1) {
+      const SnMeta& cmeta = S.meta[__ldg(S.child + q0 + lane)];
+      cm2 = cmeta.nr - cmeta.w;
+      ccb = cmeta.cboff;
+      crel = cmeta.rptr + cmeta.w;
+    }
+    const int nq = min(32, m.c1 - q0);
+    for (int k = 0; k < nq; ++k) {
+      const int m2c = __shfl_sync(kFull, cm2, k);
+      const long long cbk = __shfl_sync(kFull, static_cast<long long>(ccb), k);
+      const long long rlk = __shfl_sync(kFull, static_cast<long long>(crel), k);
+      const int reli = lane < m2c ? __ldg(S.relp + rlk + lane) : 0;
+      const double* Cc = a.CB + cbk;
+      for (int j = 0; j < m2c; ++j) {
+        const int relj = __shfl_sync(kFull, reli, j);
+        if (lane >= j && lane < m2c) F[relj * nr + reli] += __ldcg(Cc + cb_col(j, m2c) + lane);
+      }
+      __syncwarp();
+    }
+  }
+  const int i = lane;
+  for (int c = 0; c < w; ++c) {
+    const double d = F[c * nr + c];
+    if (i == 0) {
+      a.D[f + c] = d;
+      if (fabs(d) <= thresh) atomicMin(a.zp, f + c);
+    }
+    double l = 0.0;
+    if (i > c && i < nr) {
+      l = F[c * nr + i] / d;
+      F[c * nr + i] = l;
+    }
+    const double dl = d * l;
+    for (int c2 = c + 1; c2 < nr; ++c2) {
+      const double lc2 = __shfl_sync(kFull, dl, c2);
+      if (i >= c2 && i < nr) F[c2 * nr + i] -= l * lc2;
+    }
+    __syncwarp();
+  }
+  double* P = a.L + m.loff;
+  double* C = a.CB + m.cboff;
+  for (int k = lane; k < w * nr; k += 32) P[k] = F[k];
+  for (int j = 0; j < m2; ++j)
+    if (lane >= j && lane < m2) C[cb_col(j, m2) + lane] = F[(w + j) * nr + (w + lane)];
+  __syncwarp();
+  if (publish && lane == 0) {
+    __threadfence();
+    st_release(a.flags + s, a.epoch);
+  }
+}
+
 constexpr int kWarpFront = 32;    // nr cap of the warp smem path
 constexpr int kCtaFront = 160;    // nr cap of the CTA smem path (160^2 doubles = 200 KB)
 
@@ -388,11 +461,14 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT) factor_kernel(FactorArgs 
     if (t < 0) break;
     // a task is a whole small subtree in postorder (one warp, no scheduling
     // between its nodes) or a single supernode
-    for (int k = __ldg(a.tptr + t); k < __ldg(a.tptr + t + 1); ++k) {
+    const bool group = t < a.nleaf;  // subtree group: children internal, only the root publishes
+    const int k0 = __ldg(a.tptr + t), k1 = __ldg(a.tptr + t + 1);
+    for (int k = k0; k < k1; ++k) {
       const int s = __ldg(a.tasks + k);
       const int nr = static_cast<int>(__ldg(a.S.sn_rptr + s + 1) - __ldg(a.S.sn_rptr + s));
       if (a.skip_big && __ldg(a.S.big + s)) continue;  // runs on the large-front path
-      if (nr <= (NT == 32 ? kWarpFront : kCtaFront)) factor_task_smem<NT>(a, s, tid, thresh, F);
+      if (NT == 32 && nr <= kWarpFront) small_task(a, s, tid, thresh, F, !group, !group || k == k1 - 1);
+      else if (nr <= (NT == 32 ? kWarpFront : kCtaFront)) factor_task_smem<NT>(a, s, tid, thresh, F);
       else factor_task<NT>(a, s, tid, thresh);
     }
   }
