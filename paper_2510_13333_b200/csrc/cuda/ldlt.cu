@@ -119,9 +119,10 @@ struct FactorArgs {
 };
 
 template <int NT>
-__device__ __forceinline__ void factor_task(const FactorArgs& a, int s, int tid, double thresh) {
+__device__ __forceinline__ void factor_task(const FactorArgs& a, int s, int tid, double thresh,
+                                            bool wait_children = true, bool publish = true) {
   const DevSymb& S = a.S;
-  if (tid == 0)
+  if (tid == 0 && wait_children)
     for (int q = __ldg(S.cptr + s); q < __ldg(S.cptr + s + 1); ++q) wait_flag(a.flags + __ldg(S.child + q), a.epoch);
   team_sync<NT>();
   const int f = __ldg(S.sn_first + s);
@@ -187,7 +188,7 @@ __device__ __forceinline__ void factor_task(const FactorArgs& a, int s, int tid,
     C[cb_col(j, m2) + i] -= acc;
   }
   team_sync<NT>();
-  if (tid == 0) {
+  if (tid == 0 && publish) {
     __threadfence();
     st_release(a.flags + s, a.epoch);
   }
@@ -469,7 +470,7 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT) factor_kernel(FactorArgs 
       if (a.skip_big && __ldg(a.S.big + s)) continue;  // runs on the large-front path
       if (NT == 32 && nr <= kWarpFront) small_task(a, s, tid, thresh, F, !group, !group || k == k1 - 1);
       else if (nr <= (NT == 32 ? kWarpFront : kCtaFront)) factor_task_smem<NT>(a, s, tid, thresh, F);
-      else factor_task<NT>(a, s, tid, thresh);
+      else factor_task<NT>(a, s, tid, thresh, !group, !group || k == k1 - 1);
     }
   }
 }

@@ -169,3 +169,33 @@ def test_large_front_dmma_path(gpu, n1, n2, dens):
     D1 = Fa.diagonal()
     Fa.refactorize(A)
     assert np.array_equal(Fa.diagonal(), D1)  # deterministic run to run
+
+
+@pytest.mark.parametrize("grid,K", [("case118", 16), ("activsg500", 16)])
+def test_scopf_kkt_parity(gpu, grid, K):
+    """The condensed SCOPF KKT (subtree groups with mid-size fronts, CTA top,
+    separator root) against the reference factorize / solve."""
+    from paper_2510_13333_b200.kkt import Kkt
+    from paper_2510_13333_b200.scopf import Scopf
+    s = Scopf(grid, K)
+    M = s.build_model()
+    kk = Kkt(M)
+    rng = np.random.default_rng(5)
+    kk.assemble(0.1 * rng.standard_normal(M.nnzh), rng.standard_normal(M.nnzj), 1.0 + rng.random(s.n), 0.0,
+                10.0 + rng.random(M.m))
+    A = kk.matrix
+    S = ps.analyze(A)
+    F = ps.factorize(A, S)
+    n = A.dim()
+    cp, ri, v = A.col_ptr(), A.row_ind(), A.values()
+    B = RefSparseSym(n, ri, np.repeat(np.arange(n, dtype=np.int32), np.diff(cp)), v)
+    G = RefFactorization(B, RefSymbolic(B, S.perm))
+    assert F.status == G.status
+    ia = F.inertia
+    assert (ia.n_pos, ia.n_neg, ia.n_zero) == G.inertia
+    assert relerr(F.diagonal(), G.diagonal()) < 1e-9
+    b = rng.standard_normal(n)
+    assert relerr(F.solve(b), G.solve(b)) < 1e-8
+    D1 = F.diagonal()
+    F.refactorize(A)
+    assert np.array_equal(F.diagonal(), D1)
