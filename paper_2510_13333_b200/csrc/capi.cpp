@@ -363,7 +363,8 @@ struct ncl_symb {
   DevBuf<int64_t> sn_rptr, sn_loff, cb_off, aptr, gm_ptr, gsp, gsrc;
   DevBuf<int> gdst;
   DevBuf<uint8_t> big;
-  DevBuf<int> lay_nodes, lay_tptr;
+  DevBuf<int> lay_nodes, lay_tptr, lay_prog;
+  DevBuf<int64_t> lay_gpo;
   DevBuf<SnMeta> meta;
   bool dev_ready = false;
 };
@@ -375,22 +376,50 @@ namespace {
 // processed by one warp without scheduling between nodes); the remaining
 // warp-part supernodes and the CTA part are single-node tasks. Order: groups
 // (dependency-free), warp singles by height, CTA singles by height.
-constexpr int kGroup = 64;
 TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int split) {
   const int nsn = Z.nsn;
   TaskLayout L;
   std::vector<uint8_t> warp(nsn, 0);
   for (int i = 0; i < split; ++i) warp[list[i]] = 1;
-  std::vector<int> size(nsn, 1);
+  // Groups are maximal warp-part subtrees whose whole multifrontal working
+  // set fits one warp's shared memory: every front nr <= kGrpFront, the
+  // program (records + relative maps + A entries) <= kGrpProg ints, the A
+  // values plus the peak contribution-block stack <= kGrpStack doubles.
+  auto wof = [&](int s) { return Z.sn_first[s + 1] - Z.sn_first[s]; };
+  auto nrof = [&](int s) { return static_cast<int>(Z.sn_rptr[s + 1] - Z.sn_rptr[s]); };
+  auto cbof = [&](int s) {
+    const int64_t m2 = nrof(s) - wof(s);
+    return m2 * (m2 + 1) / 2;
+  };
+  std::vector<uint8_t> fits(nsn, 0);
+  std::vector<int64_t> prog(nsn, 0), na(nsn, 0), stk(nsn, 0);
   for (int i = 0; i < split; ++i) {
-    const int s = list[i], p = Z.sn_parent[s];
-    if (p >= 0 && warp[p]) size[p] += size[s];
+    const int s = list[i];
+    bool ok = nrof(s) <= kGrpFront;
+    int64_t pr = 8 + 2 * (Z.a_ptr[s + 1] - Z.a_ptr[s]), a = Z.a_ptr[s + 1] - Z.a_ptr[s], pk = 0, run = 0;
+    for (int q = Z.cptr[s]; q < Z.cptr[s + 1]; ++q) {
+      const int c = Z.child[q];
+      ok = ok && fits[c];
+      pr += prog[c] + 2 + (nrof(c) - wof(c));
+      a += na[c];
+      pk = std::max(pk, run + stk[c]);
+      run += cbof(c);
+    }
+    pk = std::max(pk, run);
+    prog[s] = pr;
+    na[s] = a;
+    stk[s] = pk;
+    fits[s] = ok && pr + 4 <= kGrpProg && pk + a <= kGrpStack;
   }
   L.tptr.push_back(0);
+  L.gpo.push_back(0);
   std::vector<std::pair<int, int>> st;  // (node, next child cursor)
+  std::vector<int> post;
+  std::vector<int> cboff(nsn, -1);  // stack offset of a pushed CB (set before its parent reads it)
   for (int i = 0; i < split; ++i) {
     const int r = list[i], p = Z.sn_parent[r];
-    if (size[r] > kGroup || (p >= 0 && warp[p] && size[p] <= kGroup)) continue;
+    if (!fits[r] || (p >= 0 && warp[p] && fits[p])) continue;
+    post.clear();
     st.emplace_back(r, Z.cptr[r]);  // postorder DFS, children ascending
     while (!st.empty()) {
       auto& top = st.back();
@@ -398,15 +427,53 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
         const int c = Z.child[top.second++];
         st.emplace_back(c, Z.cptr[c]);
       } else {
-        L.nodes.push_back(top.first);
+        post.push_back(top.first);
         st.pop_back();
       }
     }
+    L.nodes.insert(L.nodes.end(), post.begin(), post.end());
     L.tptr.push_back(static_cast<int>(L.nodes.size()));
+    // program: [nnodes, nA, 0, len] [aoff x nA] [asrc x nA] then per node
+    // [s, f, w, nr, nch, push_off(-1 = root), a_first, a_cnt] and per child
+    // [m2c, stack_off, rel x m2c]; stack offsets from a postorder simulation
+    const size_t base = L.prog.size();
+    const int nA = static_cast<int>(na[r]);
+    L.prog.insert(L.prog.end(), {static_cast<int>(post.size()), nA, 0, 0});
+    const size_t aoff0 = L.prog.size();
+    L.prog.resize(aoff0 + 2 * static_cast<size_t>(nA));
+    int top = 0, afirst = 0;
+    for (int s : post) {
+      const int acnt = static_cast<int>(Z.a_ptr[s + 1] - Z.a_ptr[s]);
+      for (int e = 0; e < acnt; ++e) {
+        L.prog[aoff0 + afirst + e] = Z.a_off[Z.a_ptr[s] + e];
+        L.prog[aoff0 + nA + afirst + e] = Z.a_src[Z.a_ptr[s] + e];
+      }
+      int pop = 0;
+      for (int q = Z.cptr[s]; q < Z.cptr[s + 1]; ++q) pop += static_cast<int>(cbof(Z.child[q]));
+      const int push = s == r ? -1 : top - pop;
+      L.prog.insert(L.prog.end(), {s, Z.sn_first[s], wof(s), nrof(s), Z.cptr[s + 1] - Z.cptr[s], push, afirst, acnt});
+      for (int q = Z.cptr[s]; q < Z.cptr[s + 1]; ++q) {
+        const int c = Z.child[q];
+        const int m2c = nrof(c) - wof(c);
+        L.prog.push_back(m2c);
+        L.prog.push_back(cboff[c]);
+        for (int k = 0; k < m2c; ++k) L.prog.push_back(Z.relp[Z.sn_rptr[c] + wof(c) + k]);
+      }
+      top -= pop;
+      if (s != r) {
+        cboff[s] = top;
+        top += static_cast<int>(cbof(s));
+      }
+      afirst += acnt;
+    }
+    L.prog[base + 3] = static_cast<int>(L.prog.size() - base);
+    L.gpo.push_back(static_cast<int64_t>(L.prog.size()));
   }
   L.nleaf = static_cast<int>(L.tptr.size()) - 1;
+  std::vector<uint8_t> grouped(nsn, 0);
+  for (int s : L.nodes) grouped[s] = 1;
   for (int i = 0; i < split; ++i)
-    if (size[list[i]] > kGroup) {
+    if (!grouped[list[i]]) {
       L.nodes.push_back(list[i]);
       L.tptr.push_back(static_cast<int>(L.nodes.size()));
     }
@@ -462,31 +529,15 @@ void upload_symb(ncl_symb* S) {
   S->gsrc.upload(Z.gsrc);
   S->big.upload(Z.big);
   S->lay_nodes.upload(S->lay.nodes);
+  S->lay_prog.upload(S->lay.prog);
+  S->lay_gpo.upload(S->lay.gpo);
   S->lay_tptr.upload(S->lay.tptr);
-  // A entries grouped by target supernode, sorted by panel offset
+  // A entries grouped by target supernode (Supernodal::a_ptr/a_src/a_off)
   const int nsn = Z.nsn;
-  std::vector<int64_t> aptr(nsn + 1, 0);
-  std::vector<int> asn(Z.amap.size());
-  for (size_t e = 0; e < Z.amap.size(); ++e) {
-    const int64_t off = Z.amap[e];
-    const int s = static_cast<int>(std::upper_bound(Z.sn_loff.begin(), Z.sn_loff.end(), off) - Z.sn_loff.begin()) - 1;
-    asn[e] = s;
-    aptr[s + 1]++;
-  }
-  for (int s = 0; s < nsn; ++s) aptr[s + 1] += aptr[s];
-  std::vector<int> asrc(Z.amap.size()), aoff(Z.amap.size());
-  {
-    std::vector<int64_t> fp(aptr.begin(), aptr.end() - 1);
-    for (size_t e = 0; e < Z.amap.size(); ++e) {
-      const int s = asn[e];
-      const int64_t q = fp[s]++;
-      asrc[q] = static_cast<int>(e);
-      aoff[q] = static_cast<int>(Z.amap[e] - Z.sn_loff[s]);
-    }
-  }
-  S->aptr.upload(aptr);
-  S->asrc.upload(asrc);
-  S->aoff.upload(aoff);
+  const std::vector<int64_t>& aptr = Z.a_ptr;
+  S->aptr.upload(Z.a_ptr);
+  S->asrc.upload(Z.a_src);
+  S->aoff.upload(Z.a_off);
   {
     std::vector<SnMeta> mv(nsn);
     for (int s = 0; s < nsn; ++s) {
@@ -531,8 +582,8 @@ void upload_symb(ncl_symb* S) {
   d.gsrc = S->gsrc.p;
   d.big = S->big.p;
   d.meta = S->meta.p;
-  d.tasks = DevTasks{S->lay_nodes.p, S->lay_tptr.p, static_cast<int>(S->lay.tptr.size()) - 1, S->lay.nleaf,
-                     S->lay.split, &S->lay.top};
+  d.tasks = DevTasks{S->lay_nodes.p, S->lay_tptr.p, S->lay_prog.p, S->lay_gpo.p,
+                     static_cast<int>(S->lay.tptr.size()) - 1, S->lay.nleaf, S->lay.split, &S->lay.top};
   d.cptr = S->cptr.p;
   d.child = S->child.p;
   d.order = S->order.p;
@@ -916,7 +967,8 @@ struct ncl_shard {
   DevBuf<double> send, recv;
   DevBuf<int> unrep;  // original indices this rank does not report (zeroed before the x all-reduce)
   TaskLayout layA, layB;
-  DevBuf<int> tA, tB;  // task pointers
+  DevBuf<int> tA, tB, pA, pB;  // task pointers, group programs
+  DevBuf<int64_t> gA, gB;
   int64_t nunrep = 0;
 };
 
@@ -929,6 +981,10 @@ void shard_upload(ncl_shard* sh) {
   sh->listB.upload(sh->layB.nodes);
   sh->tA.upload(sh->layA.tptr);
   sh->tB.upload(sh->layB.tptr);
+  sh->pA.upload(sh->layA.prog);
+  sh->pB.upload(sh->layB.prog);
+  sh->gA.upload(sh->layA.gpo);
+  sh->gB.upload(sh->layB.gpo);
   sh->bids.upload(sh->P.boundary);
   sh->bowner.upload(sh->P.bowner);
   sh->cb_off.upload(sh->P.cb_pack_off);
@@ -948,12 +1004,12 @@ void shard_upload(ncl_shard* sh) {
   sh->dev_ready = true;
 }
 DevTasks tasks_A(ncl_shard* sh) {
-  return DevTasks{sh->listA.p, sh->tA.p, static_cast<int>(sh->layA.tptr.size()) - 1, sh->layA.nleaf, sh->layA.split,
-                  &sh->layA.top};
+  return DevTasks{sh->listA.p, sh->tA.p, sh->pA.p, sh->gA.p, static_cast<int>(sh->layA.tptr.size()) - 1,
+                  sh->layA.nleaf, sh->layA.split, &sh->layA.top};
 }
 DevTasks tasks_B(ncl_shard* sh) {
-  return DevTasks{sh->listB.p, sh->tB.p, static_cast<int>(sh->layB.tptr.size()) - 1, sh->layB.nleaf, sh->layB.split,
-                  &sh->layB.top};
+  return DevTasks{sh->listB.p, sh->tB.p, sh->pB.p, sh->gB.p, static_cast<int>(sh->layB.tptr.size()) - 1,
+                  sh->layB.nleaf, sh->layB.split, &sh->layB.top};
 }
 void need_comm(const ncl_shard* sh) {
   if (sh->P.world == 1) return;

@@ -50,6 +50,8 @@ static_assert(sizeof(SnMeta) == 64, "SnMeta must stay one 64-byte record");
 struct DevTasks {
   const int* ids = nullptr;
   const int* tptr = nullptr;
+  const int* prog = nullptr;       // group programs (factor)
+  const int64_t* gpo = nullptr;    // [ngroups+1]
   int n = 0, nleaf = 0, split = 0;  // counts / indices in TASKS
   const TopSched* top = nullptr;    // host pointer; nullptr or !any_big -> one persistent launch
 };
@@ -118,7 +120,14 @@ struct TaskLayout {
   std::vector<int> nodes, tptr;
   int nleaf = 0, split = 0;
   TopSched top;
+  // group programs (one per group task, see build_layout): int stream
+  std::vector<int> prog;
+  std::vector<int64_t> gpo;  // [ngroups+1]
 };
+// per-warp shared-memory budget of a group task (csrc/cuda/ldlt.cu)
+constexpr int kGrpFront = 32;       // fronts of group nodes: nr <= 32
+constexpr int kGrpStack = 1024;     // doubles: A values + contribution-block stack
+constexpr int kGrpProg = 1024;      // ints: the group program
 
 constexpr int kTickets = 40;  // ticket counters per symbolic handle
 

@@ -114,6 +114,8 @@ struct FactorArgs {
   int t0, t1;          // ticket range of this launch (indices into tasks)
   const int* tasks;    // supernode ids: tasks are ranges tptr[t]..tptr[t+1] (postorder subtrees)
   const int* tptr;     // task -> node range
+  const int* prog;     // group programs (tasks < nleaf)
+  const int64_t* gpo;
   int nleaf;           // dependency-free tasks at the head
   int skip_big;        // leave nr > kCtaFront to the blocked DMMA path
 };
@@ -446,6 +448,77 @@ __device__ __forceinline__ void small_task(const FactorArgs& a, int s, int lane,
   }
 }
 
+// A whole subtree group by one warp, entirely in shared memory: the group
+// program (csrc/capi.cpp build_layout) and its A values are loaded once,
+// children's contribution blocks live on a shared-memory stack (multifrontal
+// postorder), and only panels and the group root's CB go to global memory.
+// Per node the arithmetic is exactly small_task's.
+__device__ __forceinline__ void group_task(const FactorArgs& a, int g, int lane, double thresh, double* F,
+                                           double* ST, int* PG) {
+  const DevSymb& S = a.S;
+  const int* gp = a.prog + __ldg(a.gpo + g);
+  const int len = __ldg(gp + 3);
+  for (int k = lane; k < len; k += 32) PG[k] = __ldg(gp + k);
+  __syncwarp();
+  const int nnodes = PG[0], nA = PG[1];
+  for (int e = lane; e < nA; e += 32) ST[e] = __ldg(a.kvals + PG[4 + nA + e]);
+  __syncwarp();
+  const int* aoffs = PG + 4;
+  double* stack = ST + nA;
+  int p = 4 + 2 * nA;
+  for (int v = 0; v < nnodes; ++v) {
+    const int s = PG[p], f = PG[p + 1], w = PG[p + 2], nr = PG[p + 3], nch = PG[p + 4], push = PG[p + 5],
+              af = PG[p + 6], ac = PG[p + 7];
+    p += 8;
+    const int m2 = nr - w;
+    for (int k = lane; k < nr * nr; k += 32) F[k] = 0.0;
+    __syncwarp();
+    for (int e = lane; e < ac; e += 32) F[aoffs[af + e]] = ST[af + e];
+    __syncwarp();
+    for (int q = 0; q < nch; ++q) {
+      const int m2c = PG[p], off = PG[p + 1];
+      const int reli = lane < m2c ? PG[p + 2 + lane] : 0;
+      const double* Cc = stack + off;
+      for (int j = 0; j < m2c; ++j) {
+        const int relj = __shfl_sync(kFull, reli, j);
+        if (lane >= j && lane < m2c) F[relj * nr + reli] += Cc[cb_col(j, m2c) + lane];
+      }
+      p += 2 + m2c;
+      __syncwarp();
+    }
+    const int i = lane;
+    for (int c = 0; c < w; ++c) {
+      const double d = F[c * nr + c];
+      if (i == 0) {
+        a.D[f + c] = d;
+        if (fabs(d) <= thresh) atomicMin(a.zp, f + c);
+      }
+      double l = 0.0;
+      if (i > c && i < nr) {
+        l = F[c * nr + i] / d;
+        F[c * nr + i] = l;
+      }
+      const double dl = d * l;
+      for (int c2 = c + 1; c2 < nr; ++c2) {
+        const double lc2 = __shfl_sync(kFull, dl, c2);
+        if (i >= c2 && i < nr) F[c2 * nr + i] -= l * lc2;
+      }
+      __syncwarp();
+    }
+    const SnMeta& m = S.meta[s];
+    double* P = a.L + m.loff;
+    for (int k = lane; k < w * nr; k += 32) P[k] = F[k];
+    double* C = push >= 0 ? stack + push : a.CB + m.cboff;
+    for (int j = 0; j < m2; ++j)
+      if (lane >= j && lane < m2) C[cb_col(j, m2) + lane] = F[(w + j) * nr + (w + lane)];
+    __syncwarp();
+    if (push < 0 && lane == 0) {  // the group root publishes its CB
+      __threadfence();
+      st_release(a.flags + s, a.epoch);
+    }
+  }
+}
+
 constexpr int kWarpFront = 32;    // nr cap of the warp smem path
 constexpr int kCtaFront = 160;    // nr cap of the CTA smem path (160^2 doubles = 200 KB)
 
@@ -454,7 +527,10 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT) factor_kernel(FactorArgs 
   __shared__ int s_ticket;
   extern __shared__ double s_front[];
   const int tid = NT == 32 ? (threadIdx.x & 31) : threadIdx.x;
-  double* F = NT == 32 ? s_front + (threadIdx.x >> 5) * kWarpFront * kWarpFront : s_front;
+  constexpr int kWarpSmem = kGrpFront * kGrpFront + kGrpStack + kGrpProg / 2;  // doubles per warp
+  double* F = NT == 32 ? s_front + (threadIdx.x >> 5) * kWarpSmem : s_front;
+  double* gST = F + kGrpFront * kGrpFront;
+  int* gPG = reinterpret_cast<int*>(gST + kGrpStack);
   const double thresh = __ldcg(a.thresh);
   Claim<NT> cl;
   for (;;) {
@@ -463,6 +539,12 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT) factor_kernel(FactorArgs 
     // a task is a whole small subtree in postorder (one warp, no scheduling
     // between its nodes) or a single supernode
     const bool group = t < a.nleaf;  // subtree group: children internal, only the root publishes
+    if constexpr (NT == 32) {
+      if (group && a.prog) {
+        group_task(a, t, tid, thresh, F, gST, gPG);
+        continue;
+      }
+    }
     const int k0 = __ldg(a.tptr + t), k1 = __ldg(a.tptr + t + 1);
     for (int k = k0; k < k1; ++k) {
       const int s = __ldg(a.tasks + k);
@@ -773,7 +855,7 @@ int persistent_grid(K fn, int threads, int ntasks, int smem = 0) {
 }
 
 static int g_fg = 0, g_fg2 = 0, g_sf = 0, g_sf2 = 0, g_sb = 0, g_sb2 = 0;
-constexpr int kFacSmem1 = 4 * kWarpFront * kWarpFront * sizeof(double);
+constexpr int kFacSmem1 = 4 * (kGrpFront * kGrpFront + kGrpStack + kGrpProg / 2) * sizeof(double);
 constexpr int kFacSmem2 = kCtaFront * kCtaFront * sizeof(double);
 static void init_grids() {
   if (g_fg) return;
@@ -802,7 +884,7 @@ void dev_factor_list(const DevSymb& S, DevFactor& F, const double* kvals, const 
                      cudaStream_t st) {
   if (T.n == 0) return;
   FactorArgs a{S, F.L, F.CB, F.D, kvals, F.scal, F.istat, S.flags, S.tickets + 2 * slot, S.epoch, 0, T.split,
-               T.ids, T.tptr, T.nleaf, 0};
+               T.ids, T.tptr, T.prog, T.gpo, T.nleaf, 0};
   if (T.split > 0) {
     COUNT(1);
     factor_kernel<32><<<g_fg, 128, kFacSmem1, st>>>(a);

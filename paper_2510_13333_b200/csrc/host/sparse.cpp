@@ -531,6 +531,27 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
       const int pos = static_cast<int>(std::lower_bound(rb, rb + nr, hi) - rb);
       Z.amap[p] = Z.sn_loff[s] + static_cast<int64_t>(lo - f) * nr + pos;
     }
+  // 6b. A entries grouped by target supernode (source slot, offset in panel)
+  {
+    Z.a_ptr.assign(nsn + 1, 0);
+    std::vector<int> asn(Z.amap.size());
+    for (size_t e = 0; e < Z.amap.size(); ++e) {
+      const int64_t off = Z.amap[e];
+      const int sn = static_cast<int>(std::upper_bound(Z.sn_loff.begin(), Z.sn_loff.end(), off) - Z.sn_loff.begin()) - 1;
+      asn[e] = sn;
+      Z.a_ptr[sn + 1]++;
+    }
+    for (int sn = 0; sn < nsn; ++sn) Z.a_ptr[sn + 1] += Z.a_ptr[sn];
+    Z.a_src.resize(Z.amap.size());
+    Z.a_off.resize(Z.amap.size());
+    std::vector<int64_t> fp(Z.a_ptr.begin(), Z.a_ptr.end() - 1);
+    for (size_t e = 0; e < Z.amap.size(); ++e) {
+      const int sn = asn[e];
+      const int64_t q = fp[sn]++;
+      Z.a_src[q] = static_cast<int>(e);
+      Z.a_off[q] = static_cast<int>(Z.amap[e] - Z.sn_loff[sn]);
+    }
+  }
   // 7. gather maps of the CTA-part fronts (order >= nsplit): for every front entry that receives anything,
   //    its sources in assembly order — the A value (encoded ~slot) first, then
   //    the children's packed CB entries in ascending child order — so the
@@ -545,13 +566,12 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
       const int sn = Z.order[t];
       want[sn] = 1;
     }
-    for (int64_t p = 0; p < static_cast<int64_t>(Z.amap.size()); ++p) {
-      const int64_t off = Z.amap[p];
-      const int sn = static_cast<int>(std::upper_bound(Z.sn_loff.begin(), Z.sn_loff.end(), off) - Z.sn_loff.begin()) - 1;
-      if (!want[sn]) continue;
-      adst_of[sn].push_back(static_cast<int>(off - Z.sn_loff[sn]));
-      asrc_of[sn].push_back(p);
-    }
+    for (int sn = 0; sn < nsn; ++sn)
+      if (want[sn])
+        for (int64_t q = Z.a_ptr[sn]; q < Z.a_ptr[sn + 1]; ++q) {
+          adst_of[sn].push_back(Z.a_off[q]);
+          asrc_of[sn].push_back(Z.a_src[q]);
+        }
     std::vector<int> cnt;
     for (int sn = 0; sn < nsn; ++sn) {
       if (!want[sn]) {

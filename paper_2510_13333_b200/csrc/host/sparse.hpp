@@ -112,6 +112,9 @@ struct Supernodal {
   std::vector<int64_t> gm_ptr, gsp, gsrc;
   std::vector<int> gdst;
   std::vector<uint8_t> big;  // [nsn] large-front path (multi-CTA gather + blocked DMMA factor)
+  // A entries grouped by supernode: [a_ptr[s], a_ptr[s+1]) -> source value slot, offset in the panel
+  std::vector<int64_t> a_ptr;
+  std::vector<int> a_src, a_off;
   int max_w = 0, max_nr = 0;
   double flops = 0.0;  // sum_j (c_j^2 + 2 c_j) over reference column counts
 };
