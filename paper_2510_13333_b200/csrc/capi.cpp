@@ -396,7 +396,7 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
   for (int i = 0; i < split; ++i) {
     const int s = list[i];
     bool ok = nrof(s) <= kGrpFront;
-    int64_t pr = 8 + 2 * (Z.a_ptr[s + 1] - Z.a_ptr[s]), a = Z.a_ptr[s + 1] - Z.a_ptr[s], pk = 0, run = 0;
+    int64_t pr = 12 + 2 * (Z.a_ptr[s + 1] - Z.a_ptr[s]), a = Z.a_ptr[s + 1] - Z.a_ptr[s], pk = 0, run = 0;
     for (int q = Z.cptr[s]; q < Z.cptr[s + 1]; ++q) {
       const int c = Z.child[q];
       ok = ok && fits[c];
@@ -434,7 +434,7 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
     L.nodes.insert(L.nodes.end(), post.begin(), post.end());
     L.tptr.push_back(static_cast<int>(L.nodes.size()));
     // program: [nnodes, nA, 0, len] [aoff x nA] [asrc x nA] then per node
-    // [s, f, w, nr, nch, push_off(-1 = root), a_first, a_cnt] and per child
+    // [s, f, w, nr, nch, push_off(-1 = root), a_first, a_cnt, loff lo/hi, cboff lo/hi] and per child
     // [m2c, stack_off, rel x m2c]; stack offsets from a postorder simulation
     const size_t base = L.prog.size();
     const int nA = static_cast<int>(na[r]);
@@ -451,7 +451,10 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
       int pop = 0;
       for (int q = Z.cptr[s]; q < Z.cptr[s + 1]; ++q) pop += static_cast<int>(cbof(Z.child[q]));
       const int push = s == r ? -1 : top - pop;
-      L.prog.insert(L.prog.end(), {s, Z.sn_first[s], wof(s), nrof(s), Z.cptr[s + 1] - Z.cptr[s], push, afirst, acnt});
+      const int64_t lo = Z.sn_loff[s], cbo = Z.cb_off[s];
+      L.prog.insert(L.prog.end(), {s, Z.sn_first[s], wof(s), nrof(s), Z.cptr[s + 1] - Z.cptr[s], push, afirst, acnt,
+                                   static_cast<int>(lo & 0xffffffff), static_cast<int>(lo >> 32),
+                                   static_cast<int>(cbo & 0xffffffff), static_cast<int>(cbo >> 32)});
       for (int q = Z.cptr[s]; q < Z.cptr[s + 1]; ++q) {
         const int c = Z.child[q];
         const int m2c = nrof(c) - wof(c);
@@ -716,7 +719,31 @@ void alloc_fact(ncl_fact* f) {
   f->F.istat = f->istat.p;
 }
 void run_factor(ncl_fact* f, ncl_sym_t M, double tol) {
+  // NCL_TASK_TRACE=<file>: per-task globaltimer start/end of the next
+  // factorization (debug timeline of the persistent schedule)
+  static const char* trace_path = std::getenv("NCL_TASK_TRACE");
+  static int traced = 0;
+  static DevBuf<unsigned long long> tbuf;
+  const int ntask = f->S->d.tasks.n;
+  if (trace_path && traced == 2) {
+    tbuf.alloc(2 * static_cast<int64_t>(ntask));
+    ck(cudaMemsetAsync(tbuf.p, 0, 2 * ntask * sizeof(unsigned long long), g_stream), "memset");
+    g_task_trace = tbuf.p;
+  }
   dev_factor(f->S->d, M->dp, f->F, M->vals.p, tol, g_stream, nullptr);
+  if (trace_path && traced++ == 2) {
+    g_task_trace = nullptr;
+    std::vector<unsigned long long> h;
+    tbuf.download(h, 2 * static_cast<int64_t>(ntask));
+    if (FILE* fp = std::fopen(trace_path, "wb")) {
+      const int hdr[4] = {ntask, f->S->d.tasks.nleaf, f->S->d.tasks.split, 0};
+      std::fwrite(hdr, sizeof(int), 4, fp);
+      std::fwrite(h.data(), sizeof(unsigned long long), h.size(), fp);
+      std::fwrite(f->S->lay.tptr.data(), sizeof(int), f->S->lay.tptr.size(), fp);
+      std::fwrite(f->S->lay.nodes.data(), sizeof(int), f->S->lay.nodes.size(), fp);
+      std::fclose(fp);
+    }
+  }
   dev_inertia(f->S->d, f->F, g_stream);
   check_launch("factorize");
 }

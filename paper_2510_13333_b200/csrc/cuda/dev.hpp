@@ -126,10 +126,12 @@ struct TaskLayout {
 };
 // per-warp shared-memory budget of a group task (csrc/cuda/ldlt.cu)
 constexpr int kGrpFront = 32;       // fronts of group nodes: nr <= 32
-constexpr int kGrpStack = 1024;     // doubles: A values + contribution-block stack
-constexpr int kGrpProg = 1024;      // ints: the group program
+constexpr int kGrpStack = 640;      // doubles: A values + contribution-block stack
+constexpr int kGrpProg = 768;       // ints: the group program
 
 constexpr int kTickets = 40;  // ticket counters per symbolic handle
+
+extern unsigned long long* g_task_trace;  // device buffer [2 * tasks] or nullptr
 
 // all launches are asynchronous on `st`
 // sharded pieces: begin (threshold, epoch, tickets) -> list(s) -> inertia

@@ -36,6 +36,12 @@ __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ void wait_flag(const int* f, int epoch) {
   while (ld_acquire(f) != epoch) __nanosleep(32);
 }
@@ -118,6 +124,7 @@ struct FactorArgs {
   const int64_t* gpo;
   int nleaf;           // dependency-free tasks at the head
   int skip_big;        // leave nr > kCtaFront to the blocked DMMA path
+  unsigned long long* trace;  // optional (NCL_TASK_TRACE): globaltimer start/end per task
 };
 
 template <int NT>
@@ -469,7 +476,11 @@ __device__ __forceinline__ void group_task(const FactorArgs& a, int g, int lane,
   for (int v = 0; v < nnodes; ++v) {
     const int s = PG[p], f = PG[p + 1], w = PG[p + 2], nr = PG[p + 3], nch = PG[p + 4], push = PG[p + 5],
               af = PG[p + 6], ac = PG[p + 7];
-    p += 8;
+    const int64_t loff = static_cast<int64_t>(static_cast<uint32_t>(PG[p + 8])) |
+                         (static_cast<int64_t>(PG[p + 9]) << 32);
+    const int64_t cboff = static_cast<int64_t>(static_cast<uint32_t>(PG[p + 10])) |
+                          (static_cast<int64_t>(PG[p + 11]) << 32);
+    p += 12;
     const int m2 = nr - w;
     for (int k = lane; k < nr * nr; k += 32) F[k] = 0.0;
     __syncwarp();
@@ -505,10 +516,9 @@ __device__ __forceinline__ void group_task(const FactorArgs& a, int g, int lane,
       }
       __syncwarp();
     }
-    const SnMeta& m = S.meta[s];
-    double* P = a.L + m.loff;
+    double* P = a.L + loff;
     for (int k = lane; k < w * nr; k += 32) P[k] = F[k];
-    double* C = push >= 0 ? stack + push : a.CB + m.cboff;
+    double* C = push >= 0 ? stack + push : a.CB + cboff;
     for (int j = 0; j < m2; ++j)
       if (lane >= j && lane < m2) C[cb_col(j, m2) + lane] = F[(w + j) * nr + (w + lane)];
     __syncwarp();
@@ -539,9 +549,11 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT) factor_kernel(FactorArgs 
     // a task is a whole small subtree in postorder (one warp, no scheduling
     // between its nodes) or a single supernode
     const bool group = t < a.nleaf;  // subtree group: children internal, only the root publishes
+    if (a.trace && tid == 0) a.trace[2 * t] = gtimer();
     if constexpr (NT == 32) {
       if (group && a.prog) {
         group_task(a, t, tid, thresh, F, gST, gPG);
+        if (a.trace && tid == 0) a.trace[2 * t + 1] = gtimer();
         continue;
       }
     }
@@ -554,6 +566,7 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT) factor_kernel(FactorArgs 
       else if (nr <= (NT == 32 ? kWarpFront : kCtaFront)) factor_task_smem<NT>(a, s, tid, thresh, F);
       else factor_task<NT>(a, s, tid, thresh, !group, !group || k == k1 - 1);
     }
+    if (a.trace && tid == 0) a.trace[2 * t + 1] = gtimer();
   }
 }
 
@@ -854,6 +867,7 @@ int persistent_grid(K fn, int threads, int ntasks, int smem = 0) {
   return std::max(1, std::min(g, ntasks));
 }
 
+unsigned long long* g_task_trace = nullptr;  // NCL_TASK_TRACE debugging
 static int g_fg = 0, g_fg2 = 0, g_sf = 0, g_sf2 = 0, g_sb = 0, g_sb2 = 0;
 constexpr int kFacSmem1 = 4 * (kGrpFront * kGrpFront + kGrpStack + kGrpProg / 2) * sizeof(double);
 constexpr int kFacSmem2 = kCtaFront * kCtaFront * sizeof(double);
@@ -884,7 +898,7 @@ void dev_factor_list(const DevSymb& S, DevFactor& F, const double* kvals, const 
                      cudaStream_t st) {
   if (T.n == 0) return;
   FactorArgs a{S, F.L, F.CB, F.D, kvals, F.scal, F.istat, S.flags, S.tickets + 2 * slot, S.epoch, 0, T.split,
-               T.ids, T.tptr, T.prog, T.gpo, T.nleaf, 0};
+               T.ids, T.tptr, T.prog, T.gpo, T.nleaf, 0, g_task_trace};
   if (T.split > 0) {
     COUNT(1);
     factor_kernel<32><<<g_fg, 128, kFacSmem1, st>>>(a);
