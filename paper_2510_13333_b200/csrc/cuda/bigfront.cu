@@ -66,9 +66,52 @@ __global__ void __launch_bounds__(256) bf_gather(BigArgs a, int64_t g0, int64_t 
   }
 }
 
+// --- panel: unblocked LDLᵀ of columns [k0, k1) over rows [k0, nr) (one CTA)
+// staged in shared memory (rows k0..nr of the kBs panel columns), warps own
+// columns c2 and lanes rows in the rank-1 updates; then W(:, c-k0) =
+// L(:, c) * d_c for the rows below the panel.
+__global__ void __launch_bounds__(256) bf_panel(BigArgs a, int k0, int k1) {
+  extern __shared__ double Ps[];  // (nr - k0) x kBs, column-major, ld = nr - k0
+  const int nr = a.nr, ld = nr - k0, kw = k1 - k0;
+  const double thresh = __ldcg(a.thresh);
+  double* F = a.F;
+  for (int e = threadIdx.x; e < ld * kw; e += blockDim.x) {
+    const int c = e / ld, i = e % ld;
+    Ps[e] = F[static_cast<int64_t>(k0 + c) * nr + k0 + i];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int c = 0; c < kw; ++c) {
+    double* Pc = Ps + c * ld;
+    const double d = Pc[c];
+    if (threadIdx.x == 0) {
+      a.D[a.f + k0 + c] = d;
+      if (fabs(d) <= thresh) atomicMin(a.zp, a.f + k0 + c);
+    }
+    for (int i = c + 1 + threadIdx.x; i < ld; i += blockDim.x) Pc[i] = Pc[i] / d;
+    __syncthreads();
+    for (int c2 = c + 1 + warp; c2 < kw; c2 += 8) {
+      const double dl = d * Pc[c2];
+      double* P2 = Ps + c2 * ld;
+      for (int i = c2 + lane; i < ld; i += 32) P2[i] -= Pc[i] * dl;
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < ld * kw; e += blockDim.x) {
+    const int c = e / ld, i = e % ld;
+    F[static_cast<int64_t>(k0 + c) * nr + k0 + i] = Ps[e];
+    const int gi = k0 + i;
+    a.Wb[static_cast<int64_t>(c) * nr + gi] = gi >= k1 ? Ps[e] * Ps[c * ld + c] : 0.0;
+  }
+  for (int e = threadIdx.x; e < kw * k0; e += blockDim.x) {  // rows above the panel: W = 0
+    const int c = e / k0, i = e % k0;
+    a.Wb[static_cast<int64_t>(c) * nr + i] = 0.0;
+  }
+}
+
 // --- panel: unblocked LDLᵀ of columns [k0, k1) over rows [k0, nr) (one CTA),
 // then W(:, c-k0) = L(:, c) * d_c for the rows below the panel.
-__global__ void __launch_bounds__(256) bf_panel(BigArgs a, int k0, int k1) {
+__global__ void __launch_bounds__(256) bf_panel_global(BigArgs a, int k0, int k1) {
   const int nr = a.nr;
   const double thresh = __ldcg(a.thresh);
   double* F = a.F;
@@ -190,7 +233,13 @@ void dev_factor_big(const DevSymb& S, DevFactor& Fa, const double* kvals, int s,
   }
   for (int k0 = 0; k0 < w; k0 += kBs) {
     const int k1 = std::min(w, k0 + kBs);
-    bf_panel<<<1, 256, 0, st>>>(a, k0, k1);
+    const int psmem = (nr - k0) * (k1 - k0) * static_cast<int>(sizeof(double));
+    if (psmem <= 220 * 1024) {
+      if (psmem > 48 * 1024) cudaFuncSetAttribute(bf_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, psmem);
+      bf_panel<<<1, 256, psmem, st>>>(a, k0, k1);
+    } else {
+      bf_panel_global<<<1, 256, 0, st>>>(a, k0, k1);  // panels taller than shared memory
+    }
     const int rest = nr - k1;
     g_kernel_launches += 1;
     if (rest > 0) {
