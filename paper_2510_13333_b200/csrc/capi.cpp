@@ -360,7 +360,7 @@ struct ncl_symb {
   int nnz = 0;
   DevSymb d;
   DevBuf<int> perm, sn_first, sn_parent, rows, relp, cptr, child, order, asrc, aoff, flags, tickets;
-  DevBuf<int64_t> sn_rptr, sn_loff, cb_off, aptr, gm_ptr, gsp, gsrc;
+  DevBuf<int64_t> sn_rptr, sn_loff, cb_off, aptr, gm_ptr, gsp, gsrc, cv_ptr, cvsp, cvsrc;
   DevBuf<int> gdst;
   DevBuf<uint8_t> big;
   DevBuf<int> lay_nodes, lay_tptr, lay_prog;
@@ -531,6 +531,9 @@ void upload_symb(ncl_symb* S) {
   S->gsp.upload(Z.gsp);
   S->gsrc.upload(Z.gsrc);
   S->big.upload(Z.big);
+  S->cv_ptr.upload(Z.cv_ptr);
+  S->cvsp.upload(Z.cvsp);
+  S->cvsrc.upload(Z.cvsrc);
   S->lay_nodes.upload(S->lay.nodes);
   S->lay_prog.upload(S->lay.prog);
   S->lay_gpo.upload(S->lay.gpo);
@@ -584,6 +587,9 @@ void upload_symb(ncl_symb* S) {
   d.gsp = S->gsp.p;
   d.gsrc = S->gsrc.p;
   d.big = S->big.p;
+  d.cv_ptr = S->cv_ptr.p;
+  d.cvsp = S->cvsp.p;
+  d.cvsrc = S->cvsrc.p;
   d.meta = S->meta.p;
   d.tasks = DevTasks{S->lay_nodes.p, S->lay_tptr.p, S->lay_prog.p, S->lay_gpo.p,
                      static_cast<int>(S->lay.tptr.size()) - 1, S->lay.nleaf, S->lay.split, &S->lay.top};

@@ -74,6 +74,9 @@ struct DevSymb {
   int64_t* gsp = nullptr;     // [entries+1] source ranges
   int64_t* gsrc = nullptr;    // ~A slot or global CB index
   uint8_t* big = nullptr;     // [nsn] 1 = large-front path
+  int64_t* cv_ptr = nullptr;  // forward-solve gather (CTA-part fronts)
+  int64_t* cvsp = nullptr;
+  int64_t* cvsrc = nullptr;
   int* cptr = nullptr;  // children CSR
   int* child = nullptr;
   int* order = nullptr;  // ticket order, leaves first

@@ -233,6 +233,40 @@ __device__ __forceinline__ double gather_sum(const DevSymb& S, const double* __r
   return acc;
 }
 
+// Gather-sums of entries [g0, g1) into F, four entries per thread at a time
+// so the dependent load chains (gsp -> gsrc -> CB) of different entries
+// overlap; each entry still sums its sources strictly in list order.
+template <int NT>
+__device__ __forceinline__ void gather4(const DevSymb& S, const double* __restrict__ kvals,
+                                        const double* __restrict__ CB, int64_t g0, int64_t g1, int tid, double* F) {
+  for (int64_t kb = g0 + tid; kb < g1; kb += 4 * NT) {
+    int64_t q[4], q1[4];
+    double acc[4];
+    int cmax = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t k = kb + u * NT;
+      q[u] = k < g1 ? __ldg(S.gsp + k) : 0;
+      q1[u] = k < g1 ? __ldg(S.gsp + k + 1) : 0;
+      acc[u] = 0.0;
+      cmax = max(cmax, static_cast<int>(q1[u] - q[u]));
+    }
+    for (int c = 0; c < cmax; ++c) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (q[u] + c < q1[u]) {
+          const int64_t src = __ldg(S.gsrc + q[u] + c);
+          acc[u] += src < 0 ? __ldg(kvals + ~src) : __ldcg(CB + src);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t k = kb + u * NT;
+      if (k < g1) F[__ldg(S.gdst + k)] = acc[u];
+    }
+  }
+}
+
 template <int NT>
 __device__ __forceinline__ void factor_task_smem(const FactorArgs& a, int s, int tid, double thresh, double* F) {
   const DevSymb& S = a.S;
@@ -249,7 +283,7 @@ __device__ __forceinline__ void factor_task_smem(const FactorArgs& a, int s, int
   if (g1 > g0) {
     // gather-sum per front entry: A value first, then the children's CB
     // entries in ascending child order (the extend-add order)
-    for (int64_t k = g0 + tid; k < g1; k += NT) F[__ldg(S.gdst + k)] = gather_sum(S, a.kvals, a.CB, k);
+    gather4<NT>(S, a.kvals, a.CB, g0, g1, tid, F);
     team_sync<NT>();
   } else {
   for (int64_t e = __ldg(S.aptr + s) + tid; e < __ldg(S.aptr + s + 1); e += NT)
@@ -648,6 +682,18 @@ __device__ __forceinline__ void fwd_task(const SolveArgs& a, int s, int tid) {
   const double* P = a.L + __ldg(S.sn_loff + s);
   double* cv = a.CV + rb;
   double* xs = a.xp + f;
+  const int64_t v0 = NT == 32 ? 0 : __ldg(S.cv_ptr + s), v1 = NT == 32 ? 0 : __ldg(S.cv_ptr + s + 1);
+  if (v1 > v0) {
+    // gather per row: b (pivot rows) then the children's CV entries in
+    // child order — the sequential extend-add's summation order
+    for (int k = tid; k < nr; k += NT) {
+      double acc = k < w ? __ldcg(a.b + __ldg(S.perm + f + k)) : 0.0;
+      for (int64_t q = __ldg(S.cvsp + v0 + k); q < __ldg(S.cvsp + v0 + k + 1); ++q) acc += __ldcg(a.CV + __ldg(S.cvsrc + q));
+      if (k < w) xs[k] = acc;
+      else cv[k] = acc;
+    }
+    team_sync<NT>();
+  } else {
   for (int k = tid; k < nr; k += NT) {
     if (k < w) xs[k] = __ldcg(a.b + __ldg(S.perm + f + k));
     else cv[k] = 0.0;
@@ -666,6 +712,7 @@ __device__ __forceinline__ void fwd_task(const SolveArgs& a, int s, int tid) {
     }
     team_sync<NT>();
   }
+  }  // extend-add path
   for (int c = 0; c < w; ++c) {
     const double xc = xs[c];
     const double* Pc = P + static_cast<int64_t>(c) * nr;

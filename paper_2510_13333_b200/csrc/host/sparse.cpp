@@ -615,6 +615,33 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
       Z.gm_ptr[sn + 1] = static_cast<int64_t>(Z.gdst.size());
     }
     Z.gsp.push_back(static_cast<int64_t>(Z.gsrc.size()));
+    // forward-solve gather map of the same fronts: row r of s sums its
+    // children's contribution-vector entries (global CV index) in child order
+    Z.cv_ptr.assign(nsn + 1, 0);
+    Z.cvsp.clear();
+    Z.cvsrc.clear();
+    std::vector<std::vector<int64_t>> rowsrc;
+    for (int sn = 0; sn < nsn; ++sn) {
+      if (!want[sn]) {
+        Z.cv_ptr[sn + 1] = Z.cv_ptr[sn];
+        continue;
+      }
+      const int nr = static_cast<int>(Z.sn_rptr[sn + 1] - Z.sn_rptr[sn]);
+      rowsrc.assign(nr, {});
+      for (int q = Z.cptr[sn]; q < Z.cptr[sn + 1]; ++q) {
+        const int c = Z.child[q];
+        const int wc = Z.sn_first[c + 1] - Z.sn_first[c];
+        const int m2c = static_cast<int>(Z.sn_rptr[c + 1] - Z.sn_rptr[c]) - wc;
+        for (int k = 0; k < m2c; ++k)
+          rowsrc[Z.relp[Z.sn_rptr[c] + wc + k]].push_back(Z.sn_rptr[c] + wc + k);
+      }
+      for (int r = 0; r < nr; ++r) {
+        Z.cvsp.push_back(static_cast<int64_t>(Z.cvsrc.size()));
+        Z.cvsrc.insert(Z.cvsrc.end(), rowsrc[r].begin(), rowsrc[r].end());
+      }
+      Z.cv_ptr[sn + 1] = Z.cv_ptr[sn] + nr;
+    }
+    Z.cvsp.push_back(static_cast<int64_t>(Z.cvsrc.size()));
     // large-front path: fronts beyond the 200 KB shared-memory cap, and fronts
     // whose assembly gathers too many child entries for one CTA (e.g. the
     // separator root under every contingency subtree)

@@ -111,6 +111,9 @@ struct Supernodal {
   // gsrc[gsp[k] .. gsp[k+1]) (~slot = A value, else a global CB index)
   std::vector<int64_t> gm_ptr, gsp, gsrc;
   std::vector<int> gdst;
+  // forward-solve gather of the same fronts: rows [cv_ptr[s], cv_ptr[s+1]) of
+  // s, row k sums cvsrc[cvsp[k] .. cvsp[k+1]) (global CV indices)
+  std::vector<int64_t> cv_ptr, cvsp, cvsrc;
   std::vector<uint8_t> big;  // [nsn] large-front path (multi-CTA gather + blocked DMMA factor)
   // A entries grouped by supernode: [a_ptr[s], a_ptr[s+1]) -> source value slot, offset in the panel
   std::vector<int64_t> a_ptr;
