@@ -210,7 +210,7 @@ std::vector<int> symbolic_order(int n, const std::vector<int>& cp, const std::ve
       } else {
         std::vector<int>& au = adj[u];
         merged.clear();
-        merged.reserve(au.size() + clique.size());
+        if (merged.capacity() < au.size() + clique.size()) merged.reserve(2 * (au.size() + clique.size()));
         size_t i = 0, j = 0;
         const size_t na = au.size(), nc = clique.size();
         while (i < na || j < nc) {
@@ -225,7 +225,7 @@ std::vector<int> symbolic_order(int n, const std::vector<int>& cp, const std::ve
           }
           if (x != v && x != u) merged.push_back(x);
         }
-        au.swap(merged);
+        au.assign(merged.begin(), merged.end());  // au keeps (and only grows) its own buffer
         if (static_cast<int>(au.size()) > kBig) to_bitmap(u);
       }
       if (degree(u) != old) heap.push(key(degree(u), u));
