@@ -396,7 +396,7 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
   for (int i = 0; i < split; ++i) {
     const int s = list[i];
     bool ok = nrof(s) <= kGrpFront;
-    int64_t pr = 12 + 2 * (Z.a_ptr[s + 1] - Z.a_ptr[s]), a = Z.a_ptr[s + 1] - Z.a_ptr[s], pk = 0, run = 0;
+    int64_t pr = 14 + 2 * (Z.a_ptr[s + 1] - Z.a_ptr[s]), a = Z.a_ptr[s + 1] - Z.a_ptr[s], pk = 0, run = 0;
     for (int q = Z.cptr[s]; q < Z.cptr[s + 1]; ++q) {
       const int c = Z.child[q];
       ok = ok && fits[c];
@@ -434,7 +434,7 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
     L.nodes.insert(L.nodes.end(), post.begin(), post.end());
     L.tptr.push_back(static_cast<int>(L.nodes.size()));
     // program: [nnodes, nA, 0, len] [aoff x nA] [asrc x nA] then per node
-    // [s, f, w, nr, nch, push_off(-1 = root), a_first, a_cnt, loff lo/hi, cboff lo/hi] and per child
+    // [s, f, w, nr, nch, push_off(-1 = root), a_first, a_cnt, loff lo/hi, cboff lo/hi, rptr lo/hi] and per child
     // [m2c, stack_off, rel x m2c]; stack offsets from a postorder simulation
     const size_t base = L.prog.size();
     const int nA = static_cast<int>(na[r]);
@@ -451,10 +451,11 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
       int pop = 0;
       for (int q = Z.cptr[s]; q < Z.cptr[s + 1]; ++q) pop += static_cast<int>(cbof(Z.child[q]));
       const int push = s == r ? -1 : top - pop;
-      const int64_t lo = Z.sn_loff[s], cbo = Z.cb_off[s];
+      const int64_t lo = Z.sn_loff[s], cbo = Z.cb_off[s], rp = Z.sn_rptr[s];
       L.prog.insert(L.prog.end(), {s, Z.sn_first[s], wof(s), nrof(s), Z.cptr[s + 1] - Z.cptr[s], push, afirst, acnt,
                                    static_cast<int>(lo & 0xffffffff), static_cast<int>(lo >> 32),
-                                   static_cast<int>(cbo & 0xffffffff), static_cast<int>(cbo >> 32)});
+                                   static_cast<int>(cbo & 0xffffffff), static_cast<int>(cbo >> 32),
+                                   static_cast<int>(rp & 0xffffffff), static_cast<int>(rp >> 32)});
       for (int q = Z.cptr[s]; q < Z.cptr[s + 1]; ++q) {
         const int c = Z.child[q];
         const int m2c = nrof(c) - wof(c);

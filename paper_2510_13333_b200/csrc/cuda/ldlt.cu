@@ -514,7 +514,7 @@ __device__ __forceinline__ void group_task(const FactorArgs& a, int g, int lane,
                          (static_cast<int64_t>(PG[p + 9]) << 32);
     const int64_t cboff = static_cast<int64_t>(static_cast<uint32_t>(PG[p + 10])) |
                           (static_cast<int64_t>(PG[p + 11]) << 32);
-    p += 12;
+    p += 14;
     const int m2 = nr - w;
     for (int k = lane; k < nr * nr; k += 32) F[k] = 0.0;
     __syncwarp();
@@ -666,8 +666,112 @@ struct SolveArgs {
   int t0, t1;
   const int* tasks;
   const int* tptr;
+  const int* prog;
+  const int64_t* gpo;
   int nleaf;
 };
+
+__device__ __forceinline__ int64_t rec64(const int* r) {
+  return static_cast<int64_t>(static_cast<uint32_t>(r[0])) | (static_cast<int64_t>(r[1]) << 32);
+}
+
+// Forward solve of a subtree group by one warp from its program (same node
+// order as the factor): lane i owns row i, children's contribution vectors
+// come from a shared-memory stack (at the factor's CB stack offsets), only
+// x (pivot rows) and the root's CV go to global memory. Same arithmetic as
+// fwd_task<32>.
+__device__ void fwd_group(const SolveArgs& a, int g, int lane, double* VS, double* ST, int* PG) {
+  const DevSymb& S = a.S;
+  const int* gp = a.prog + __ldg(a.gpo + g);
+  const int len = __ldg(gp + 3);
+  for (int k = lane; k < len; k += 32) PG[k] = __ldg(gp + k);
+  __syncwarp();
+  const int nnodes = PG[0], nA = PG[1];
+  int p = 4 + 2 * nA;
+  for (int v = 0; v < nnodes; ++v) {
+    const int* R = PG + p;
+    const int s = R[0], f = R[1], w = R[2], nr = R[3], nch = R[4], push = R[5];
+    const int64_t loff = rec64(R + 8), rb = rec64(R + 12);
+    p += 14;
+    if (lane < nr) VS[lane] = lane < w ? __ldcg(a.b + __ldg(S.perm + f + lane)) : 0.0;
+    __syncwarp();
+    for (int q = 0; q < nch; ++q) {
+      const int m2c = PG[p], off = PG[p + 1];
+      if (lane < m2c) VS[PG[p + 2 + lane]] += ST[off + lane];
+      p += 2 + m2c;
+      __syncwarp();
+    }
+    const double* P = a.L + loff;
+    for (int c = 0; c < w; ++c) {
+      const double xc = VS[c];
+      if (lane > c && lane < nr) VS[lane] -= P[c * nr + lane] * xc;
+      __syncwarp();
+    }
+    if (lane < w) a.xp[f + lane] = VS[lane];
+    if (lane >= w && lane < nr) {
+      if (push >= 0) ST[push + (lane - w)] = VS[lane];
+      else a.CV[rb + lane] = VS[lane];
+    }
+    __syncwarp();
+    if (push < 0 && lane == 0) {
+      __threadfence();
+      st_release(a.flags + s, a.epoch);
+    }
+  }
+}
+
+// Backward solve of a group (reverse postorder; the root waits for its
+// parent, which lies outside the group). Same arithmetic as bwd_task<32>.
+__device__ void bwd_group(const SolveArgs& a, int g, int lane, int* PG, int* OFF) {
+  const DevSymb& S = a.S;
+  const int* gp = a.prog + __ldg(a.gpo + g);
+  const int len = __ldg(gp + 3);
+  for (int k = lane; k < len; k += 32) PG[k] = __ldg(gp + k);
+  __syncwarp();
+  const int nnodes = PG[0], nA = PG[1];
+  if (lane == 0) {  // record offsets of the nodes (variable-length records)
+    int p = 4 + 2 * nA;
+    for (int v = 0; v < nnodes; ++v) {
+      OFF[v] = p;
+      const int nch = PG[p + 4];
+      p += 14;
+      for (int q = 0; q < nch; ++q) p += 2 + PG[p];
+    }
+  }
+  __syncwarp();
+  for (int v = nnodes - 1; v >= 0; --v) {
+    const int* R = PG + OFF[v];
+    const int s = R[0], f = R[1], w = R[2], nr = R[3];
+    const int64_t loff = rec64(R + 8), rb = rec64(R + 12);
+    if (v == nnodes - 1) {
+      const int ps = __ldg(S.sn_parent + s);
+      if (lane == 0 && ps >= 0) wait_flag(a.flags + ps, a.epoch);
+      __syncwarp();
+    }
+    const double* P = a.L + loff;
+    const double xi = (lane >= w && lane < nr) ? __ldcg(a.xp + __ldg(S.rows + rb + lane)) : 0.0;
+    double T = 0.0;  // lane c < w holds T[c]
+    for (int c = 0; c < w; ++c) {
+      double acc = (lane >= w && lane < nr) ? P[c * nr + lane] * xi : 0.0;
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+      if (lane == c) T = acc;
+    }
+    double xs = lane < w ? a.xp[f + lane] : 0.0;
+    for (int c = w - 1; c >= 0; --c) {
+      double vv = 0.0;
+      if (lane == c) {
+        vv = xs / __ldg(a.D + f + c) - T;
+        xs = vv;
+        a.xp[f + c] = vv;
+        a.x[__ldg(S.perm + f + c)] = vv;
+      }
+      vv = __shfl_sync(kFull, vv, c);
+      if (lane < c) T += P[lane * nr + c] * vv;
+    }
+    __syncwarp();
+  }
+}
+
 
 template <int NT>
 __device__ __forceinline__ void fwd_task(const SolveArgs& a, int s, int tid) {
@@ -769,14 +873,23 @@ __device__ __forceinline__ void bwd_task(const SolveArgs& a, int s, int tid) {
   }
 }
 
+// per warp: VS[32] + stack[kGrpStack] + program[kGrpProg ints] + record offsets[kGrpProg ints]
+constexpr int kSolWarp = 32 + kGrpStack + kGrpProg;  // doubles (two int arrays of kGrpProg = kGrpProg doubles)
+
 template <int NT>
 __global__ void __launch_bounds__(NT == 32 ? 128 : NT) fwd_kernel(SolveArgs a) {
   __shared__ int s_ticket;
+  extern __shared__ double s_sol[];
   const int tid = NT == 32 ? (threadIdx.x & 31) : threadIdx.x;
   Claim<NT> cl;
   for (;;) {
     const int t = cl.next(a.ticket, a.t0, a.t1, a.nleaf, tid, &s_ticket);
     if (t < 0) break;
+    if (NT == 32 && a.prog && t < a.nleaf) {
+      double* VS = s_sol + (threadIdx.x >> 5) * kSolWarp;
+      fwd_group(a, t, tid, VS, VS + 32, reinterpret_cast<int*>(VS + 32 + kGrpStack));
+      continue;
+    }
     for (int k = __ldg(a.tptr + t); k < __ldg(a.tptr + t + 1); ++k) fwd_task<NT>(a, __ldg(a.tasks + k), tid);
   }
 }
@@ -785,6 +898,7 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT) fwd_kernel(SolveArgs a) {
 template <int NT>
 __global__ void __launch_bounds__(NT == 32 ? 128 : NT) bwd_kernel(SolveArgs a) {
   __shared__ int s_ticket;
+  extern __shared__ double s_sol[];
   const int tid = NT == 32 ? (threadIdx.x & 31) : threadIdx.x;
   for (;;) {
     int t;
@@ -800,6 +914,12 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT) bwd_kernel(SolveArgs a) {
     }
     const int k = a.t1 - 1 - t;
     if (k < a.t0) break;
+    if (NT == 32 && a.prog && k < a.nleaf) {
+      double* VS = s_sol + (threadIdx.x >> 5) * kSolWarp;
+      int* PG = reinterpret_cast<int*>(VS + 32 + kGrpStack);
+      bwd_group(a, k, tid, PG, PG + kGrpProg);
+      continue;
+    }
     for (int j = __ldg(a.tptr + k + 1) - 1; j >= __ldg(a.tptr + k); --j) bwd_task<NT>(a, __ldg(a.tasks + j), tid);
   }
 }
@@ -915,6 +1035,7 @@ int persistent_grid(K fn, int threads, int ntasks, int smem = 0) {
 }
 
 unsigned long long* g_task_trace = nullptr;  // NCL_TASK_TRACE debugging
+constexpr int kSolSmem = 4 * kSolWarp * sizeof(double);
 static int g_fg = 0, g_fg2 = 0, g_sf = 0, g_sf2 = 0, g_sb = 0, g_sb2 = 0;
 constexpr int kFacSmem1 = 4 * (kGrpFront * kGrpFront + kGrpStack + kGrpProg / 2) * sizeof(double);
 constexpr int kFacSmem2 = kCtaFront * kCtaFront * sizeof(double);
@@ -924,9 +1045,11 @@ static void init_grids() {
   cudaFuncSetAttribute(factor_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFacSmem2);
   g_fg = persistent_grid(factor_kernel<32>, 128, 1 << 30, kFacSmem1);
   g_fg2 = persistent_grid(factor_kernel<256>, 256, 1 << 30, kFacSmem2);
-  g_sf = persistent_grid(fwd_kernel<32>, 128, 1 << 30);
+  cudaFuncSetAttribute(fwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSolSmem);
+  cudaFuncSetAttribute(bwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSolSmem);
+  g_sf = persistent_grid(fwd_kernel<32>, 128, 1 << 30, kSolSmem);
   g_sf2 = persistent_grid(fwd_kernel<256>, 256, 1 << 30);
-  g_sb = persistent_grid(bwd_kernel<32>, 128, 1 << 30);
+  g_sb = persistent_grid(bwd_kernel<32>, 128, 1 << 30, kSolSmem);
   g_sb2 = persistent_grid(bwd_kernel<256>, 256, 1 << 30);
 }
 
@@ -1008,8 +1131,8 @@ void dev_solve_fwd_list(const DevSymb& S, DevFactor& F, const double* b, const D
                         cudaStream_t st) {
   if (T.n == 0) return;
   SolveArgs fa{S, F.L, F.D, F.CV, F.xp, b, nullptr, S.flags + S.nsn, S.tickets + 2 * slot, S.epoch, 0, T.split,
-               T.ids, T.tptr, T.nleaf};
-  if (T.split > 0) COUNT(1), fwd_kernel<32><<<g_sf, 128, 0, st>>>(fa);
+               T.ids, T.tptr, T.prog, T.gpo, T.nleaf};
+  if (T.split > 0) COUNT(1), fwd_kernel<32><<<g_sf, 128, kSolSmem, st>>>(fa);
   if (T.split < T.n) {
     fa.ticket = S.tickets + 2 * slot + 1;
     fa.t0 = T.split;
@@ -1023,14 +1146,14 @@ void dev_solve_fwd_list(const DevSymb& S, DevFactor& F, const double* b, const D
 void dev_solve_bwd_list(const DevSymb& S, DevFactor& F, double* x, const DevTasks& T, int slot, cudaStream_t st) {
   if (T.n == 0) return;
   SolveArgs ba{S, F.L, F.D, F.CV, F.xp, nullptr, x, S.flags + 2 * S.nsn, S.tickets + 2 * slot, S.epoch, T.split,
-               T.n, T.ids, T.tptr, T.nleaf};
+               T.n, T.ids, T.tptr, T.prog, T.gpo, T.nleaf};
   if (T.split < T.n) COUNT(1), bwd_kernel<256><<<std::min(g_sb2, T.n - T.split), 256, 0, st>>>(ba);
   if (T.split > 0) {
     ba.ticket = S.tickets + 2 * slot + 1;
     ba.t0 = 0;
     ba.t1 = T.split;
     COUNT(1);
-    bwd_kernel<32><<<g_sb, 128, 0, st>>>(ba);
+    bwd_kernel<32><<<g_sb, 128, kSolSmem, st>>>(ba);
   }
 }
 
