@@ -504,9 +504,17 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
       }
       ++e;
     }
-    t.lvl_begin.push_back(i);
-    t.lvl_end.push_back(e);
-    t.big.push_back(std::move(big));
+    // merge levels without large fronts into one segment (one persistent
+    // launch, flags order them); a segment closes at a level holding large
+    // fronts, which run after that level's small fronts
+    if (!t.lvl_begin.empty() && t.big.back().empty()) {
+      t.lvl_end.back() = e;
+      t.big.back() = std::move(big);
+    } else {
+      t.lvl_begin.push_back(i);
+      t.lvl_end.push_back(e);
+      t.big.push_back(std::move(big));
+    }
     i = e;
   }
   return L;
