@@ -231,8 +231,12 @@ void dev_factor_big(const DevSymb& S, DevFactor& Fa, const double* kvals, int s,
     bf_gather<<<static_cast<int>(std::min<int64_t>((ne + 255) / 256, 4 * 148)), 256, 0, st>>>(a, g0, g1);
     g_kernel_launches += 1;
   }
-  for (int k0 = 0; k0 < w; k0 += kBs) {
-    const int k1 = std::min(w, k0 + kBs);
+  // panel width: 32 columns while a panel fits 220 KB of shared memory,
+  // narrower for very tall fronts (a function of nr only: deterministic)
+  int pw = kBs;
+  while (pw > 8 && static_cast<int64_t>(nr) * pw * 8 > 220 * 1024) pw /= 2;
+  for (int k0 = 0; k0 < w; k0 += pw) {
+    const int k1 = std::min(w, k0 + pw);
     const int psmem = (nr - k0) * (k1 - k0) * static_cast<int>(sizeof(double));
     if (psmem <= 220 * 1024) {
       if (psmem > 48 * 1024) cudaFuncSetAttribute(bf_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, psmem);
