@@ -366,6 +366,7 @@ struct ncl_symb {
   DevBuf<int> lay_nodes, lay_tptr, lay_prog;
   DevBuf<int64_t> lay_gpo;
   DevBuf<SnMeta> meta;
+  std::vector<DevBuf<BigDesc>> top_dev;
   bool dev_ready = false;
 };
 
@@ -493,12 +494,22 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
   for (int i = L.split; i < ntask;) {
     const int h = Z.height[node_of(i)];
     int e = i;
-    std::vector<int64_t> big;
+    std::vector<BigDesc> big;
     while (e < ntask && Z.height[node_of(e)] == h) {
       const int s = node_of(e);
       const int nr = static_cast<int>(Z.sn_rptr[s + 1] - Z.sn_rptr[s]);
       if (Z.big[s]) {
-        big.insert(big.end(), {s, Z.sn_first[s], Z.sn_first[s + 1] - Z.sn_first[s], nr, Z.gm_ptr[s], Z.gm_ptr[s + 1]});
+        BigDesc b{};
+        b.s = s;
+        b.f = Z.sn_first[s];
+        b.w = Z.sn_first[s + 1] - Z.sn_first[s];
+        b.nr = nr;
+        b.pw = 32;  // panel width: while a panel fits 220 KB of shared memory (a function of nr only)
+        while (b.pw > 8 && static_cast<int64_t>(nr) * b.pw * 8 > 220 * 1024) b.pw /= 2;
+        b.npan = (b.w + b.pw - 1) / b.pw;
+        b.g0 = Z.gm_ptr[s];
+        b.g1 = Z.gm_ptr[s + 1];
+        big.push_back(b);
         t.any_big = true;
         t.max_nr = std::max(t.max_nr, nr);
       }
@@ -506,7 +517,7 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
     }
     // merge levels without large fronts into one segment (one persistent
     // launch, flags order them); a segment closes at a level holding large
-    // fronts, which run after that level's small fronts
+    // fronts, which run (as one batch) after that level's small fronts
     if (!t.lvl_begin.empty() && t.big.back().empty()) {
       t.lvl_end.back() = e;
       t.big.back() = std::move(big);
@@ -517,7 +528,30 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
     }
     i = e;
   }
+  for (auto& seg : t.big) {  // scratch layout of each batch
+    int64_t fo = 0, wo = 0;
+    for (auto& b : seg) {
+      b.foff = fo;
+      b.woff = wo;
+      fo += static_cast<int64_t>(b.nr) * b.nr;
+      wo += static_cast<int64_t>(b.nr) * 32;
+    }
+    t.scratch_f = std::max(t.scratch_f, fo);
+    t.scratch_w = std::max(t.scratch_w, wo);
+  }
   return L;
+}
+
+// device copies of the per-segment large-front descriptors
+void upload_top(TopSched& t, std::vector<DevBuf<BigDesc>>& store) {
+  store.clear();
+  store.resize(t.big.size());
+  t.big_dev.assign(t.big.size(), nullptr);
+  for (size_t k = 0; k < t.big.size(); ++k)
+    if (!t.big[k].empty()) {
+      store[k].upload(t.big[k]);
+      t.big_dev[k] = store[k].p;
+    }
 }
 
 void upload_symb(ncl_symb* S) {
@@ -543,6 +577,7 @@ void upload_symb(ncl_symb* S) {
   S->cv_ptr.upload(Z.cv_ptr);
   S->cvsp.upload(Z.cvsp);
   S->cvsrc.upload(Z.cvsrc);
+  upload_top(S->lay.top, S->top_dev);
   S->lay_nodes.upload(S->lay.nodes);
   S->lay_prog.upload(S->lay.prog);
   S->lay_gpo.upload(S->lay.gpo);
@@ -654,7 +689,7 @@ API int ncl_symb_info_get(ncl_symb_t S, ncl_symb_info* info) {
     info->cb_storage = S->Z.cb_storage;
     info->nsplit = S->Z.nsplit;
     int nb = 0;
-    for (const auto& lv : S->lay.top.big) nb += static_cast<int>(lv.size() / 6);
+    for (const auto& lv : S->lay.top.big) nb += static_cast<int>(lv.size());
     info->n_big = nb;
     info->n_tasks = static_cast<int>(S->lay.tptr.size()) - 1;
   });
@@ -721,10 +756,9 @@ void alloc_fact(ncl_fact* f) {
   f->F.L = f->L.p;
   f->F.CB = f->CB.p;
   f->F.CV = f->CV.p;
-  if (f->S->lay.top.any_big) {  // scratch of the blocked large-front path
-    const int64_t mx = f->S->lay.top.max_nr;
-    f->bigF.alloc(mx * mx);
-    f->bigW.alloc(mx * 32);
+  if (f->S->lay.top.any_big) {  // scratch of the batched large-front path
+    f->bigF.alloc(f->S->lay.top.scratch_f);
+    f->bigW.alloc(f->S->lay.top.scratch_w);
     f->F.bigF = f->bigF.p;
     f->F.bigW = f->bigW.p;
   }
@@ -1009,6 +1043,7 @@ struct ncl_shard {
   DevBuf<double> send, recv;
   DevBuf<int> unrep;  // original indices this rank does not report (zeroed before the x all-reduce)
   TaskLayout layA, layB;
+  std::vector<DevBuf<BigDesc>> topA_dev, topB_dev;
   DevBuf<int> tA, tB, pA, pB;  // task pointers, group programs
   DevBuf<int64_t> gA, gB;
   int64_t nunrep = 0;
@@ -1019,6 +1054,8 @@ void shard_upload(ncl_shard* sh) {
   if (sh->dev_ready) return;
   ensure_init();
   upload_symb(sh->S);
+  upload_top(sh->layA.top, sh->topA_dev);
+  upload_top(sh->layB.top, sh->topB_dev);
   sh->listA.upload(sh->layA.nodes);
   sh->listB.upload(sh->layB.nodes);
   sh->tA.upload(sh->layA.tptr);
@@ -1052,6 +1089,16 @@ DevTasks tasks_A(ncl_shard* sh) {
 DevTasks tasks_B(ncl_shard* sh) {
   return DevTasks{sh->listB.p, sh->tB.p, sh->pB.p, sh->gB.p, static_cast<int>(sh->layB.tptr.size()) - 1,
                   sh->layB.nleaf, sh->layB.split, &sh->layB.top};
+}
+void grow_scratch(ncl_fact* F, ncl_shard* sh) {
+  const int64_t nf = std::max(sh->layA.top.scratch_f, sh->layB.top.scratch_f);
+  const int64_t nw = std::max(sh->layA.top.scratch_w, sh->layB.top.scratch_w);
+  if (nf > 0) {
+    F->bigF.alloc(std::max<int64_t>(nf, F->bigF.n));
+    F->bigW.alloc(std::max<int64_t>(nw, F->bigW.n));
+    F->F.bigF = F->bigF.p;
+    F->F.bigW = F->bigW.p;
+  }
 }
 void need_comm(const ncl_shard* sh) {
   if (sh->P.world == 1) return;
@@ -1122,6 +1169,7 @@ API int ncl_shard_refactorize(ncl_fact_t F, ncl_sym_t M, ncl_shard_t sh, double 
     ensure_dev(M, "factorize");
     shard_upload(sh);
     DevSymb& d = F->S->d;
+    grow_scratch(F, sh);
     dev_factor_begin(d, M->dp, F->F, M->vals.p, tol, g_stream);
     dev_factor_list(d, F->F, M->vals.p, tasks_A(sh), 0, g_stream);
     if (sh->P.world > 1) allgather_blocks(sh, F->F.CB, 0, d.flags, d.epoch);
@@ -1152,6 +1200,7 @@ API int ncl_shard_refactorize_emulated(ncl_fact_t F, ncl_sym_t M, ncl_shard_t* p
       shard_upload(plans[r]);
     }
     DevSymb& d = F->S->d;
+    for (int r = 0; r < G; ++r) grow_scratch(F, plans[r]);
     dev_factor_begin(d, M->dp, F->F, M->vals.p, tol, g_stream);
     for (int r = 0; r < G; ++r) dev_factor_list(d, F->F, M->vals.p, tasks_A(plans[r]), r, g_stream);
     dev_factor_list(d, F->F, M->vals.p, tasks_B(plans[0]), G, g_stream);

@@ -25,23 +25,25 @@ constexpr unsigned kFullMask = 0xffffffffu;
 
 struct BigArgs {
   DevSymb S;
-  int s, f, w, nr, m2;
-  double* F;        // scratch front, nr x nr column-major
-  double* Wb;       // scratch W = L21 * D for the current panel (nr x kBs)
-  double* L;        // panels
-  double* CB;       // contribution blocks
+  const BigDesc* d;   // the batch's fronts
+  double* Fs;         // scratch fronts (BigDesc::foff)
+  double* Ws;         // scratch W (BigDesc::woff)
+  double* L;          // panels
+  double* CB;         // contribution blocks
   double* D;
   const double* kvals;
   const double* thresh;
   int* zp;
 };
 
-// --- assembly: one thread per front entry that receives anything, summing
-// its sources (A value, then children's CB entries in ascending child order)
-// from the gather map — spread over the whole GPU
-__global__ void __launch_bounds__(256) bf_gather(BigArgs a, int64_t g0, int64_t g1) {
+// --- assembly: front blockIdx.y; one thread per front entry that receives
+// anything, summing its sources (A value, then the children's CB entries in
+// ascending child order) from the gather map
+__global__ void __launch_bounds__(256) bf_gather(BigArgs a) {
+  const BigDesc b = a.d[blockIdx.y];
   const DevSymb& S = a.S;
-  for (int64_t k = g0 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < g1;
+  double* F = a.Fs + b.foff;
+  for (int64_t k = b.g0 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < b.g1;
        k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     int64_t q = __ldg(S.gsp + k);
     const int64_t q1 = __ldg(S.gsp + k + 1);
@@ -62,19 +64,22 @@ __global__ void __launch_bounds__(256) bf_gather(BigArgs a, int64_t g0, int64_t 
       const int64_t src = __ldg(S.gsrc + q);
       acc += src < 0 ? __ldg(a.kvals + ~src) : __ldcg(a.CB + src);
     }
-    a.F[__ldg(S.gdst + k)] = acc;
+    F[__ldg(S.gdst + k)] = acc;
   }
 }
 
-// --- panel: unblocked LDLᵀ of columns [k0, k1) over rows [k0, nr) (one CTA)
-// staged in shared memory (rows k0..nr of the kBs panel columns), warps own
-// columns c2 and lanes rows in the rank-1 updates; then W(:, c-k0) =
-// L(:, c) * d_c for the rows below the panel.
-__global__ void __launch_bounds__(256) bf_panel(BigArgs a, int k0, int k1) {
-  extern __shared__ double Ps[];  // (nr - k0) x kBs, column-major, ld = nr - k0
-  const int nr = a.nr, ld = nr - k0, kw = k1 - k0;
+// --- panel step: front blockIdx.x factors its panel `step` (columns
+// [k0, k1), rows [k0, nr)) staged in shared memory: warps own columns c2,
+// lanes rows in the rank-1 updates; then W(:, c-k0) = L(:, c) d_c below it.
+__global__ void __launch_bounds__(256) bf_panel(BigArgs a, int step) {
+  extern __shared__ double Ps[];
+  const BigDesc b = a.d[blockIdx.x];
+  if (step >= b.npan) return;
+  const int nr = b.nr, k0 = step * b.pw, k1 = min(b.w, k0 + b.pw);
+  const int ld = nr - k0, kw = k1 - k0;
   const double thresh = __ldcg(a.thresh);
-  double* F = a.F;
+  double* F = a.Fs + b.foff;
+  double* W = a.Ws + b.woff;
   for (int e = threadIdx.x; e < ld * kw; e += blockDim.x) {
     const int c = e / ld, i = e % ld;
     Ps[e] = F[static_cast<int64_t>(k0 + c) * nr + k0 + i];
@@ -83,15 +88,15 @@ __global__ void __launch_bounds__(256) bf_panel(BigArgs a, int k0, int k1) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int c = 0; c < kw; ++c) {
     double* Pc = Ps + c * ld;
-    const double d = Pc[c];
+    const double dd = Pc[c];
     if (threadIdx.x == 0) {
-      a.D[a.f + k0 + c] = d;
-      if (fabs(d) <= thresh) atomicMin(a.zp, a.f + k0 + c);
+      a.D[b.f + k0 + c] = dd;
+      if (fabs(dd) <= thresh) atomicMin(a.zp, b.f + k0 + c);
     }
-    for (int i = c + 1 + threadIdx.x; i < ld; i += blockDim.x) Pc[i] = Pc[i] / d;
+    for (int i = c + 1 + threadIdx.x; i < ld; i += blockDim.x) Pc[i] = Pc[i] / dd;
     __syncthreads();
     for (int c2 = c + 1 + warp; c2 < kw; c2 += 8) {
-      const double dl = d * Pc[c2];
+      const double dl = dd * Pc[c2];
       double* P2 = Ps + c2 * ld;
       for (int i = c2 + lane; i < ld; i += 32) P2[i] -= Pc[i] * dl;
     }
@@ -101,40 +106,11 @@ __global__ void __launch_bounds__(256) bf_panel(BigArgs a, int k0, int k1) {
     const int c = e / ld, i = e % ld;
     F[static_cast<int64_t>(k0 + c) * nr + k0 + i] = Ps[e];
     const int gi = k0 + i;
-    a.Wb[static_cast<int64_t>(c) * nr + gi] = gi >= k1 ? Ps[e] * Ps[c * ld + c] : 0.0;
+    W[static_cast<int64_t>(c) * nr + gi] = gi >= k1 ? Ps[e] * Ps[c * ld + c] : 0.0;
   }
   for (int e = threadIdx.x; e < kw * k0; e += blockDim.x) {  // rows above the panel: W = 0
     const int c = e / k0, i = e % k0;
-    a.Wb[static_cast<int64_t>(c) * nr + i] = 0.0;
-  }
-}
-
-// --- panel: unblocked LDLᵀ of columns [k0, k1) over rows [k0, nr) (one CTA),
-// then W(:, c-k0) = L(:, c) * d_c for the rows below the panel.
-__global__ void __launch_bounds__(256) bf_panel_global(BigArgs a, int k0, int k1) {
-  const int nr = a.nr;
-  const double thresh = __ldcg(a.thresh);
-  double* F = a.F;
-  for (int c = k0; c < k1; ++c) {
-    double* Fc = F + static_cast<int64_t>(c) * nr;
-    const double d = Fc[c];
-    if (threadIdx.x == 0) {
-      a.D[a.f + c] = d;
-      if (fabs(d) <= thresh) atomicMin(a.zp, a.f + c);
-    }
-    for (int i = c + 1 + threadIdx.x; i < nr; i += blockDim.x) Fc[i] = Fc[i] / d;
-    __syncthreads();
-    const int rem = k1 - c - 1;
-    for (int64_t e = threadIdx.x; e < static_cast<int64_t>(rem) * nr; e += blockDim.x) {
-      const int c2 = c + 1 + static_cast<int>(e / nr), i = static_cast<int>(e % nr);
-      if (i >= c2) F[static_cast<int64_t>(c2) * nr + i] -= Fc[i] * (d * Fc[c2]);
-    }
-    __syncthreads();
-  }
-  for (int64_t e = threadIdx.x; e < static_cast<int64_t>(k1 - k0) * nr; e += blockDim.x) {
-    const int c = k0 + static_cast<int>(e / nr), i = static_cast<int>(e % nr);
-    const double* Fc = F + static_cast<int64_t>(c) * nr;
-    a.Wb[static_cast<int64_t>(c - k0) * nr + i] = i >= k1 ? Fc[i] * Fc[c] : 0.0;
+    W[static_cast<int64_t>(c) * nr + i] = 0.0;
   }
 }
 
@@ -144,25 +120,32 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double av, double b
                : "d"(av), "d"(bv));
 }
 
-// --- trailing update on the tensor cores: for the lower triangle of
-// [k1, nr)^2, F(i, j) -= sum_{c in [k0,k1)} L(i, c) W(j, c). Grid: one CTA per
-// 64x64 tile (ti >= tj), 4 warps of 32x32, k = kBs in steps of 4.
-__global__ void __launch_bounds__(128) bf_syrk_dmma(BigArgs a, int k0, int k1, int ntiles) {
+// --- trailing update of panel `step` on the tensor cores: front blockIdx.y,
+// 64x64 tile blockIdx.x of the lower triangle of [k1, nr)^2:
+// F(i, j) -= sum_{c in panel} L(i, c) W(j, c); 4 warps of 32x32, DMMA k = 4.
+__global__ void __launch_bounds__(128) bf_syrk_dmma(BigArgs a, int step) {
   __shared__ double As[kBs][kTile + 1];
   __shared__ double Bs[kBs][kTile + 1];
-  const int nr = a.nr;
-  // tile index -> (ti, tj), ti >= tj
-  int t = blockIdx.x, ti = 0;
+  const BigDesc b = a.d[blockIdx.y];
+  if (step >= b.npan) return;
+  const int nr = b.nr, k0 = step * b.pw, k1 = min(b.w, k0 + b.pw);
+  const int rest = nr - k1;
+  if (rest <= 0) return;
+  const int nt = (rest + kTile - 1) / kTile;
+  if (static_cast<int>(blockIdx.x) >= nt * (nt + 1) / 2) return;
+  int t = blockIdx.x, ti = 0;  // tile index -> (ti, tj), ti >= tj
   while (t > ti) t -= ++ti;
   const int tj = t;
   const int i0 = k1 + ti * kTile, j0 = k1 + tj * kTile;
   const int kw = k1 - k0;
+  const double* F = a.Fs + b.foff;
+  const double* W = a.Ws + b.woff;
   for (int e = threadIdx.x; e < kBs * kTile; e += blockDim.x) {
     const int c = e / kTile, r = e % kTile;
     const bool okc = c < kw;
     const int gi = i0 + r, gj = j0 + r;
-    As[c][r] = okc && gi < nr ? a.F[static_cast<int64_t>(k0 + c) * nr + gi] : 0.0;
-    Bs[c][r] = okc && gj < nr ? a.Wb[static_cast<int64_t>(c) * nr + gj] : 0.0;
+    As[c][r] = okc && gi < nr ? F[static_cast<int64_t>(k0 + c) * nr + gi] : 0.0;
+    Bs[c][r] = okc && gj < nr ? W[static_cast<int64_t>(c) * nr + gj] : 0.0;
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -185,6 +168,7 @@ __global__ void __launch_bounds__(128) bf_syrk_dmma(BigArgs a, int k0, int k1, i
 #pragma unroll
       for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], av[mi], bv[ni]);
   }
+  double* Fw = a.Fs + b.foff;
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
@@ -192,70 +176,82 @@ __global__ void __launch_bounds__(128) bf_syrk_dmma(BigArgs a, int k0, int k1, i
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int gi = i0 + wi + mi * 8 + g, gj = j0 + wj + ni * 8 + 2 * tg + h;
-        if (gi < nr && gj < nr && gi >= gj) a.F[static_cast<int64_t>(gj) * nr + gi] -= acc[mi][ni][h];
+        if (gi < nr && gj < nr && gi >= gj) Fw[static_cast<int64_t>(gj) * nr + gi] -= acc[mi][ni][h];
       }
 }
 
-__global__ void __launch_bounds__(256) bf_writeout(BigArgs a, int* flags, int epoch) {
-  const int nr = a.nr, w = a.w, m2 = a.m2;
-  double* P = a.L + __ldg(a.S.sn_loff + a.s);
-  double* C = a.CB + __ldg(a.S.cb_off + a.s);
+// --- write-back: front blockIdx.y, panel (w columns) to L, lower CB
+__global__ void __launch_bounds__(256) bf_writeout(BigArgs a) {
+  const BigDesc b = a.d[blockIdx.y];
+  const int nr = b.nr, w = b.w, m2 = nr - w;
+  const double* F = a.Fs + b.foff;
+  double* P = a.L + __ldg(a.S.sn_loff + b.s);
+  double* C = a.CB + __ldg(a.S.cb_off + b.s);
   const int64_t np = static_cast<int64_t>(w) * nr, nc = static_cast<int64_t>(m2) * m2;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < np + nc;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     if (e < np) {
-      P[e] = a.F[e];
+      P[e] = F[e];
     } else {
       const int64_t k = e - np;
       const int i = static_cast<int>(k % m2), j = static_cast<int>(k / m2);
-      if (i >= j) C[cb_col(j, m2) + i] = a.F[static_cast<int64_t>(w + j) * nr + (w + i)];
+      if (i >= j) C[cb_col(j, m2) + i] = F[static_cast<int64_t>(w + j) * nr + (w + i)];
     }
   }
 }
 
-__global__ void bf_publish(int* flags, int s, int epoch) {
+__global__ void bf_publish(const BigDesc* d, int nf, int* flags, int epoch) {
   __threadfence();
-  flags[s] = epoch;
+  for (int k = threadIdx.x; k < nf; k += blockDim.x) flags[d[k].s] = epoch;
 }
 
 }  // namespace
 
-// Factor one large supernode (all launches on st, in order). F / Wb: scratch
-// of nr*nr and nr*kBs doubles.
-void dev_factor_big(const DevSymb& S, DevFactor& Fa, const double* kvals, int s, int f, int w, int nr, int64_t g0,
-                    int64_t g1, double* F, double* Wb, cudaStream_t st) {
-  BigArgs a{S, s, f, w, nr, nr - w, F, Wb, Fa.L, Fa.CB, Fa.D, kvals, Fa.scal, Fa.istat};
-  cudaMemsetAsync(F, 0, static_cast<size_t>(nr) * nr * sizeof(double), st);
-  const int64_t ne = g1 - g0;
-  if (ne > 0) {
-    bf_gather<<<static_cast<int>(std::min<int64_t>((ne + 255) / 256, 4 * 148)), 256, 0, st>>>(a, g0, g1);
+// Factor all large fronts of one segment as a batch: one launch per phase
+// (assembly, each panel step, its DMMA trailing update, write-back), each
+// front on its own grid row. Per front the arithmetic equals processing it
+// alone.
+void dev_factor_big_batch(const DevSymb& S, DevFactor& Fa, const double* kvals, const std::vector<BigDesc>& h,
+                          const BigDesc* d, cudaStream_t st) {
+  const int nf = static_cast<int>(h.size());
+  if (nf == 0) return;
+  BigArgs a{S, d, Fa.bigF, Fa.bigW, Fa.L, Fa.CB, Fa.D, kvals, Fa.scal, Fa.istat};
+  int64_t fsz = 0, emax = 0, wmax = 0;
+  int steps = 0;
+  for (const BigDesc& b : h) {
+    fsz = std::max(fsz, b.foff + static_cast<int64_t>(b.nr) * b.nr);
+    emax = std::max(emax, b.g1 - b.g0);
+    wmax = std::max<int64_t>(wmax, static_cast<int64_t>(b.w) * b.nr + static_cast<int64_t>(b.nr - b.w) * (b.nr - b.w));
+    steps = std::max(steps, b.npan);
+  }
+  cudaMemsetAsync(Fa.bigF, 0, fsz * sizeof(double), st);
+  if (emax > 0) {
+    bf_gather<<<dim3(static_cast<unsigned>(std::min<int64_t>((emax + 255) / 256, 64)), nf), 256, 0, st>>>(a);
     g_kernel_launches += 1;
   }
-  // panel width: 32 columns while a panel fits 220 KB of shared memory,
-  // narrower for very tall fronts (a function of nr only: deterministic)
-  int pw = kBs;
-  while (pw > 8 && static_cast<int64_t>(nr) * pw * 8 > 220 * 1024) pw /= 2;
-  for (int k0 = 0; k0 < w; k0 += pw) {
-    const int k1 = std::min(w, k0 + pw);
-    const int psmem = (nr - k0) * (k1 - k0) * static_cast<int>(sizeof(double));
-    if (psmem <= 220 * 1024) {
-      if (psmem > 48 * 1024) cudaFuncSetAttribute(bf_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, psmem);
-      bf_panel<<<1, 256, psmem, st>>>(a, k0, k1);
-    } else {
-      bf_panel_global<<<1, 256, 0, st>>>(a, k0, k1);  // panels taller than shared memory
+  static int smem_set = 0;
+  if (!smem_set) {
+    cudaFuncSetAttribute(bf_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    smem_set = 1;
+  }
+  for (int k = 0; k < steps; ++k) {
+    int psmem = 0, tiles = 0;
+    for (const BigDesc& b : h) {
+      if (k >= b.npan) continue;
+      const int k0 = k * b.pw, k1 = std::min(b.w, k0 + b.pw);
+      psmem = std::max(psmem, (b.nr - k0) * (k1 - k0) * static_cast<int>(sizeof(double)));
+      const int nt = (b.nr - k1 + kTile - 1) / kTile;
+      tiles = std::max(tiles, nt * (nt + 1) / 2);
     }
-    const int rest = nr - k1;
+    bf_panel<<<nf, 256, psmem, st>>>(a, k);
     g_kernel_launches += 1;
-    if (rest > 0) {
-      const int nt = (rest + kTile - 1) / kTile;
-      const int ntiles = nt * (nt + 1) / 2;
-      bf_syrk_dmma<<<ntiles, 128, 0, st>>>(a, k0, k1, ntiles);
+    if (tiles > 0) {
+      bf_syrk_dmma<<<dim3(tiles, nf), 128, 0, st>>>(a, k);
       g_kernel_launches += 1;
     }
   }
-  const int64_t tot = static_cast<int64_t>(w) * nr + static_cast<int64_t>(nr - w) * (nr - w);
-  bf_writeout<<<static_cast<int>(std::min<int64_t>((tot + 255) / 256, 2048)), 256, 0, st>>>(a, S.flags, S.epoch);
-  bf_publish<<<1, 1, 0, st>>>(S.flags, s, S.epoch);
+  bf_writeout<<<dim3(static_cast<unsigned>(std::min<int64_t>((wmax + 255) / 256, 512)), nf), 256, 0, st>>>(a);
+  bf_publish<<<1, 256, 0, st>>>(d, nf, S.flags, S.epoch);
   g_kernel_launches += 2;
 }
 

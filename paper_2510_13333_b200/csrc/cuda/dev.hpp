@@ -23,11 +23,19 @@ extern int64_t g_kernel_launches;
 // Host-side schedule of the CTA part of a list when it holds fronts too large
 // for shared memory: per height level the [begin, end) index range in the
 // list and the large supernodes (s, f, w, nr) that run the blocked DMMA path.
+// One large front of a batch (csrc/cuda/bigfront.cu)
+struct BigDesc {
+  int s, f, w, nr, pw, npan;  // supernode, first column, width, rows, panel width, panels
+  int64_t g0, g1;             // gather-map entry range
+  int64_t foff, woff;         // offsets of its scratch front (nr^2) and W (nr * pw)
+};
 struct TopSched {
-  std::vector<int> lvl_begin, lvl_end;
-  std::vector<std::vector<int64_t>> big;  // per level: (s, f, w, nr, gather begin, gather end) sextuples
+  std::vector<int> lvl_begin, lvl_end;   // segments of the CTA part (task index ranges)
+  std::vector<std::vector<BigDesc>> big;  // per segment: its large fronts (run as one batch)
+  std::vector<const BigDesc*> big_dev;    // per segment: device copy of `big`
   bool any_big = false;
   int max_nr = 0;
+  int64_t scratch_f = 0, scratch_w = 0;   // largest per-segment scratch (doubles)
 };
 // Packed per-supernode metadata (one 64-byte record, four 16-byte loads):
 // everything a small-front task needs before touching the numbers.
@@ -153,8 +161,9 @@ void dev_shard_pack(const DevSymb& S, const double* src, const int* bids, const 
 void dev_shard_unpack(const DevSymb& S, double* dst, const int* bids, const int* bowner, const int64_t* pack_off,
                       int nb, int rank, int cv, const double* recv, int64_t chunk, int* flags, int epoch,
                       cudaStream_t st);
-void dev_factor_big(const DevSymb& S, DevFactor& F, const double* kvals, int s, int f, int w, int nr, int64_t g0,
-                    int64_t g1, double* Fs, double* Wb, cudaStream_t st);
+// all large fronts of one segment, batched (same arithmetic per front as one at a time)
+void dev_factor_big_batch(const DevSymb& S, DevFactor& F, const double* kvals, const std::vector<BigDesc>& h,
+                          const BigDesc* d, cudaStream_t st);
 void dev_zero_indexed(double* x, const int* idx, int64_t n, cudaStream_t st);
 void dev_factor(const DevSymb& S, const DevPattern& P, DevFactor& F, const double* kvals, double pivot_tol,
                 cudaStream_t st, const TopSched* top = nullptr);

@@ -1081,7 +1081,7 @@ void dev_factor_list(const DevSymb& S, DevFactor& F, const double* kvals, const 
     a.nleaf = 0;
     for (size_t L = 0; L < ts.lvl_begin.size(); ++L) {
       const int b = ts.lvl_begin[L], e = ts.lvl_end[L];
-      const int nsmall = (e - b) - static_cast<int>(ts.big[L].size() / 6);
+      const int nsmall = (e - b) - static_cast<int>(ts.big[L].size());
       if (nsmall > 0) {
         cudaMemsetAsync(S.tickets + kTickets - 1, 0, sizeof(int), st);
         a.ticket = S.tickets + kTickets - 1;
@@ -1090,11 +1090,7 @@ void dev_factor_list(const DevSymb& S, DevFactor& F, const double* kvals, const 
         COUNT(1);
         factor_kernel<256><<<std::min(g_fg2, e - b), 256, kFacSmem2, st>>>(a);
       }
-      for (size_t q = 0; q < ts.big[L].size(); q += 6) {
-        const int64_t* bq = ts.big[L].data() + q;
-        dev_factor_big(S, F, kvals, static_cast<int>(bq[0]), static_cast<int>(bq[1]), static_cast<int>(bq[2]),
-                       static_cast<int>(bq[3]), bq[4], bq[5], F.bigF, F.bigW, st);
-      }
+      if (!ts.big[L].empty()) dev_factor_big_batch(S, F, kvals, ts.big[L], ts.big_dev[L], st);
     }
     return;
   }
