@@ -817,15 +817,40 @@ __device__ __forceinline__ void fwd_task(const SolveArgs& a, int s, int tid) {
     team_sync<NT>();
   }
   }  // extend-add path
-  for (int c = 0; c < w; ++c) {
-    const double xc = xs[c];
-    const double* Pc = P + static_cast<int64_t>(c) * nr;
-    for (int i = c + 1 + tid; i < nr; i += NT) {
-      const double u = Pc[i] * xc;
-      if (i < w) xs[i] -= u;
-      else cv[i] -= u;
+  if constexpr (NT == 32) {
+    for (int c = 0; c < w; ++c) {
+      const double xc = xs[c];
+      const double* Pc = P + static_cast<int64_t>(c) * nr;
+      for (int i = c + 1 + tid; i < nr; i += NT) {
+        const double u = Pc[i] * xc;
+        if (i < w) xs[i] -= u;
+        else cv[i] -= u;
+      }
+      team_sync<NT>();
     }
-    team_sync<NT>();
+  } else {
+    // blocked: warp 0 solves each 32-column diagonal block (no CTA barrier
+    // per column), then all threads apply the block to the rows below it
+    const int lane = tid & 31;
+    for (int c0 = 0; c0 < w; c0 += 32) {
+      const int c1 = min(w, c0 + 32);
+      if (tid < 32) {
+        for (int c = c0; c < c1; ++c) {
+          const double xc = xs[c];
+          const int i = c0 + lane;
+          if (i > c && i < c1) xs[i] -= P[static_cast<int64_t>(c) * nr + i] * xc;
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+      for (int i = c1 + tid; i < nr; i += NT) {
+        double acc = 0.0;
+        for (int c = c0; c < c1; ++c) acc += P[static_cast<int64_t>(c) * nr + i] * xs[c];
+        if (i < w) xs[i] -= acc;
+        else cv[i] -= acc;
+      }
+      __syncthreads();
+    }
   }
   if (tid == 0) {
     __threadfence();
@@ -856,16 +881,46 @@ __device__ __forceinline__ void bwd_task(const SolveArgs& a, int s, int tid) {
     if (lane == 0) T[c] = acc;
   }
   team_sync<NT>();
-  for (int c = w - 1; c >= 0; --c) {
-    if (tid == 0) {
-      const double v = xs[c] / __ldg(a.D + f + c) - T[c];
-      xs[c] = v;
-      a.x[__ldg(S.perm + f + c)] = v;
+  if constexpr (NT == 32) {
+    for (int c = w - 1; c >= 0; --c) {
+      if (tid == 0) {
+        const double v = xs[c] / __ldg(a.D + f + c) - T[c];
+        xs[c] = v;
+        a.x[__ldg(S.perm + f + c)] = v;
+      }
+      team_sync<NT>();
+      const double v = xs[c];
+      for (int c2 = tid; c2 < c; c2 += NT) T[c2] += P[static_cast<int64_t>(c2) * nr + c] * v;
+      team_sync<NT>();
     }
-    team_sync<NT>();
-    const double v = xs[c];
-    for (int c2 = tid; c2 < c; c2 += NT) T[c2] += P[static_cast<int64_t>(c2) * nr + c] * v;
-    team_sync<NT>();
+  } else {
+    // blocked from the bottom: warp 0 solves a 32-column block, then all
+    // threads fold it into T of the columns above
+    for (int c1 = w; c1 > 0; c1 -= 32) {
+      const int c0 = max(0, c1 - 32);
+      if (tid < 32) {
+        for (int c = c1 - 1; c >= c0; --c) {
+          if (lane == 0) {
+            const double v = xs[c] / __ldg(a.D + f + c) - T[c];
+            xs[c] = v;
+            a.x[__ldg(S.perm + f + c)] = v;
+          }
+          __syncwarp();
+          const double v = xs[c];
+          const int c2 = c0 + lane;
+          if (c2 < c) T[c2] += P[static_cast<int64_t>(c2) * nr + c] * v;
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+      for (int c2 = tid; c2 < c0; c2 += NT) {
+        double acc = 0.0;
+        const double* Pc2 = P + static_cast<int64_t>(c2) * nr;
+        for (int c = c0; c < c1; ++c) acc += Pc2[c] * xs[c];
+        T[c2] += acc;
+      }
+      __syncthreads();
+    }
   }
   if (tid == 0) {
     __threadfence();
