@@ -97,11 +97,9 @@ void SymPattern::slot_trip_csr(std::vector<int>& ptr, std::vector<int>& idx) con
 // --- symbolic_order (sparse_sym.cpp:139-191) --------------------------------
 // Same rule: repeatedly eliminate the node with the lexicographically smallest
 // (current degree, original index); its neighbours become a clique. The
-// reference keeps a std::set of (degree,node); we keep a binary min-heap of
-// packed 64-bit keys with lazy invalidation (a popped key is live iff the node
-// is alive and its stored degree still equals the key's degree). Keys are
-// unique per (degree,node), so the pop sequence equals the set's begin()
-// sequence. Adjacency lists stay sorted; the clique merge is the same
+// reference keeps a std::set of (degree,node); we keep a bucket queue of
+// per-degree min-heaps with lazy invalidation (a popped entry is live iff the
+// node is alive and its current degree still equals the entry's degree). Adjacency lists stay sorted; the clique merge is the same
 // (adj[u] \ {v}) ∪ (clique \ {u}).
 std::vector<int> symbolic_order(int n, const std::vector<int>& cp, const std::vector<int>& ri) {
   std::vector<int> cnt(n + 1, 0);
@@ -128,13 +126,19 @@ std::vector<int> symbolic_order(int n, const std::vector<int>& cp, const std::ve
     a.erase(std::unique(a.begin(), a.end()), a.end());
   }
 
-  using Key = uint64_t;
-  auto key = [](int deg, int node) { return (static_cast<Key>(deg) << 32) | static_cast<uint32_t>(node); };
-  std::vector<Key> heapv;
-  heapv.reserve(static_cast<size_t>(n) * 4);
-  for (int i = 0; i < n; ++i) heapv.push_back(key(static_cast<int>(adj[i].size()), i));
-  std::priority_queue<Key, std::vector<Key>, std::greater<Key>> heap(std::greater<Key>(), std::move(heapv));
-
+  // Bucket queue: one min-heap of node ids per degree. Popping the smallest
+  // node of the smallest non-empty degree yields exactly the (degree, node)
+  // lexicographic sequence of one global heap (stale entries included), i.e.
+  // the reference std::set's begin() sequence.
+  std::vector<std::vector<int>> bucket(n + 1);
+  int dmin = n + 1;
+  auto push = [&](int d, int v) {
+    auto& b = bucket[d];
+    b.push_back(v);
+    std::push_heap(b.begin(), b.end(), std::greater<int>());
+    if (d < dmin) dmin = d;
+  };
+  for (int i = 0; i < n; ++i) push(static_cast<int>(adj[i].size()), i);
   std::vector<char> dead(n, 0);
   std::vector<int> perm;
   perm.reserve(n);
@@ -166,11 +170,14 @@ std::vector<int> symbolic_order(int n, const std::vector<int>& cp, const std::ve
     std::vector<int>().swap(adj[u]);
   };
   std::vector<int> clique, merged;
-  while (!heap.empty()) {
-    const Key k = heap.top();
-    heap.pop();
-    const int v = static_cast<int>(k & 0xffffffffu);
-    const int deg = static_cast<int>(k >> 32);
+  for (;;) {
+    while (dmin <= n && bucket[dmin].empty()) ++dmin;
+    if (dmin > n) break;
+    auto& bk = bucket[dmin];
+    std::pop_heap(bk.begin(), bk.end(), std::greater<int>());
+    const int v = bk.back();
+    bk.pop_back();
+    const int deg = dmin;
     if (dead[v] || deg != degree(v)) continue;
     perm.push_back(v);
     dead[v] = 1;
@@ -228,7 +235,7 @@ std::vector<int> symbolic_order(int n, const std::vector<int>& cp, const std::ve
         au.assign(merged.begin(), merged.end());  // au keeps (and only grows) its own buffer
         if (static_cast<int>(au.size()) > kBig) to_bitmap(u);
       }
-      if (degree(u) != old) heap.push(key(degree(u), u));
+      if (degree(u) != old) push(degree(u), u);
     }
     clique.clear();
     std::vector<int>().swap(clique);
