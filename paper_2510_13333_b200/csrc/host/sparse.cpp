@@ -524,6 +524,7 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
   // 6. A -> panel map, diagonal positions
   const int nnz = cp[n];
   Z.amap.resize(nnz);
+  std::vector<int> asn(nnz);  // target supernode of every A entry
   Z.diag_pos.clear();
   for (int c = 0; c < n; ++c)
     for (int p = cp[c]; p < cp[c + 1]; ++p) {
@@ -537,17 +538,12 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
       const int nr = static_cast<int>(Z.sn_rptr[s + 1] - Z.sn_rptr[s]);
       const int pos = static_cast<int>(std::lower_bound(rb, rb + nr, hi) - rb);
       Z.amap[p] = Z.sn_loff[s] + static_cast<int64_t>(lo - f) * nr + pos;
+      asn[p] = s;
     }
   // 6b. A entries grouped by target supernode (source slot, offset in panel)
   {
     Z.a_ptr.assign(nsn + 1, 0);
-    std::vector<int> asn(Z.amap.size());
-    for (size_t e = 0; e < Z.amap.size(); ++e) {
-      const int64_t off = Z.amap[e];
-      const int sn = static_cast<int>(std::upper_bound(Z.sn_loff.begin(), Z.sn_loff.end(), off) - Z.sn_loff.begin()) - 1;
-      asn[e] = sn;
-      Z.a_ptr[sn + 1]++;
-    }
+    for (size_t e = 0; e < Z.amap.size(); ++e) Z.a_ptr[asn[e] + 1]++;
     for (int sn = 0; sn < nsn; ++sn) Z.a_ptr[sn + 1] += Z.a_ptr[sn];
     Z.a_src.resize(Z.amap.size());
     Z.a_off.resize(Z.amap.size());
