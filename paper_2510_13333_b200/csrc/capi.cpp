@@ -446,7 +446,8 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
     for (int s : post) {
       const int acnt = static_cast<int>(Z.a_ptr[s + 1] - Z.a_ptr[s]);
       for (int e = 0; e < acnt; ++e) {
-        L.prog[aoff0 + afirst + e] = Z.a_off[Z.a_ptr[s] + e];
+        const int off = Z.a_off[Z.a_ptr[s] + e], nr_s = nrof(s);  // panel offset -> packed-lower front offset
+        L.prog[aoff0 + afirst + e] = static_cast<int>(cb_col(off / nr_s, nr_s)) + off % nr_s;
         L.prog[aoff0 + nA + afirst + e] = Z.a_src[Z.a_ptr[s] + e];
       }
       int pop = 0;

@@ -136,9 +136,9 @@ struct TaskLayout {
   std::vector<int64_t> gpo;  // [ngroups+1]
 };
 // per-warp shared-memory budget of a group task (csrc/cuda/ldlt.cu)
-constexpr int kGrpFront = 32;       // fronts of group nodes: nr <= 32
-constexpr int kGrpStack = 640;      // doubles: A values + contribution-block stack
-constexpr int kGrpProg = 768;       // ints: the group program
+constexpr int kGrpFront = 32;       // fronts of group nodes: nr <= 32 (packed lower: 528 doubles)
+constexpr int kGrpStack = 512;      // doubles: A values + contribution-block stack
+constexpr int kGrpProg = 640;       // ints: the group program
 
 constexpr int kTickets = 40;  // ticket counters per symbolic handle
 

@@ -429,10 +429,13 @@ __device__ __forceinline__ void small_task(const FactorArgs& a, int s, int lane,
   const int nr = m.nr, w = m.w, f = m.f, m2 = nr - w;
   if (wait_children)
     for (int q = m.c0 + lane; q < m.c1; q += 32) wait_flag(a.flags + __ldg(S.child + q), a.epoch);
-  for (int k = lane; k < nr * nr; k += 32) F[k] = 0.0;
+  // the front is PACKED lower (column c at cb_col(c, nr)): half the shared memory
+  for (int k = lane; k < nr * (nr + 1) / 2; k += 32) F[k] = 0.0;
   __syncwarp();
-  for (int e = lane; e < m.na; e += 32)
-    F[__ldg(S.aoff + m.a0 + e)] = __ldg(a.kvals + __ldg(S.asrc + m.a0 + e));
+  for (int e = lane; e < m.na; e += 32) {
+    const int off = __ldg(S.aoff + m.a0 + e);
+    F[cb_col(off / nr, nr) + off % nr] = __ldg(a.kvals + __ldg(S.asrc + m.a0 + e));
+  }
   __syncwarp();
   for (int q0 = m.c0; q0 < m.c1; q0 += 32) {
     // lane k fetches child q0+k's metadata; then children in order
@@ -453,35 +456,36 @@ __device__ __forceinline__ void small_task(const FactorArgs& a, int s, int lane,
       const double* Cc = a.CB + cbk;
       for (int j = 0; j < m2c; ++j) {
         const int relj = __shfl_sync(kFull, reli, j);
-        if (lane >= j && lane < m2c) F[relj * nr + reli] += __ldcg(Cc + cb_col(j, m2c) + lane);
+        if (lane >= j && lane < m2c) F[cb_col(relj, nr) + reli] += __ldcg(Cc + cb_col(j, m2c) + lane);
       }
       __syncwarp();
     }
   }
   const int i = lane;
   for (int c = 0; c < w; ++c) {
-    const double d = F[c * nr + c];
+    const double d = F[cb_col(c, nr) + c];
     if (i == 0) {
       a.D[f + c] = d;
       if (fabs(d) <= thresh) atomicMin(a.zp, f + c);
     }
     double l = 0.0;
     if (i > c && i < nr) {
-      l = F[c * nr + i] / d;
-      F[c * nr + i] = l;
+      l = F[cb_col(c, nr) + i] / d;
+      F[cb_col(c, nr) + i] = l;
     }
     const double dl = d * l;
     for (int c2 = c + 1; c2 < nr; ++c2) {
       const double lc2 = __shfl_sync(kFull, dl, c2);
-      if (i >= c2 && i < nr) F[c2 * nr + i] -= l * lc2;
+      if (i >= c2 && i < nr) F[cb_col(c2, nr) + i] -= l * lc2;
     }
     __syncwarp();
   }
   double* P = a.L + m.loff;
   double* C = a.CB + m.cboff;
-  for (int k = lane; k < w * nr; k += 32) P[k] = F[k];
+  for (int c = 0; c < w; ++c)
+    if (lane < nr) P[c * nr + lane] = lane >= c ? F[cb_col(c, nr) + lane] : 0.0;
   for (int j = 0; j < m2; ++j)
-    if (lane >= j && lane < m2) C[cb_col(j, m2) + lane] = F[(w + j) * nr + (w + lane)];
+    if (lane >= j && lane < m2) C[cb_col(j, m2) + lane] = F[cb_col(w + j, nr) + w + lane];
   __syncwarp();
   if (publish && lane == 0) {
     __threadfence();
@@ -516,9 +520,9 @@ __device__ __forceinline__ void group_task(const FactorArgs& a, int g, int lane,
                           (static_cast<int64_t>(PG[p + 11]) << 32);
     p += 14;
     const int m2 = nr - w;
-    for (int k = lane; k < nr * nr; k += 32) F[k] = 0.0;
+    for (int k = lane; k < nr * (nr + 1) / 2; k += 32) F[k] = 0.0;  // packed lower front
     __syncwarp();
-    for (int e = lane; e < ac; e += 32) F[aoffs[af + e]] = ST[af + e];
+    for (int e = lane; e < ac; e += 32) F[aoffs[af + e]] = ST[af + e];  // program holds packed offsets
     __syncwarp();
     for (int q = 0; q < nch; ++q) {
       const int m2c = PG[p], off = PG[p + 1];
@@ -526,35 +530,36 @@ __device__ __forceinline__ void group_task(const FactorArgs& a, int g, int lane,
       const double* Cc = stack + off;
       for (int j = 0; j < m2c; ++j) {
         const int relj = __shfl_sync(kFull, reli, j);
-        if (lane >= j && lane < m2c) F[relj * nr + reli] += Cc[cb_col(j, m2c) + lane];
+        if (lane >= j && lane < m2c) F[cb_col(relj, nr) + reli] += Cc[cb_col(j, m2c) + lane];
       }
       p += 2 + m2c;
       __syncwarp();
     }
     const int i = lane;
     for (int c = 0; c < w; ++c) {
-      const double d = F[c * nr + c];
+      const double d = F[cb_col(c, nr) + c];
       if (i == 0) {
         a.D[f + c] = d;
         if (fabs(d) <= thresh) atomicMin(a.zp, f + c);
       }
       double l = 0.0;
       if (i > c && i < nr) {
-        l = F[c * nr + i] / d;
-        F[c * nr + i] = l;
+        l = F[cb_col(c, nr) + i] / d;
+        F[cb_col(c, nr) + i] = l;
       }
       const double dl = d * l;
       for (int c2 = c + 1; c2 < nr; ++c2) {
         const double lc2 = __shfl_sync(kFull, dl, c2);
-        if (i >= c2 && i < nr) F[c2 * nr + i] -= l * lc2;
+        if (i >= c2 && i < nr) F[cb_col(c2, nr) + i] -= l * lc2;
       }
       __syncwarp();
     }
     double* P = a.L + loff;
-    for (int k = lane; k < w * nr; k += 32) P[k] = F[k];
+    for (int c = 0; c < w; ++c)
+      if (lane < nr) P[c * nr + lane] = lane >= c ? F[cb_col(c, nr) + lane] : 0.0;
     double* C = push >= 0 ? stack + push : a.CB + cboff;
     for (int j = 0; j < m2; ++j)
-      if (lane >= j && lane < m2) C[cb_col(j, m2) + lane] = F[(w + j) * nr + (w + lane)];
+      if (lane >= j && lane < m2) C[cb_col(j, m2) + lane] = F[cb_col(w + j, nr) + w + lane];
     __syncwarp();
     if (push < 0 && lane == 0) {  // the group root publishes its CB
       __threadfence();
@@ -571,9 +576,10 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT) factor_kernel(FactorArgs 
   __shared__ int s_ticket;
   extern __shared__ double s_front[];
   const int tid = NT == 32 ? (threadIdx.x & 31) : threadIdx.x;
-  constexpr int kWarpSmem = kGrpFront * kGrpFront + kGrpStack + kGrpProg / 2;  // doubles per warp
+  constexpr int kFrontPk = kGrpFront * (kGrpFront + 1) / 2;              // packed lower 32 x 32
+  constexpr int kWarpSmem = kFrontPk + kGrpStack + kGrpProg / 2;          // doubles per warp
   double* F = NT == 32 ? s_front + (threadIdx.x >> 5) * kWarpSmem : s_front;
-  double* gST = F + kGrpFront * kGrpFront;
+  double* gST = F + kFrontPk;
   int* gPG = reinterpret_cast<int*>(gST + kGrpStack);
   const double thresh = __ldcg(a.thresh);
   Claim<NT> cl;
@@ -1092,7 +1098,7 @@ int persistent_grid(K fn, int threads, int ntasks, int smem = 0) {
 unsigned long long* g_task_trace = nullptr;  // NCL_TASK_TRACE debugging
 constexpr int kSolSmem = 4 * kSolWarp * sizeof(double);
 static int g_fg = 0, g_fg2 = 0, g_sf = 0, g_sf2 = 0, g_sb = 0, g_sb2 = 0;
-constexpr int kFacSmem1 = 4 * (kGrpFront * kGrpFront + kGrpStack + kGrpProg / 2) * sizeof(double);
+constexpr int kFacSmem1 = 4 * (kGrpFront * (kGrpFront + 1) / 2 + kGrpStack + kGrpProg / 2) * sizeof(double);
 constexpr int kFacSmem2 = kCtaFront * kCtaFront * sizeof(double);
 static void init_grids() {
   if (g_fg) return;
