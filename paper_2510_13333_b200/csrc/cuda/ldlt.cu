@@ -168,20 +168,43 @@ __device__ __forceinline__ void factor_task(const FactorArgs& a, int s, int tid,
     }
     team_sync<NT>();
   }
-  // 4. dense LDLᵀ of the w pivot columns (right-looking inside the panel)
-  for (int c = 0; c < w; ++c) {
-    double* Pc = P + static_cast<int64_t>(c) * nr;
-    const double dc = Pc[c];
-    if (tid == 0) {
-      a.D[f + c] = dc;
-      if (fabs(dc) <= thresh) atomicMin(a.zp, f + c);
+  // 4. dense LDLᵀ of the w pivot columns: blocked right-looking, 8-column
+  //    panels factored column by column, then one rank-8 update of the later
+  //    pivot columns (lanes over rows, no index division)
+  constexpr int kPb4 = 8;
+  for (int c0 = 0; c0 < w; c0 += kPb4) {
+    const int c1 = min(w, c0 + kPb4);
+    for (int c = c0; c < c1; ++c) {
+      double* Pc = P + static_cast<int64_t>(c) * nr;
+      const double dc = Pc[c];
+      if (tid == 0) {
+        a.D[f + c] = dc;
+        if (fabs(dc) <= thresh) atomicMin(a.zp, f + c);
+      }
+      for (int i = c + 1 + tid; i < nr; i += NT) Pc[i] = Pc[i] / dc;
+      team_sync<NT>();
+      for (int c2 = c + 1; c2 < c1; ++c2) {
+        const double dl = dc * Pc[c2];
+        double* P2 = P + static_cast<int64_t>(c2) * nr;
+        for (int i = c2 + tid; i < nr; i += NT) P2[i] -= Pc[i] * dl;
+      }
+      team_sync<NT>();
     }
-    for (int i = c + 1 + tid; i < nr; i += NT) Pc[i] = Pc[i] / dc;
-    team_sync<NT>();
-    const int rem = w - c - 1;
-    for (int e = tid; e < rem * nr; e += NT) {
-      const int c2 = c + 1 + e / nr, i = e % nr;
-      if (i >= c2) P[static_cast<int64_t>(c2) * nr + i] -= Pc[i] * (dc * Pc[c2]);
+    const int kb = c1 - c0;
+    for (int j = c1; j < w; ++j) {
+      double dlj[kPb4];
+#pragma unroll
+      for (int k = 0; k < kPb4; ++k)
+        dlj[k] = k < kb ? P[static_cast<int64_t>(c0 + k) * nr + (c0 + k)] * P[static_cast<int64_t>(c0 + k) * nr + j]
+                        : 0.0;
+      double* Pj = P + static_cast<int64_t>(j) * nr;
+      for (int i = j + tid; i < nr; i += NT) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < kPb4; ++k)
+          if (k < kb) acc += P[static_cast<int64_t>(c0 + k) * nr + i] * dlj[k];
+        Pj[i] -= acc;
+      }
     }
     team_sync<NT>();
   }
