@@ -209,15 +209,63 @@ __device__ __forceinline__ void factor_task(const FactorArgs& a, int s, int tid,
     team_sync<NT>();
   }
   // 5. Schur update of the contribution block: C -= L21 D L21ᵀ (lower)
-  for (int e = tid; e < m2 * m2; e += NT) {
-    const int i = e % m2, j = e / m2;
-    if (i < j) continue;
-    double acc = 0.0;
-    for (int c = 0; c < w; ++c) {
-      const double* Pc = P + static_cast<int64_t>(c) * nr;
-      acc += Pc[w + i] * (Pc[c] * Pc[w + j]);
+  constexpr int kRows = 4;  // warp path: lane-held rows (m2 <= 128)
+  bool done5 = false;
+  if constexpr (NT == 32) {
+   if (m2 <= 32 * kRows) {
+    done5 = true;
+    // 4-column chunks of L21 in registers (lane owns rows lane + 32 r);
+    // L(w+j, c) d_c broadcast by shuffles; one CB pass per chunk
+    const int lane = tid;
+    for (int c0 = 0; c0 < w; c0 += 4) {
+      const int kb = min(4, w - c0);
+      double dd[4], Lr[kRows][4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) dd[k] = k < kb ? P[static_cast<int64_t>(c0 + k) * nr + (c0 + k)] : 0.0;
+#pragma unroll
+      for (int r = 0; r < kRows; ++r)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int i = lane + 32 * r;
+          Lr[r][k] = (i < m2 && k < kb) ? P[static_cast<int64_t>(c0 + k) * nr + w + i] : 0.0;
+        }
+      for (int j = 0; j < m2; ++j) {
+        const int rj = j >> 5, lj = j & 31;
+        double dl[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          double v = 0.0;
+#pragma unroll
+          for (int r = 0; r < kRows; ++r) v = r == rj ? Lr[r][k] : v;
+          dl[k] = dd[k] * __shfl_sync(kFull, v, lj);
+        }
+        double* Cj = C + cb_col(j, m2);
+#pragma unroll
+        for (int r = 0; r < kRows; ++r) {
+          const int i = lane + 32 * r;
+          if (i >= j && i < m2) {
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) acc += Lr[r][k] * dl[k];
+            Cj[i] -= acc;
+          }
+        }
+      }
+      __syncwarp();
     }
-    C[cb_col(j, m2) + i] -= acc;
+   }
+  }
+  if (!done5) {
+    for (int e = tid; e < m2 * m2; e += NT) {
+      const int i = e % m2, j = e / m2;
+      if (i < j) continue;
+      double acc = 0.0;
+      for (int c = 0; c < w; ++c) {
+        const double* Pc = P + static_cast<int64_t>(c) * nr;
+        acc += Pc[w + i] * (Pc[c] * Pc[w + j]);
+      }
+      C[cb_col(j, m2) + i] -= acc;
+    }
   }
   team_sync<NT>();
   if (tid == 0 && publish) {
