@@ -514,7 +514,7 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
   }
   // phase split: the narrow top of the tree (at most kTopTasks supernodes)
   // runs with a whole CTA per supernode, everything below with a warp each.
-  constexpr int kTopTasks = 2048;
+  constexpr int kTopTasks = 8192;
   Z.nsplit = nsn;
   for (int h = Z.max_height; h >= 0; --h) {
     if (nsn - hc[h] > kTopTasks) break;
