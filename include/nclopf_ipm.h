@@ -51,7 +51,7 @@ typedef struct ncl_options {
   double pivot_tol;     /* 1e-14 for the condensed K (sparse_sym.hpp:125 default 1e-12 is for O(1) diagonals) */
   /* linear solve (sparse_sym.hpp:136-139) */
   double refine_target; /* 1e-8 */
-  int refine_max_sweeps;/* 5 */
+  int refine_max_sweeps;/* 2 (solve_refined's own default is 5) */
   double mu_warm_frac;  /* warm start mu = max(mu_min, mu_warm_frac * omega_n) */
   double acceptable_factor; /* Ipopt 'acceptable' exit: E_0 <= acceptable_factor * omega_n ... */
   int acceptable_iter;      /* ... for this many consecutive iterations (10, 15) */

@@ -18,3 +18,8 @@ if len(sys.argv) > 3:
     t0 = time.time(); ref = ref_ncl_solve(R, s.bounds()); rr = ref["result"]
     print(json.dumps({"oracle": True, "status": ref["status"], "wall": time.time() - t0,
                       **{k: rr[k] for k in ["outer_iters", "inner_iters", "factorizations", "objective", "r_inf", "t_factor", "t_solve", "t_eval"]}}))
+import collections
+tr = [t for t in out.trace if "iter" in t]
+print(json.dumps({"sweeps": dict(collections.Counter(t["sweeps"] for t in tr)),
+                  "factorizations_per_iter": dict(collections.Counter(t["factorizations"] for t in tr)),
+                  "ls_backtracks": dict(collections.Counter(t["ls"] for t in tr))}))
