@@ -96,7 +96,7 @@ def _compare(g, r):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("grid,K", [("case9", 0), ("case9", 2), ("case118", 4)])
+@pytest.mark.parametrize("grid,K", [("case9", 0), ("case9", 2), ("case118", 4), ("case118", 16), ("activsg500", 16)])
 def test_gpu_solve_matches_oracle(gpu, grid, K):
     from paper_2510_13333_b200.ipm import solve_scopf
     s = Scopf(grid, K)
