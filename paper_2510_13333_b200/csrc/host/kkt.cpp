@@ -36,7 +36,7 @@ KktMap build_kkt(int n, int m, const std::vector<std::pair<int, int>>& hc,
         terms.push_back(static_cast<int>(a));
         terms.push_back(static_cast<int>(b));
       }
-  for (int64_t k = 0; k < nt; ++k) P.add(K.trow[k], K.tcol[k], 0.0);
+  P.add_pattern(K.trow, K.tcol);
   P.finalize();
   const int nnz = P.nnz();
   const auto& slot = P.trip_slot();

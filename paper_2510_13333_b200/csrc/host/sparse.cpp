@@ -30,6 +30,17 @@ void SymPattern::add(int row, int col, double value) {
   ++cursor_;
 }
 
+void SymPattern::add_pattern(const std::vector<int>& rows, const std::vector<int>& cols) {
+  if (finalized_) fail(NCL_E_LOGIC, "SparseSym::add: pattern already finalized");
+  for (size_t k = 0; k < rows.size(); ++k) {
+    if (rows[k] < cols[k]) fail(NCL_E_INVALID, "SparseSym::add: row < col (store lower triangle)");
+    if (cols[k] < 0 || rows[k] >= n_) fail(NCL_E_INVALID, "SparseSym::add: index out of range");
+  }
+  trows_.insert(trows_.end(), rows.begin(), rows.end());
+  tcols_.insert(tcols_.end(), cols.begin(), cols.end());
+  tvals_.resize(trows_.size(), 0.0);
+}
+
 // --- SparseSym::finalize (sparse_sym.cpp:28-56) -----------------------------
 // Stable (col,row) ordering realised as a stable counting sort on col
 // followed by a stable sort on row inside each column; identical order to the
@@ -37,18 +48,24 @@ void SymPattern::add(int row, int col, double value) {
 void SymPattern::finalize() {
   if (finalized_) fail(NCL_E_LOGIC, "SparseSym::finalize: already finalized");
   const int64_t nt = static_cast<int64_t>(trows_.size());
-  std::vector<int64_t> cstart(n_ + 1, 0);
-  for (int64_t k = 0; k < nt; ++k) cstart[tcols_[k] + 1]++;
-  for (int c = 0; c < n_; ++c) cstart[c + 1] += cstart[c];
-  std::vector<int> order(nt);
+  // LSD radix order: a stable counting sort by row, then a stable counting
+  // sort by column — the (col, row) order with ties in insertion order, i.e.
+  // exactly the reference's std::stable_sort result, in O(nt).
+  std::vector<int> by_row(nt), order(nt);
   {
-    std::vector<int64_t> fillp(cstart.begin(), cstart.end() - 1);
-    for (int64_t k = 0; k < nt; ++k) order[fillp[tcols_[k]]++] = static_cast<int>(k);
+    std::vector<int64_t> rs(n_ + 1, 0);
+    for (int64_t k = 0; k < nt; ++k) rs[trows_[k] + 1]++;
+    for (int r = 0; r < n_; ++r) rs[r + 1] += rs[r];
+    for (int64_t k = 0; k < nt; ++k) by_row[rs[trows_[k]]++] = static_cast<int>(k);
   }
-  for (int c = 0; c < n_; ++c) {
-    auto b = order.begin() + cstart[c], e = order.begin() + cstart[c + 1];
-    if (e - b > 1)
-      std::stable_sort(b, e, [&](int a, int bb) { return trows_[a] < trows_[bb]; });
+  {
+    std::vector<int64_t> cs(n_ + 1, 0);
+    for (int64_t k = 0; k < nt; ++k) cs[tcols_[k] + 1]++;
+    for (int c = 0; c < n_; ++c) cs[c + 1] += cs[c];
+    for (int64_t q = 0; q < nt; ++q) {
+      const int k = by_row[q];
+      order[cs[tcols_[k]]++] = k;
+    }
   }
   colptr_.assign(n_ + 1, 0);
   rowind_.clear();

@@ -32,6 +32,8 @@ class SymPattern {
 
   // throws Error{NCL_E_INVALID|NCL_E_LOGIC}
   void add(int row, int col, double value);
+  // bulk add() of zero-valued triplets before finalize (same checks)
+  void add_pattern(const std::vector<int>& rows, const std::vector<int>& cols);
   void finalize();
   void begin_refill();
   void refill();  // host-side merge of recorded triplets (reference refill semantics)
