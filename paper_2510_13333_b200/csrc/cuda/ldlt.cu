@@ -309,7 +309,8 @@ __device__ __forceinline__ double gather_sum(const DevSymb& S, const double* __r
 // overlap; each entry still sums its sources strictly in list order.
 template <int NT>
 __device__ __forceinline__ void gather4(const DevSymb& S, const double* __restrict__ kvals,
-                                        const double* __restrict__ CB, int64_t g0, int64_t g1, int tid, double* F) {
+                                        const double* __restrict__ CB, int64_t g0, int64_t g1, int tid, double* F,
+                                        int nr) {
   for (int64_t kb = g0 + tid; kb < g1; kb += 4 * NT) {
     int64_t q[4], q1[4];
     double acc[4];
@@ -333,7 +334,10 @@ __device__ __forceinline__ void gather4(const DevSymb& S, const double* __restri
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int64_t k = kb + u * NT;
-      if (k < g1) F[__ldg(S.gdst + k)] = acc[u];
+      if (k < g1) {
+        const int d = __ldg(S.gdst + k);  // full-layout position rj * nr + ri -> packed lower
+        F[cb_col(d / nr, nr) + d % nr] = acc[u];
+      }
     }
   }
 }
@@ -348,17 +352,22 @@ __device__ __forceinline__ void factor_task_smem(const FactorArgs& a, int s, int
   const int64_t rb = __ldg(S.sn_rptr + s);
   const int nr = static_cast<int>(__ldg(S.sn_rptr + s + 1) - rb);
   const int m2 = nr - w;
-  for (int k = tid; k < nr * nr; k += NT) F[k] = 0.0;
+  // the front is PACKED lower-triangular (column c at cb_col(c, nr)): 160 rows
+  // fit in 100 KB, two CTAs per SM
+  for (int k = tid; k < nr * (nr + 1) / 2; k += NT) F[k] = 0.0;
   team_sync<NT>();
   const int64_t g0 = NT == 32 ? 0 : __ldg(S.gm_ptr + s), g1 = NT == 32 ? 0 : __ldg(S.gm_ptr + s + 1);
   if (g1 > g0) {
     // gather-sum per front entry: A value first, then the children's CB
     // entries in ascending child order (the extend-add order)
-    gather4<NT>(S, a.kvals, a.CB, g0, g1, tid, F);
+    gather4<NT>(S, a.kvals, a.CB, g0, g1, tid, F, nr);
     team_sync<NT>();
   } else {
   for (int64_t e = __ldg(S.aptr + s) + tid; e < __ldg(S.aptr + s + 1); e += NT)
-    F[__ldg(S.aoff + e)] = __ldg(a.kvals + __ldg(S.asrc + e));  // panel offset c*nr + r == front offset
+    {
+      const int off = __ldg(S.aoff + e);  // panel offset c*nr + r
+      F[cb_col(off / nr, nr) + off % nr] = __ldg(a.kvals + __ldg(S.asrc + e));
+    }
   team_sync<NT>();
   if constexpr (NT == 32) {
     for (int q = __ldg(S.cptr + s); q < __ldg(S.cptr + s + 1); ++q) {
@@ -370,7 +379,7 @@ __device__ __forceinline__ void factor_task_smem(const FactorArgs& a, int s, int
       const double* Cc = a.CB + __ldg(S.cb_off + c);
       for (int j = 0; j < m2c; ++j) {
         const int rj = __ldg(rel + j);
-        for (int i = j + tid; i < m2c; i += 32) F[rj * nr + __ldg(rel + i)] += __ldcg(Cc + cb_col(j, m2c) + i);
+        for (int i = j + tid; i < m2c; i += 32) F[cb_col(rj, nr) + __ldg(rel + i)] += __ldcg(Cc + cb_col(j, m2c) + i);
       }
       __syncwarp();
     }
@@ -396,7 +405,7 @@ __device__ __forceinline__ void factor_task_smem(const FactorArgs& a, int s, int
       for (int j = lo; j < m2c; ++j) {
         const int rj = __ldg(rel + j);
         if (rj >= cb1) break;
-        double* Fj = F + rj * nr;
+        double* Fj = F + cb_col(rj, nr);
         const double* Cj = Cc + cb_col(j, m2c);
         for (int i = j + lane; i < m2c; i += 32) Fj[__ldg(rel + i)] += __ldcg(Cj + i);
       }
@@ -407,20 +416,20 @@ __device__ __forceinline__ void factor_task_smem(const FactorArgs& a, int s, int
   if constexpr (NT == 32) {
     const int i = tid;
     for (int c = 0; c < w; ++c) {
-      const double d = F[c * nr + c];
+      const double d = F[cb_col(c, nr) + c];
       if (i == 0) {
         a.D[f + c] = d;
         if (fabs(d) <= thresh) atomicMin(a.zp, f + c);
       }
       double l = 0.0;
       if (i > c && i < nr) {
-        l = F[c * nr + i] / d;
-        F[c * nr + i] = l;
+        l = F[cb_col(c, nr) + i] / d;
+        F[cb_col(c, nr) + i] = l;
       }
       const double dl = d * l;
       for (int c2 = c + 1; c2 < nr; ++c2) {
         const double lc2 = __shfl_sync(kFull, dl, c2);  // d * L(c2, c)
-        if (i >= c2 && i < nr) F[c2 * nr + i] -= l * lc2;
+        if (i >= c2 && i < nr) F[cb_col(c2, nr) + i] -= l * lc2;
       }
       __syncwarp();
     }
@@ -435,7 +444,7 @@ __device__ __forceinline__ void factor_task_smem(const FactorArgs& a, int s, int
       const int c1 = min(w, c0 + kPb);
       if (warp == 0) {
         for (int c = c0; c < c1; ++c) {
-          double* Fc = F + c * nr;
+          double* Fc = F + cb_col(c, nr);
           const double d = Fc[c];
           if (lane == 0) {
             a.D[f + c] = d;
@@ -445,7 +454,7 @@ __device__ __forceinline__ void factor_task_smem(const FactorArgs& a, int s, int
           __syncwarp();
           for (int c2 = c + 1; c2 < c1; ++c2) {
             const double dl = d * Fc[c2];
-            double* F2 = F + c2 * nr;
+            double* F2 = F + cb_col(c2, nr);
             for (int i = c2 + lane; i < nr; i += 32) F2[i] -= Fc[i] * dl;
           }
           __syncwarp();
@@ -456,13 +465,14 @@ __device__ __forceinline__ void factor_task_smem(const FactorArgs& a, int s, int
       for (int j = c1 + warp; j < nr; j += NT / 32) {
         double dlj[kPb];
 #pragma unroll
-        for (int k = 0; k < kPb; ++k) dlj[k] = k < kb ? F[(c0 + k) * nr + (c0 + k)] * F[(c0 + k) * nr + j] : 0.0;
-        double* Fj = F + j * nr;
+        for (int k = 0; k < kPb; ++k)
+          dlj[k] = k < kb ? F[cb_col(c0 + k, nr) + (c0 + k)] * F[cb_col(c0 + k, nr) + j] : 0.0;
+        double* Fj = F + cb_col(j, nr);
         for (int i = j + lane; i < nr; i += 32) {
           double acc = 0.0;
 #pragma unroll
           for (int k = 0; k < kPb; ++k)
-            if (k < kb) acc += F[(c0 + k) * nr + i] * dlj[k];
+            if (k < kb) acc += F[cb_col(c0 + k, nr) + i] * dlj[k];
           Fj[i] -= acc;
         }
       }
@@ -471,11 +481,14 @@ __device__ __forceinline__ void factor_task_smem(const FactorArgs& a, int s, int
   }
   double* P = a.L + __ldg(S.sn_loff + s);
   double* C = a.CB + __ldg(S.cb_off + s);
-  for (int k = tid; k < w * nr; k += NT) P[k] = F[k];
+  for (int k = tid; k < w * nr; k += NT) {
+    const int c = k / nr, i = k % nr;
+    P[k] = i >= c ? F[cb_col(c, nr) + i] : 0.0;
+  }
   {
     const int lane = tid & 31, warp = tid >> 5;
     for (int j = warp; j < m2; j += NT / 32) {
-      const double* Fj = F + (w + j) * nr + w;
+      const double* Fj = F + cb_col(w + j, nr) + w;
       double* Cj = C + cb_col(j, m2);
       for (int i = j + lane; i < m2; i += 32) Cj[i] = Fj[i];
     }
@@ -1170,7 +1183,7 @@ unsigned long long* g_task_trace = nullptr;  // NCL_TASK_TRACE debugging
 constexpr int kSolSmem = 4 * kSolWarp * sizeof(double);
 static int g_fg = 0, g_fg2 = 0, g_sf = 0, g_sf2 = 0, g_sb = 0, g_sb2 = 0;
 constexpr int kFacSmem1 = 4 * (kGrpFront * (kGrpFront + 1) / 2 + kGrpStack + kGrpProg / 2) * sizeof(double);
-constexpr int kFacSmem2 = kCtaFront * kCtaFront * sizeof(double);
+constexpr int kFacSmem2 = kCtaFront * (kCtaFront + 1) / 2 * sizeof(double);  // packed lower front
 static void init_grids() {
   if (g_fg) return;
   cudaFuncSetAttribute(factor_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFacSmem1);
