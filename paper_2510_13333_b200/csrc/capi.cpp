@@ -507,9 +507,14 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
         b.nr = nr;
         b.pw = 32;  // panel width: while a panel fits 220 KB of shared memory (a function of nr only)
         while (b.pw > 8 && static_cast<int64_t>(nr) * b.pw * 8 > 220 * 1024) b.pw /= 2;
-        b.npan = (b.w + b.pw - 1) / b.pw;
+        b.npan = nr <= 160 ? 0 : (b.w + b.pw - 1) / b.pw;  // <= kCtaFront: one CTA (dev_big_cta)
         b.g0 = Z.gm_ptr[s];
         b.g1 = Z.gm_ptr[s + 1];
+        // lanes per front entry in the assembly: ~4 sources per lane
+        const int64_t nsrc = b.g1 > b.g0 ? Z.gsp[b.g1] - Z.gsp[b.g0] : 0;
+        const int64_t per = b.g1 > b.g0 ? nsrc / (b.g1 - b.g0) : 0;
+        b.gsz = 1;
+        while (b.gsz < 32 && 4 * b.gsz < per) b.gsz *= 2;
         big.push_back(b);
         t.any_big = true;
         t.max_nr = std::max(t.max_nr, nr);

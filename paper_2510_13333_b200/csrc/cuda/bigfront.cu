@@ -36,35 +36,45 @@ struct BigArgs {
   int* zp;
 };
 
-// --- assembly: front blockIdx.y; one thread per front entry that receives
-// anything, summing its sources (A value, then the children's CB entries in
-// ascending child order) from the gather map
+// --- assembly: front blockIdx.y; a group of b.gsz lanes per front entry that
+// receives anything: lane r sums sources r, r + gsz, ... (A value first, then
+// the children's CB entries in ascending child order), the group combines its
+// partial sums by a fixed xor butterfly (gsz = 1: the plain sequential sum).
+// The per-front gsz is fixed by the symbolic analysis: deterministic.
 __global__ void __launch_bounds__(256) bf_gather(BigArgs a) {
   const BigDesc b = a.d[blockIdx.y];
   const DevSymb& S = a.S;
   double* F = a.Fs + b.foff;
-  for (int64_t k = b.g0 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < b.g1;
-       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    int64_t q = __ldg(S.gsp + k);
-    const int64_t q1 = __ldg(S.gsp + k + 1);
+  const int G = b.gsz, lane = threadIdx.x & 31;
+  const int per_warp = 32 / G;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  for (int64_t base = b.g0 + gw * per_warp; base < b.g1; base += nwarps * per_warp) {  // warp-uniform trip count
+    const int64_t k = base + lane / G;
+    const int r = lane % G;
     double acc = 0.0;
-    for (; q + 4 <= q1; q += 4) {
-      const int64_t s0 = __ldg(S.gsrc + q), s1 = __ldg(S.gsrc + q + 1), s2 = __ldg(S.gsrc + q + 2),
-                    s3 = __ldg(S.gsrc + q + 3);
-      const double v0 = s0 < 0 ? __ldg(a.kvals + ~s0) : __ldcg(a.CB + s0);
-      const double v1 = s1 < 0 ? __ldg(a.kvals + ~s1) : __ldcg(a.CB + s1);
-      const double v2 = s2 < 0 ? __ldg(a.kvals + ~s2) : __ldcg(a.CB + s2);
-      const double v3 = s3 < 0 ? __ldg(a.kvals + ~s3) : __ldcg(a.CB + s3);
-      acc += v0;
-      acc += v1;
-      acc += v2;
-      acc += v3;
+    if (k < b.g1) {
+      int64_t q = __ldg(S.gsp + k) + r;
+      const int64_t q1 = __ldg(S.gsp + k + 1);
+      for (; q + 3 * G < q1; q += 4 * G) {
+        const int64_t s0 = __ldg(S.gsrc + q), s1 = __ldg(S.gsrc + q + G), s2 = __ldg(S.gsrc + q + 2 * G),
+                      s3 = __ldg(S.gsrc + q + 3 * G);
+        const double v0 = s0 < 0 ? __ldg(a.kvals + ~s0) : __ldcg(a.CB + s0);
+        const double v1 = s1 < 0 ? __ldg(a.kvals + ~s1) : __ldcg(a.CB + s1);
+        const double v2 = s2 < 0 ? __ldg(a.kvals + ~s2) : __ldcg(a.CB + s2);
+        const double v3 = s3 < 0 ? __ldg(a.kvals + ~s3) : __ldcg(a.CB + s3);
+        acc += v0;
+        acc += v1;
+        acc += v2;
+        acc += v3;
+      }
+      for (; q < q1; q += G) {
+        const int64_t src = __ldg(S.gsrc + q);
+        acc += src < 0 ? __ldg(a.kvals + ~src) : __ldcg(a.CB + src);
+      }
     }
-    for (; q < q1; ++q) {
-      const int64_t src = __ldg(S.gsrc + q);
-      acc += src < 0 ? __ldg(a.kvals + ~src) : __ldcg(a.CB + src);
-    }
-    F[__ldg(S.gdst + k)] = acc;
+    for (int o = G >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(kFullMask, acc, o);
+    if (k < b.g1 && r == 0) F[__ldg(S.gdst + k)] = acc;
   }
 }
 
@@ -93,7 +103,7 @@ __global__ void __launch_bounds__(256) bf_panel(BigArgs a, int step) {
       a.D[b.f + k0 + c] = dd;
       if (fabs(dd) <= thresh) atomicMin(a.zp, b.f + k0 + c);
     }
-    for (int i = c + 1 + threadIdx.x; i < ld; i += blockDim.x) Pc[i] = Pc[i] / dd;
+    for (int i = c + 1 + threadIdx.x; i < ld; i += blockDim.x) Pc[i] = Pc[i] != 0.0 ? Pc[i] / dd : 0.0;  // zero numerators skip the slow path
     __syncthreads();
     for (int c2 = c + 1 + warp; c2 < kw; c2 += 8) {
       const double dl = dd * Pc[c2];
@@ -183,6 +193,7 @@ __global__ void __launch_bounds__(128) bf_syrk_dmma(BigArgs a, int step) {
 // --- write-back: front blockIdx.y, panel (w columns) to L, lower CB
 __global__ void __launch_bounds__(256) bf_writeout(BigArgs a) {
   const BigDesc b = a.d[blockIdx.y];
+  if (b.npan == 0) return;  // written by its CTA (dev_big_cta)
   const int nr = b.nr, w = b.w, m2 = nr - w;
   const double* F = a.Fs + b.foff;
   double* P = a.L + __ldg(a.S.sn_loff + b.s);
@@ -217,16 +228,17 @@ void dev_factor_big_batch(const DevSymb& S, DevFactor& Fa, const double* kvals, 
   if (nf == 0) return;
   BigArgs a{S, d, Fa.bigF, Fa.bigW, Fa.L, Fa.CB, Fa.D, kvals, Fa.scal, Fa.istat};
   int64_t fsz = 0, emax = 0, wmax = 0;
-  int steps = 0;
+  int steps = 0, ncta = 0;
   for (const BigDesc& b : h) {
     fsz = std::max(fsz, b.foff + static_cast<int64_t>(b.nr) * b.nr);
-    emax = std::max(emax, b.g1 - b.g0);
+    emax = std::max(emax, (b.g1 - b.g0) * b.gsz);
+    ncta += b.npan == 0;
     wmax = std::max<int64_t>(wmax, static_cast<int64_t>(b.w) * b.nr + static_cast<int64_t>(b.nr - b.w) * (b.nr - b.w));
     steps = std::max(steps, b.npan);
   }
   cudaMemsetAsync(Fa.bigF, 0, fsz * sizeof(double), st);
   if (emax > 0) {
-    bf_gather<<<dim3(static_cast<unsigned>(std::min<int64_t>((emax + 255) / 256, 64)), nf), 256, 0, st>>>(a);
+    bf_gather<<<dim3(static_cast<unsigned>(std::min<int64_t>((emax + 255) / 256, 1024)), nf), 256, 0, st>>>(a);
     g_kernel_launches += 1;
   }
   static int smem_set = 0;
@@ -234,6 +246,7 @@ void dev_factor_big_batch(const DevSymb& S, DevFactor& Fa, const double* kvals, 
     cudaFuncSetAttribute(bf_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     smem_set = 1;
   }
+  if (ncta > 0) dev_big_cta(S, Fa, d, nf, st);
   for (int k = 0; k < steps; ++k) {
     int psmem = 0, tiles = 0;
     for (const BigDesc& b : h) {
@@ -250,9 +263,10 @@ void dev_factor_big_batch(const DevSymb& S, DevFactor& Fa, const double* kvals, 
       g_kernel_launches += 1;
     }
   }
-  bf_writeout<<<dim3(static_cast<unsigned>(std::min<int64_t>((wmax + 255) / 256, 512)), nf), 256, 0, st>>>(a);
+  if (steps > 0)
+    bf_writeout<<<dim3(static_cast<unsigned>(std::min<int64_t>((wmax + 255) / 256, 512)), nf), 256, 0, st>>>(a);
   bf_publish<<<1, 256, 0, st>>>(d, nf, S.flags, S.epoch);
-  g_kernel_launches += 2;
+  g_kernel_launches += (steps > 0) + 1;
 }
 
 int big_front_panel() { return kBs; }

@@ -25,7 +25,8 @@ extern int64_t g_kernel_launches;
 // list and the large supernodes (s, f, w, nr) that run the blocked DMMA path.
 // One large front of a batch (csrc/cuda/bigfront.cu)
 struct BigDesc {
-  int s, f, w, nr, pw, npan;  // supernode, first column, width, rows, panel width, panels
+  int s, f, w, nr, pw, npan;  // supernode, first column, width, rows, panel width, panels (0: one-CTA front)
+  int gsz, pad_;              // lanes summing one front entry's gather sources (power of two)
   int64_t g0, g1;             // gather-map entry range
   int64_t foff, woff;         // offsets of its scratch front (nr^2) and W (nr * pw)
 };
@@ -162,6 +163,9 @@ void dev_shard_unpack(const DevSymb& S, double* dst, const int* bids, const int*
                       int nb, int rank, int cv, const double* recv, int64_t chunk, int* flags, int epoch,
                       cudaStream_t st);
 // all large fronts of one segment, batched (same arithmetic per front as one at a time)
+// one CTA per heavy-gather front with nr <= the CTA front cap (npan == 0):
+// scratch front (full layout, assembled) -> shared memory -> cta_dense
+void dev_big_cta(const DevSymb& S, DevFactor& F, const BigDesc* d, int nf, cudaStream_t st);
 void dev_factor_big_batch(const DevSymb& S, DevFactor& F, const double* kvals, const std::vector<BigDesc>& h,
                           const BigDesc* d, cudaStream_t st);
 void dev_zero_indexed(double* x, const int* idx, int64_t n, cudaStream_t st);

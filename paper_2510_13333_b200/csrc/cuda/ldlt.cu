@@ -26,6 +26,8 @@ namespace nclb {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kWarpFront = 32;    // nr cap of the warp smem path
+constexpr int kCtaFront = 160;    // nr cap of the CTA smem path (packed lower: 100 KB, two CTAs per SM)
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
@@ -46,6 +48,27 @@ __device__ __forceinline__ void wait_flag(const int* f, int epoch) {
   while (ld_acquire(f) != epoch) __nanosleep(32);
 }
 
+
+// x / d with a zero numerator short-circuited: the FP64 division's fast path
+// rejects x == 0 (exponent check) and CALLs the slow-path subroutine, and
+// fronts are full of structural zeros. Divides 1 / d instead (the operand is
+// laundered through asm so the compiler cannot fold the select back into the
+// division) and returns +0 (instead of a signed zero). Branch-free.
+__device__ __forceinline__ double divz(double x, double d) {
+  const bool z = x == 0.0;
+  double xs = z ? 1.0 : x;
+  asm("mov.b64 %0, %0;" : "+d"(xs));  // opaque: keeps x == 0 off the division's slow path
+  const double q = xs / d;  // branch-free: the lanes stay converged
+  return z ? 0.0 : q;
+}
+
+// FP64 tensor-core MMA (warp-wide, m8n8k4, row.col): {c0, c1} += A(g, tg) B(tg, g)
+// per lane g = lane / 4, tg = lane % 4 (tcgen05 has no f64 kind on sm_100a)
+__device__ __forceinline__ void dmma(double& c0, double& c1, double av, double bv) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(av), "d"(bv));
+}
 
 __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
   // non-negative doubles order like their bit patterns
@@ -131,8 +154,8 @@ template <int NT>
 __device__ __forceinline__ void factor_task(const FactorArgs& a, int s, int tid, double thresh,
                                             bool wait_children = true, bool publish = true) {
   const DevSymb& S = a.S;
-  if (tid == 0 && wait_children)
-    for (int q = __ldg(S.cptr + s); q < __ldg(S.cptr + s + 1); ++q) wait_flag(a.flags + __ldg(S.child + q), a.epoch);
+  if (wait_children)  // one thread per child: the polls overlap instead of chaining
+    for (int q = __ldg(S.cptr + s) + tid; q < __ldg(S.cptr + s + 1); q += NT) wait_flag(a.flags + __ldg(S.child + q), a.epoch);
   team_sync<NT>();
   const int f = __ldg(S.sn_first + s);
   const int w = __ldg(S.sn_first + s + 1) - f;
@@ -181,7 +204,7 @@ __device__ __forceinline__ void factor_task(const FactorArgs& a, int s, int tid,
         a.D[f + c] = dc;
         if (fabs(dc) <= thresh) atomicMin(a.zp, f + c);
       }
-      for (int i = c + 1 + tid; i < nr; i += NT) Pc[i] = Pc[i] / dc;
+      for (int i = c + 1 + tid; i < nr; i += NT) Pc[i] = divz(Pc[i], dc);
       team_sync<NT>();
       for (int c2 = c + 1; c2 < c1; ++c2) {
         const double dl = dc * Pc[c2];
@@ -342,11 +365,189 @@ __device__ __forceinline__ void gather4(const DevSymb& S, const double* __restri
   }
 }
 
+#ifdef NCL_DENSE_PROF  // tools/front_bench.cu: per-phase clocks of cta_dense (thread 0)
+__device__ long long g_dense_prof[5];
+#define DPROF_T0 long long dp_t = clock64();
+#define DPROF(k)                                  \
+  if (tid == 0) {                                 \
+    const long long dp_n = clock64();             \
+    g_dense_prof[k] += dp_n - dp_t;               \
+    dp_t = dp_n;                                  \
+  }
+#else
+#define DPROF_T0
+#define DPROF(k)
+#endif
+
+// Dense LDLᵀ of an assembled front in shared memory (packed lower, column c
+// at cb_col(c, nr)): factors its w pivot columns, writes the panel (nr x w,
+// column-major) to P and the Schur complement (packed lower m2 x m2) to C.
+template <int NT>
+__device__ __forceinline__ void cta_dense(double* F, int nr, int w, int f, double thresh, double* D, int* zp,
+                                          double* P, double* C, int tid) {
+  const int m2 = nr - w;
+  DPROF_T0
+  if constexpr (NT == 32) {
+    const int i = tid;
+    for (int c = 0; c < w; ++c) {
+      const double d = F[cb_col(c, nr) + c];
+      if (i == 0) {
+        D[f + c] = d;
+        if (fabs(d) <= thresh) atomicMin(zp, f + c);
+      }
+      double l = 0.0;
+      if (i > c && i < nr) {
+        l = divz(F[cb_col(c, nr) + i], d);
+        F[cb_col(c, nr) + i] = l;
+      }
+      const double dl = d * l;
+      for (int c2 = c + 1; c2 < nr; ++c2) {
+        const double lc2 = __shfl_sync(kFull, dl, c2);  // d * L(c2, c)
+        if (i >= c2 && i < nr) F[cb_col(c2, nr) + i] -= l * lc2;
+      }
+      __syncwarp();
+    }
+  } else {
+    // blocked right-looking LDLᵀ, panels of kPb = 8 columns:
+    //  (a) warp 0 factors the panel's kb x kb diagonal block in registers
+    //      (lane l holds block row c0 + l, pivots broadcast by shuffles);
+    //  (b) every thread takes one row below the block and finishes its kb
+    //      panel entries on its own (row-oriented: for each k, divide by d_k,
+    //      then subtract L(i,k) d_k L(k2,k) from the later k2 — the very
+    //      operations, in the very order, of the column-oriented update);
+    //  (c) all warps apply the rank-8 update F22 -= L21 (D L21)ᵀ to the
+    //      trailing lower triangle on the FP64 tensor cores (mma.m8n8k4.f64,
+    //      8 x 8 tiles, two k-steps), tiles dealt round-robin to the warps.
+    constexpr int kPb = 8;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, tg = lane & 3;
+    for (int c0 = 0; c0 < w; c0 += kPb) {
+      const int kb = min(kPb, w - c0);
+      if (warp == 0) {
+        double x[kPb];
+        const int i = c0 + lane;
+#pragma unroll
+        for (int k = 0; k < kPb; ++k) x[k] = (k < kb && k <= lane && lane < kb) ? F[cb_col(c0 + k, nr) + i] : 0.0;
+#pragma unroll
+        for (int k = 0; k < kPb; ++k) {
+          if (k < kb) {
+            const double d = __shfl_sync(kFull, x[k], k);
+            if (lane > k && lane < kb) x[k] = divz(x[k], d);
+            const double dlo = d * x[k];  // lane k2: d * L(c0 + k2, c0 + k)
+#pragma unroll
+            for (int k2 = 0; k2 < kPb; ++k2) {  // full range: unrolls with k
+              if (k2 > k && k2 < kb) {
+                const double dl = __shfl_sync(kFull, dlo, k2);
+                if (lane >= k2 && lane < kb) x[k2] -= x[k] * dl;
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < kPb; ++k)
+          if (k < kb && k <= lane && lane < kb) F[cb_col(c0 + k, nr) + i] = x[k];
+        if (lane < kb) {  // lane k's diagonal entry is the pivot d_k
+          double dk = 0.0;
+#pragma unroll
+          for (int k = 0; k < kPb; ++k)
+            if (k == lane) dk = x[k];
+          D[f + c0 + lane] = dk;
+          if (fabs(dk) <= thresh) atomicMin(zp, f + c0 + lane);
+        }
+      }
+      DPROF(0)
+      __syncthreads();
+      DPROF(1)
+      for (int i = c0 + kb + tid; i < nr; i += NT) {
+        double x[kPb];
+#pragma unroll
+        for (int k = 0; k < kPb; ++k) x[k] = k < kb ? F[cb_col(c0 + k, nr) + i] : 0.0;
+#pragma unroll
+        for (int k = 0; k < kPb; ++k) {
+          if (k < kb) {
+            const double* Lk = F + cb_col(c0 + k, nr);
+            const double d = Lk[c0 + k];
+            x[k] = divz(x[k], d);
+#pragma unroll
+            for (int k2 = 0; k2 < kPb; ++k2)
+              if (k2 > k && k2 < kb) x[k2] -= x[k] * (d * Lk[c0 + k2]);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < kPb; ++k)
+          if (k < kb) F[cb_col(c0 + k, nr) + i] = x[k];
+      }
+      __syncthreads();
+      DPROF(2)
+      const int c1 = c0 + kb, m = nr - c1;
+      if (m > 0) {
+        const int T = (m + 7) >> 3;
+        const int ka = tg, kc = tg + 4;  // this lane's two k indices (A column / B row)
+        const double* La = F + cb_col(c0 + ka, nr);
+        const double* Lc = F + cb_col(c0 + kc, nr);
+        const double da = ka < kb ? La[c0 + ka] : 0.0;
+        const double dc = kc < kb ? Lc[c0 + kc] : 0.0;
+        // tile rows ti dealt to the warps in snake order (row ti holds ti + 1
+        // tiles); per row the A fragments stay in registers and four tiles
+        // are in flight at a time (loads, 8 DMMAs, then the read-modify-writes)
+        for (int r = 0; r * 8 < T; ++r) {
+          const int ti = (r & 1) ? r * 8 + 7 - warp : r * 8 + warp;
+          if (ti >= T) continue;
+          const int i = c1 + ti * 8 + g;
+          double a0 = 0.0, a1 = 0.0;
+          if (i < nr) {
+            if (ka < kb) a0 = La[i];
+            if (kc < kb) a1 = Lc[i];
+          }
+          for (int tj0 = 0; tj0 <= ti; tj0 += 4) {
+            double b0[4], b1[4], acc[4][2];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int j = c1 + (tj0 + u) * 8 + g;
+              const bool ok = tj0 + u <= ti && j < nr;
+              b0[u] = ok && ka < kb ? da * La[j] : 0.0;
+              b1[u] = ok && kc < kb ? dc * Lc[j] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              acc[u][0] = acc[u][1] = 0.0;
+              dmma(acc[u][0], acc[u][1], a0, b0[u]);
+              dmma(acc[u][0], acc[u][1], a1, b1[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int jj = c1 + (tj0 + u) * 8 + 2 * tg;
+              if (tj0 + u <= ti && i < nr) {
+                if (jj < nr && i >= jj) F[cb_col(jj, nr) + i] -= acc[u][0];
+                if (jj + 1 < nr && i >= jj + 1) F[cb_col(jj + 1, nr) + i] -= acc[u][1];
+              }
+            }
+          }
+        }
+      }
+      __syncthreads();
+      DPROF(3)
+    }
+  }
+  for (int k = tid; k < w * nr; k += NT) {
+    const int c = k / nr, i = k % nr;
+    P[k] = i >= c ? F[cb_col(c, nr) + i] : 0.0;
+  }
+  {
+    const int lane = tid & 31, warp = tid >> 5;
+    for (int j = warp; j < m2; j += NT / 32) {
+      const double* Fj = F + cb_col(w + j, nr) + w;
+      double* Cj = C + cb_col(j, m2);
+      for (int i = j + lane; i < m2; i += 32) Cj[i] = Fj[i];
+    }
+  }
+  DPROF(4)
+}
+
 template <int NT>
 __device__ __forceinline__ void factor_task_smem(const FactorArgs& a, int s, int tid, double thresh, double* F) {
   const DevSymb& S = a.S;
-  if (tid == 0)
-    for (int q = __ldg(S.cptr + s); q < __ldg(S.cptr + s + 1); ++q) wait_flag(a.flags + __ldg(S.child + q), a.epoch);
+  for (int q = __ldg(S.cptr + s) + tid; q < __ldg(S.cptr + s + 1); q += NT) wait_flag(a.flags + __ldg(S.child + q), a.epoch);
   const int f = __ldg(S.sn_first + s);
   const int w = __ldg(S.sn_first + s + 1) - f;
   const int64_t rb = __ldg(S.sn_rptr + s);
@@ -413,86 +614,7 @@ __device__ __forceinline__ void factor_task_smem(const FactorArgs& a, int s, int
     __syncthreads();
   }
   }  // scatter / extend-add path
-  if constexpr (NT == 32) {
-    const int i = tid;
-    for (int c = 0; c < w; ++c) {
-      const double d = F[cb_col(c, nr) + c];
-      if (i == 0) {
-        a.D[f + c] = d;
-        if (fabs(d) <= thresh) atomicMin(a.zp, f + c);
-      }
-      double l = 0.0;
-      if (i > c && i < nr) {
-        l = F[cb_col(c, nr) + i] / d;
-        F[cb_col(c, nr) + i] = l;
-      }
-      const double dl = d * l;
-      for (int c2 = c + 1; c2 < nr; ++c2) {
-        const double lc2 = __shfl_sync(kFull, dl, c2);  // d * L(c2, c)
-        if (i >= c2 && i < nr) F[cb_col(c2, nr) + i] -= l * lc2;
-      }
-      __syncwarp();
-    }
-  } else {
-    // blocked right-looking LDLᵀ, panels of kPb columns:
-    //  (a) warp 0 factors the panel (rows c0..nr) with __syncwarp only,
-    //  (b) all warps apply the rank-kPb update to the trailing lower
-    //      triangle: warps own columns j, lanes rows i >= j.
-    constexpr int kPb = 8;
-    const int lane = tid & 31, warp = tid >> 5;
-    for (int c0 = 0; c0 < w; c0 += kPb) {
-      const int c1 = min(w, c0 + kPb);
-      if (warp == 0) {
-        for (int c = c0; c < c1; ++c) {
-          double* Fc = F + cb_col(c, nr);
-          const double d = Fc[c];
-          if (lane == 0) {
-            a.D[f + c] = d;
-            if (fabs(d) <= thresh) atomicMin(a.zp, f + c);
-          }
-          for (int i = c + 1 + lane; i < nr; i += 32) Fc[i] = Fc[i] / d;
-          __syncwarp();
-          for (int c2 = c + 1; c2 < c1; ++c2) {
-            const double dl = d * Fc[c2];
-            double* F2 = F + cb_col(c2, nr);
-            for (int i = c2 + lane; i < nr; i += 32) F2[i] -= Fc[i] * dl;
-          }
-          __syncwarp();
-        }
-      }
-      __syncthreads();
-      const int kb = c1 - c0;
-      for (int j = c1 + warp; j < nr; j += NT / 32) {
-        double dlj[kPb];
-#pragma unroll
-        for (int k = 0; k < kPb; ++k)
-          dlj[k] = k < kb ? F[cb_col(c0 + k, nr) + (c0 + k)] * F[cb_col(c0 + k, nr) + j] : 0.0;
-        double* Fj = F + cb_col(j, nr);
-        for (int i = j + lane; i < nr; i += 32) {
-          double acc = 0.0;
-#pragma unroll
-          for (int k = 0; k < kPb; ++k)
-            if (k < kb) acc += F[cb_col(c0 + k, nr) + i] * dlj[k];
-          Fj[i] -= acc;
-        }
-      }
-      __syncthreads();
-    }
-  }
-  double* P = a.L + __ldg(S.sn_loff + s);
-  double* C = a.CB + __ldg(S.cb_off + s);
-  for (int k = tid; k < w * nr; k += NT) {
-    const int c = k / nr, i = k % nr;
-    P[k] = i >= c ? F[cb_col(c, nr) + i] : 0.0;
-  }
-  {
-    const int lane = tid & 31, warp = tid >> 5;
-    for (int j = warp; j < m2; j += NT / 32) {
-      const double* Fj = F + cb_col(w + j, nr) + w;
-      double* Cj = C + cb_col(j, m2);
-      for (int i = j + lane; i < m2; i += 32) Cj[i] = Fj[i];
-    }
-  }
+  cta_dense<NT>(F, nr, w, f, thresh, a.D, a.zp, a.L + __ldg(S.sn_loff + s), a.CB + __ldg(S.cb_off + s), tid);
   team_sync<NT>();
   if (tid == 0) {
     __threadfence();
@@ -554,7 +676,7 @@ __device__ __forceinline__ void small_task(const FactorArgs& a, int s, int lane,
     }
     double l = 0.0;
     if (i > c && i < nr) {
-      l = F[cb_col(c, nr) + i] / d;
+      l = divz(F[cb_col(c, nr) + i], d);
       F[cb_col(c, nr) + i] = l;
     }
     const double dl = d * l;
@@ -628,7 +750,7 @@ __device__ __forceinline__ void group_task(const FactorArgs& a, int g, int lane,
       }
       double l = 0.0;
       if (i > c && i < nr) {
-        l = F[cb_col(c, nr) + i] / d;
+        l = divz(F[cb_col(c, nr) + i], d);
         F[cb_col(c, nr) + i] = l;
       }
       const double dl = d * l;
@@ -652,11 +774,9 @@ __device__ __forceinline__ void group_task(const FactorArgs& a, int g, int lane,
   }
 }
 
-constexpr int kWarpFront = 32;    // nr cap of the warp smem path
-constexpr int kCtaFront = 160;    // nr cap of the CTA smem path (160^2 doubles = 200 KB)
 
 template <int NT>
-__global__ void __launch_bounds__(NT == 32 ? 128 : NT) factor_kernel(FactorArgs a) {
+__global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 5 : 2) factor_kernel(FactorArgs a) {
   __shared__ int s_ticket;
   extern __shared__ double s_front[];
   const int tid = NT == 32 ? (threadIdx.x & 31) : threadIdx.x;
@@ -687,11 +807,28 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT) factor_kernel(FactorArgs 
       const int nr = static_cast<int>(__ldg(a.S.sn_rptr + s + 1) - __ldg(a.S.sn_rptr + s));
       if (a.skip_big && __ldg(a.S.big + s)) continue;  // runs on the large-front path
       if (NT == 32 && nr <= kWarpFront) small_task(a, s, tid, thresh, F, !group, !group || k == k1 - 1);
-      else if (nr <= (NT == 32 ? kWarpFront : kCtaFront)) factor_task_smem<NT>(a, s, tid, thresh, F);
+      else if (NT != 32 && nr <= kCtaFront) factor_task_smem<NT>(a, s, tid, thresh, F);
       else factor_task<NT>(a, s, tid, thresh, !group, !group || k == k1 - 1);
     }
     if (a.trace && tid == 0) a.trace[2 * t + 1] = gtimer();
   }
+}
+
+// Heavy-gather front that fits the CTA path: bf_gather assembled it (many
+// children, multi-CTA) into its full-layout scratch; one CTA factors it here
+// with the same arithmetic as the CTA smem path.
+__global__ void __launch_bounds__(256) big_cta_kernel(DevSymb S, const BigDesc* d, const double* Fs, double* L,
+                                                      double* CB, double* D, const double* thresh_p, int* zp) {
+  extern __shared__ double s_front[];
+  const BigDesc b = d[blockIdx.x];
+  if (b.npan != 0) return;
+  const int nr = b.nr, tid = threadIdx.x;
+  const double* G = Fs + b.foff;
+  for (int c = tid >> 5; c < nr; c += 8)
+    for (int i = c + (tid & 31); i < nr; i += 32) s_front[cb_col(c, nr) + i] = __ldcg(G + static_cast<int64_t>(c) * nr + i);
+  __syncthreads();
+  cta_dense<256>(s_front, nr, b.w, b.f, __ldcg(thresh_p), D, zp, L + __ldg(S.sn_loff + b.s), CB + __ldg(S.cb_off + b.s),
+                 tid);
 }
 
 __global__ void maxdiag_kernel(const int* __restrict__ pos, int nd, const double* __restrict__ v, double* out) {
@@ -850,7 +987,7 @@ __device__ void bwd_group(const SolveArgs& a, int g, int lane, int* PG, int* OFF
     for (int c = w - 1; c >= 0; --c) {
       double vv = 0.0;
       if (lane == c) {
-        vv = xs / __ldg(a.D + f + c) - T;
+        vv = divz(xs, __ldg(a.D + f + c)) - T;
         xs = vv;
         a.xp[f + c] = vv;
         a.x[__ldg(S.perm + f + c)] = vv;
@@ -866,8 +1003,7 @@ __device__ void bwd_group(const SolveArgs& a, int g, int lane, int* PG, int* OFF
 template <int NT>
 __device__ __forceinline__ void fwd_task(const SolveArgs& a, int s, int tid) {
   const DevSymb& S = a.S;
-  if (tid == 0)
-    for (int q = __ldg(S.cptr + s); q < __ldg(S.cptr + s + 1); ++q) wait_flag(a.flags + __ldg(S.child + q), a.epoch);
+  for (int q = __ldg(S.cptr + s) + tid; q < __ldg(S.cptr + s + 1); q += NT) wait_flag(a.flags + __ldg(S.child + q), a.epoch);
   team_sync<NT>();
   const int f = __ldg(S.sn_first + s);
   const int w = __ldg(S.sn_first + s + 1) - f;
@@ -974,7 +1110,7 @@ __device__ __forceinline__ void bwd_task(const SolveArgs& a, int s, int tid) {
   if constexpr (NT == 32) {
     for (int c = w - 1; c >= 0; --c) {
       if (tid == 0) {
-        const double v = xs[c] / __ldg(a.D + f + c) - T[c];
+        const double v = divz(xs[c], __ldg(a.D + f + c)) - T[c];
         xs[c] = v;
         a.x[__ldg(S.perm + f + c)] = v;
       }
@@ -991,7 +1127,7 @@ __device__ __forceinline__ void bwd_task(const SolveArgs& a, int s, int tid) {
       if (tid < 32) {
         for (int c = c1 - 1; c >= c0; --c) {
           if (lane == 0) {
-            const double v = xs[c] / __ldg(a.D + f + c) - T[c];
+            const double v = divz(xs[c], __ldg(a.D + f + c)) - T[c];
             xs[c] = v;
             a.x[__ldg(S.perm + f + c)] = v;
           }
@@ -1196,6 +1332,16 @@ static void init_grids() {
   g_sf2 = persistent_grid(fwd_kernel<256>, 256, 1 << 30);
   g_sb = persistent_grid(bwd_kernel<32>, 128, 1 << 30, kSolSmem);
   g_sb2 = persistent_grid(bwd_kernel<256>, 256, 1 << 30);
+}
+
+void dev_big_cta(const DevSymb& S, DevFactor& F, const BigDesc* d, int nf, cudaStream_t st) {
+  static int set = 0;
+  if (!set) {
+    cudaFuncSetAttribute(big_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFacSmem2);
+    set = 1;
+  }
+  big_cta_kernel<<<nf, 256, kFacSmem2, st>>>(S, d, F.bigF, F.L, F.CB, F.D, F.scal, F.istat);
+  COUNT(1);
 }
 
 void dev_factor_begin(const DevSymb& S0, const DevPattern& P, DevFactor& F, const double* kvals, double pivot_tol,

@@ -3,6 +3,7 @@
 #include "sparse.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <queue>
@@ -359,7 +360,10 @@ void true_L_structure(const SymbolicCore& S, std::vector<int64_t>& lp, std::vect
 Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
                             const std::vector<int>& ri, int relax) {
   constexpr int64_t kSmemFront = 160;       // = kCtaFront (csrc/cuda/ldlt.cu)
-  constexpr int64_t kHeavyGather = 400000;  // child entries one CTA assembles comfortably
+  // child entries one CTA assembles comfortably; beyond, the front is assembled
+  // by a multi-CTA gather (NCL_HEAVY_GATHER overrides: tests drive that path)
+  static const char* heavy_env = std::getenv("NCL_HEAVY_GATHER");
+  const int64_t kHeavyGather = heavy_env ? std::atoll(heavy_env) : 400000;
   const int n = S.n;
   Supernodal Z;
   // 1a. fundamental partition: j+1 joins j's supernode iff parent[j]==j+1 and

@@ -171,8 +171,27 @@ def test_large_front_dmma_path(gpu, n1, n2, dens):
     assert np.array_equal(Fa.diagonal(), D1)  # deterministic run to run
 
 
+def _heavy_gather_fronts(threshold):
+    """NCL_HEAVY_GATHER is read once per process: run the check in a child."""
+    import os
+    import subprocess
+    import sys
+    code = ("import tests.test_ldlt_gpu as t; t.test_scopf_kkt_parity(None, 'activsg500', 16, min_big=2)")
+    env = dict(os.environ, NCL_HEAVY_GATHER=str(threshold))
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.gpu
+def test_heavy_gather_fronts_multi_cta_assembly(gpu):
+    """Fronts with many child entries are assembled by the multi-CTA grouped
+    gather and (nr <= 160) factored by one CTA from the scratch front
+    (bigfront.cu bf_gather + ldlt.cu big_cta_kernel): forced on the 500x16 KKT."""
+    _heavy_gather_fronts(2000)
+
+
 @pytest.mark.parametrize("grid,K", [("case118", 16), ("activsg500", 16)])
-def test_scopf_kkt_parity(gpu, grid, K):
+def test_scopf_kkt_parity(gpu, grid, K, min_big=0):
     """The condensed SCOPF KKT (subtree groups with mid-size fronts, CTA top,
     separator root) against the reference factorize / solve."""
     from paper_2510_13333_b200.kkt import Kkt
@@ -185,6 +204,7 @@ def test_scopf_kkt_parity(gpu, grid, K):
                 10.0 + rng.random(M.m))
     A = kk.matrix
     S = ps.analyze(A)
+    assert S.info().n_big >= min_big
     F = ps.factorize(A, S)
     n = A.dim()
     cp, ri, v = A.col_ptr(), A.row_ind(), A.values()

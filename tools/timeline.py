@@ -1,0 +1,70 @@
+"""Per-phase / per-height timeline of one traced factorization.
+
+    NCL_TASK_TRACE=gpurun_out/trace.bin python bench.py --steps 2 --warmup 1 --no-solve --no-cpu-baseline
+    python tools/timeline.py gpurun_out/trace.bin [grid K]
+
+The trace (capi.cpp run_factor) holds per-task globaltimer start/end, the task
+layout (tptr, nodes); heights/parents come from re-running the symbolic
+analysis of the same KKT here (deterministic)."""
+import sys
+
+import numpy as np
+
+sys.path.insert(0, ".")
+
+
+def main():
+    path = sys.argv[1]
+    grid = sys.argv[2] if len(sys.argv) > 2 else "activsg500"
+    K = int(sys.argv[3]) if len(sys.argv) > 3 else 256
+    raw = open(path, "rb").read()
+    ntask, nleaf, split, _ = np.frombuffer(raw[:16], np.int32)
+    o = 16
+    tr = np.frombuffer(raw[o:o + 16 * ntask], np.uint64).reshape(ntask, 2).astype(np.int64)
+    o += 16 * ntask
+    tptr = np.frombuffer(raw[o:o + 4 * (ntask + 1)], np.int32)
+    o += 4 * (ntask + 1)
+    nodes = np.frombuffer(raw[o:], np.int32)
+    from paper_2510_13333_b200 import sparse as ps
+    from paper_2510_13333_b200.kkt import Kkt
+    from paper_2510_13333_b200.scopf import Scopf
+    sc = Scopf(grid, K, seed=2510)
+    S = ps.analyze(Kkt(sc.build_model()).matrix)
+    d = ps.supernodes(S)
+    h, par = d["height"], d["parent"]
+    w = np.diff(d["first"])
+    nr = np.diff(d["rptr"])
+    valid = tr[:, 0] > 0
+    t0 = tr[valid, 0].min()
+    st, en = (tr[:, 0] - t0) / 1e3, (tr[:, 1] - t0) / 1e3  # us
+    task_of = np.full(len(par), -1, np.int64)
+    for t in range(ntask):
+        task_of[nodes[tptr[t]:tptr[t + 1]]] = t
+    # ready time of a task: max end over the tasks of its nodes' children
+    ready = np.zeros(ntask)
+    for s_ in range(len(par)):
+        p = par[s_]
+        if p >= 0 and task_of[p] != task_of[s_] and task_of[p] >= 0 and task_of[s_] >= 0:
+            tp = task_of[p]
+            ready[tp] = max(ready[tp], en[task_of[s_]])
+    print(f"tasks {ntask} (groups {nleaf}, singles {split - nleaf}, cta {ntask - split}); end {en[valid].max():.1f} us")
+    for name, a, b in (("groups", 0, nleaf), ("singles", nleaf, split), ("cta", split, ntask)):
+        if b <= a:
+            continue
+        sl = slice(a, b)
+        print(f"{name:8s} start {st[sl].min():8.1f} end {en[sl].max():8.1f} mean dur {np.mean(en[sl] - st[sl]):7.2f} "
+              f"mean wait {np.mean(np.maximum(0, st[sl] - ready[sl])):7.2f}")
+    print("cta part by height of the task's last node: n, start, end, mean dur, p90 dur, mean nr, mean w, mean start-ready")
+    hl = np.array([h[nodes[tptr[t + 1] - 1]] for t in range(split, ntask)])
+    lastn = np.array([nodes[tptr[t + 1] - 1] for t in range(split, ntask)])
+    for lv in np.unique(hl):
+        m = hl == lv
+        idx = np.arange(split, ntask)[m]
+        du = en[idx] - st[idx]
+        print(f"  h={lv:2d} {m.sum():5d} {st[idx].min():8.1f} {en[idx].max():8.1f} {du.mean():7.2f} "
+              f"{np.percentile(du, 90):7.2f} {nr[lastn[m]].mean():6.1f} {w[lastn[m]].mean():5.1f} "
+              f"{np.mean(st[idx] - ready[idx]):7.2f}")
+
+
+if __name__ == "__main__":
+    main()
