@@ -929,15 +929,26 @@ __device__ void fwd_group(const SolveArgs& a, int g, int lane, double* VS, doubl
       __syncwarp();
     }
     const double* P = a.L + loff;
-    for (int c = 0; c < w; ++c) {
-      const double xc = VS[c];
-      if (lane > c && lane < nr) VS[lane] -= P[c * nr + lane] * xc;
-      __syncwarp();
+    // lane i owns row i in a register; panel columns are fetched eight at a
+    // time (all loads in flight), the pivots broadcast by shuffles
+    double y = lane < nr ? VS[lane] : 0.0;
+    for (int c0 = 0; c0 < w; c0 += 8) {
+      double pv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        pv[u] = (c0 + u < w && lane > c0 + u && lane < nr) ? __ldg(P + (c0 + u) * nr + lane) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (c0 + u < w) {
+          const double xc = __shfl_sync(kFull, y, c0 + u);
+          if (lane > c0 + u && lane < nr) y -= pv[u] * xc;
+        }
+      }
     }
-    if (lane < w) a.xp[f + lane] = VS[lane];
+    if (lane < w) a.xp[f + lane] = y;
     if (lane >= w && lane < nr) {
-      if (push >= 0) ST[push + (lane - w)] = VS[lane];
-      else a.CV[rb + lane] = VS[lane];
+      if (push >= 0) ST[push + (lane - w)] = y;
+      else a.CV[rb + lane] = y;
     }
     __syncwarp();
     if (push < 0 && lane == 0) {
@@ -976,29 +987,98 @@ __device__ void bwd_group(const SolveArgs& a, int g, int lane, int* PG, int* OFF
       __syncwarp();
     }
     const double* P = a.L + loff;
-    const double xi = (lane >= w && lane < nr) ? __ldcg(a.xp + __ldg(S.rows + rb + lane)) : 0.0;
+    const bool below = lane >= w && lane < nr;
+    const double xi = below ? __ldcg(a.xp + __ldg(S.rows + rb + lane)) : 0.0;
+    const double dl = lane < w ? __ldg(a.D + f + lane) : 1.0;
+    const int pl = lane < w ? __ldg(S.perm + f + lane) : 0;
     double T = 0.0;  // lane c < w holds T[c]
-    for (int c = 0; c < w; ++c) {
-      double acc = (lane >= w && lane < nr) ? P[c * nr + lane] * xi : 0.0;
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
-      if (lane == c) T = acc;
+    for (int c0 = 0; c0 < w; c0 += 8) {  // eight columns' loads and reductions in flight
+      double acc[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[u] = (c0 + u < w && below) ? __ldg(P + (c0 + u) * nr + lane) * xi : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] += __shfl_xor_sync(kFull, acc[u], o);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (lane == c0 + u) T = acc[u];
     }
     double xs = lane < w ? a.xp[f + lane] : 0.0;
-    for (int c = w - 1; c >= 0; --c) {
-      double vv = 0.0;
-      if (lane == c) {
-        vv = divz(xs, __ldg(a.D + f + c)) - T;
-        xs = vv;
-        a.xp[f + c] = vv;
-        a.x[__ldg(S.perm + f + c)] = vv;
+    for (int c1 = w; c1 > 0; c1 -= 8) {  // upper part: column c of row lane < c, eight at a time
+      double pu[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = c1 - 1 - u;
+        pu[u] = (c >= 0 && lane < c) ? __ldg(P + lane * nr + c) : 0.0;
       }
-      vv = __shfl_sync(kFull, vv, c);
-      if (lane < c) T += P[lane * nr + c] * vv;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = c1 - 1 - u;
+        if (c >= 0) {
+          double vv = 0.0;
+          if (lane == c) {
+            vv = divz(xs, dl) - T;
+            xs = vv;
+            a.xp[f + c] = vv;
+            a.x[pl] = vv;
+          }
+          vv = __shfl_sync(kFull, vv, c);
+          if (lane < c) T += pu[u] * vv;
+        }
+      }
     }
     __syncwarp();
   }
 }
 
+
+// Forward triangular part of a single (one warp, nr <= 32 kSl): lane l owns
+// rows l + 32 q in registers, pivots by shuffle, panel columns fetched four
+// at a time. Same operations and order as the column loop.
+template <int kSl>
+__device__ __forceinline__ void fwd_warp_reg(const double* __restrict__ P, int nr, int w, double* xs, double* cv,
+                                             int tid) {
+  double y[kSl];
+#pragma unroll
+  for (int q = 0; q < kSl; ++q) {
+    const int r = tid + 32 * q;
+    y[q] = r < nr ? (r < w ? xs[r] : cv[r]) : 0.0;
+  }
+  for (int c0 = 0; c0 < w; c0 += 4) {
+    double pv[4][kSl];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int q = 0; q < kSl; ++q) {
+        const int c = c0 + u, r = tid + 32 * q;
+        pv[u][q] = (c < w && r > c && r < nr) ? __ldg(P + static_cast<int64_t>(c) * nr + r) : 0.0;
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = c0 + u;
+      if (c < w) {
+        const int qc = c >> 5;
+        double yc = y[0];
+#pragma unroll
+        for (int q = 1; q < kSl; ++q) yc = qc == q ? y[q] : yc;
+        const double xc = __shfl_sync(kFull, yc, c & 31);
+#pragma unroll
+        for (int q = 0; q < kSl; ++q) {
+          const int r = tid + 32 * q;
+          if (r > c && r < nr) y[q] -= pv[u][q] * xc;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kSl; ++q) {
+    const int r = tid + 32 * q;
+    if (r < w) xs[r] = y[q];
+    else if (r < nr) cv[r] = y[q];
+  }
+  __syncwarp();
+}
 
 template <int NT>
 __device__ __forceinline__ void fwd_task(const SolveArgs& a, int s, int tid) {
@@ -1043,7 +1123,7 @@ __device__ __forceinline__ void fwd_task(const SolveArgs& a, int s, int tid) {
     team_sync<NT>();
   }
   }  // extend-add path
-  if constexpr (NT == 32) {
+  if (NT == 32 && nr > kCtaFront) {  // generic warp fallback (no such single in the SCOPF layouts)
     for (int c = 0; c < w; ++c) {
       const double xc = xs[c];
       const double* Pc = P + static_cast<int64_t>(c) * nr;
@@ -1054,19 +1134,33 @@ __device__ __forceinline__ void fwd_task(const SolveArgs& a, int s, int tid) {
       }
       team_sync<NT>();
     }
+  } else if constexpr (NT == 32) {
+    if (nr <= 32) fwd_warp_reg<1>(P, nr, w, xs, cv, tid);
+    else fwd_warp_reg<(kCtaFront + 31) / 32>(P, nr, w, xs, cv, tid);
   } else {
-    // blocked: warp 0 solves each 32-column diagonal block (no CTA barrier
-    // per column), then all threads apply the block to the rows below it
+    // blocked: warp 0 solves each 32-column diagonal block in registers
+    // (no CTA barrier per column), then all threads apply the block to the
+    // rows below it
     const int lane = tid & 31;
     for (int c0 = 0; c0 < w; c0 += 32) {
       const int c1 = min(w, c0 + 32);
       if (tid < 32) {
-        for (int c = c0; c < c1; ++c) {
-          const double xc = xs[c];
-          const int i = c0 + lane;
-          if (i > c && i < c1) xs[i] -= P[static_cast<int64_t>(c) * nr + i] * xc;
-          __syncwarp();
+        const int i = c0 + lane;
+        double y = i < c1 ? xs[i] : 0.0;
+        for (int c = c0; c < c1; c += 4) {
+          double pv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            pv[u] = (c + u < c1 && i > c + u && i < c1) ? __ldg(P + static_cast<int64_t>(c + u) * nr + i) : 0.0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (c + u < c1) {
+              const double xc = __shfl_sync(kFull, y, c + u - c0);
+              if (i > c + u && i < c1) y -= pv[u] * xc;
+            }
+          }
         }
+        if (i < c1) xs[i] = y;
       }
       __syncthreads();
       for (int i = c1 + tid; i < nr; i += NT) {
@@ -1084,6 +1178,80 @@ __device__ __forceinline__ void fwd_task(const SolveArgs& a, int s, int tid) {
   }
 }
 
+// Backward part of a single (one warp): registers throughout — lane l holds
+// the ancestor values of rows w + l + 32 q and T / x of pivot columns l + 32 q;
+// the same operation order as the shared-memory CTA version.
+template <int kSl>
+__device__ __forceinline__ void bwd_warp_reg(const SolveArgs& a, const double* __restrict__ P, const int* Rs, int f,
+                                             int nr, int w, double* xs, int lane) {
+  const DevSymb& S = a.S;
+  double xi[kSl], Tq[kSl], xq[kSl], dq[kSl];
+  int pq[kSl];
+#pragma unroll
+  for (int q = 0; q < kSl; ++q) {
+    const int i = w + lane + 32 * q, c = lane + 32 * q;
+    xi[q] = i < nr ? __ldcg(a.xp + __ldg(Rs + i)) : 0.0;
+    Tq[q] = 0.0;
+    xq[q] = c < w ? xs[c] : 0.0;
+    dq[q] = c < w ? __ldg(a.D + f + c) : 1.0;
+    pq[q] = c < w ? __ldg(S.perm + f + c) : 0;
+  }
+  for (int c0 = 0; c0 < w; c0 += 4) {
+    double acc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      acc[u] = 0.0;
+      const double* Pc = P + static_cast<int64_t>(c0 + u) * nr;
+#pragma unroll
+      for (int q = 0; q < kSl; ++q) {
+        const int i = w + lane + 32 * q;
+        if (c0 + u < w && i < nr) acc[u] += __ldg(Pc + i) * xi[q];
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u] += __shfl_xor_sync(kFull, acc[u], o);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = c0 + u;
+#pragma unroll
+      for (int q = 0; q < kSl; ++q)
+        if (c < w && c == lane + 32 * q) Tq[q] = acc[u];
+    }
+  }
+  for (int c1 = w; c1 > 0; c1 -= 2) {
+    double pu[2][kSl];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int q = 0; q < kSl; ++q) {
+        const int c = c1 - 1 - u, c2 = lane + 32 * q;
+        pu[u][q] = (c >= 0 && c2 < c) ? __ldg(P + static_cast<int64_t>(c2) * nr + c) : 0.0;
+      }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int c = c1 - 1 - u;
+      if (c >= 0) {
+        double v = 0.0;
+#pragma unroll
+        for (int q = 0; q < kSl; ++q)
+          if (c == lane + 32 * q) {
+            v = divz(xq[q], dq[q]) - Tq[q];
+            xq[q] = v;
+            xs[c] = v;
+            a.x[pq[q]] = v;
+          }
+        v = __shfl_sync(kFull, v, c & 31);
+#pragma unroll
+        for (int q = 0; q < kSl; ++q)
+          if (lane + 32 * q < c) Tq[q] += pu[u][q] * v;
+      }
+    }
+  }
+  __syncwarp();
+}
+
 template <int NT>
 __device__ __forceinline__ void bwd_task(const SolveArgs& a, int s, int tid) {
   const DevSymb& S = a.S;
@@ -1099,15 +1267,15 @@ __device__ __forceinline__ void bwd_task(const SolveArgs& a, int s, int tid) {
   double* T = a.CV + rb;  // the first w CV slots are free during the backward sweep
   double* xs = a.xp + f;
   const int lane = tid & 31, warp = tid >> 5;
-  for (int c = warp; c < w; c += NT / 32) {
-    const double* Pc = P + static_cast<int64_t>(c) * nr;
-    double acc = 0.0;
-    for (int i = w + lane; i < nr; i += 32) acc += Pc[i] * __ldcg(a.xp + __ldg(Rs + i));
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
-    if (lane == 0) T[c] = acc;
-  }
-  team_sync<NT>();
-  if constexpr (NT == 32) {
+  if (NT == 32 && nr > kCtaFront) {  // generic warp fallback (no such single in the SCOPF layouts)
+    for (int c = 0; c < w; ++c) {
+      const double* Pc = P + static_cast<int64_t>(c) * nr;
+      double acc = 0.0;
+      for (int i = w + lane; i < nr; i += 32) acc += Pc[i] * __ldcg(a.xp + __ldg(Rs + i));
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+      if (lane == 0) T[c] = acc;
+    }
+    team_sync<NT>();
     for (int c = w - 1; c >= 0; --c) {
       if (tid == 0) {
         const double v = divz(xs[c], __ldg(a.D + f + c)) - T[c];
@@ -1119,23 +1287,52 @@ __device__ __forceinline__ void bwd_task(const SolveArgs& a, int s, int tid) {
       for (int c2 = tid; c2 < c; c2 += NT) T[c2] += P[static_cast<int64_t>(c2) * nr + c] * v;
       team_sync<NT>();
     }
+  } else if constexpr (NT == 32) {
+    if (nr - w <= 32 && w <= 32) bwd_warp_reg<1>(a, P, Rs, f, nr, w, xs, lane);
+    else bwd_warp_reg<(kCtaFront + 31) / 32>(a, P, Rs, f, nr, w, xs, lane);
   } else {
+  for (int c = warp; c < w; c += NT / 32) {
+    const double* Pc = P + static_cast<int64_t>(c) * nr;
+    double acc = 0.0;
+    for (int i = w + lane; i < nr; i += 32) acc += Pc[i] * __ldcg(a.xp + __ldg(Rs + i));
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+    if (lane == 0) T[c] = acc;
+  }
+  team_sync<NT>();
     // blocked from the bottom: warp 0 solves a 32-column block, then all
     // threads fold it into T of the columns above
     for (int c1 = w; c1 > 0; c1 -= 32) {
       const int c0 = max(0, c1 - 32);
-      if (tid < 32) {
-        for (int c = c1 - 1; c >= c0; --c) {
-          if (lane == 0) {
-            const double v = divz(xs[c], __ldg(a.D + f + c)) - T[c];
-            xs[c] = v;
-            a.x[__ldg(S.perm + f + c)] = v;
+      if (tid < 32) {  // the 32-column block in registers: lane l is column c0 + l
+        const int c2 = c0 + lane;
+        const bool in = c2 < c1;
+        double Tl = in ? T[c2] : 0.0, xl = in ? xs[c2] : 0.0;
+        const double dl = in ? __ldg(a.D + f + c2) : 1.0;
+        for (int cb = c1 - 1; cb >= c0; cb -= 4) {
+          double pu[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int c = cb - u;
+            pu[u] = (c >= c0 && c2 < c) ? __ldg(P + static_cast<int64_t>(c2) * nr + c) : 0.0;
           }
-          __syncwarp();
-          const double v = xs[c];
-          const int c2 = c0 + lane;
-          if (c2 < c) T[c2] += P[static_cast<int64_t>(c2) * nr + c] * v;
-          __syncwarp();
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int c = cb - u;
+            if (c >= c0) {
+              double v = 0.0;
+              if (c2 == c) {
+                v = divz(xl, dl) - Tl;
+                xl = v;
+                a.x[__ldg(S.perm + f + c)] = v;
+              }
+              v = __shfl_sync(kFull, v, c - c0);
+              if (c2 < c) Tl += pu[u] * v;
+            }
+          }
+        }
+        if (in) {
+          xs[c2] = xl;
+          T[c2] = Tl;
         }
       }
       __syncthreads();
@@ -1158,7 +1355,7 @@ __device__ __forceinline__ void bwd_task(const SolveArgs& a, int s, int tid) {
 constexpr int kSolWarp = 32 + kGrpStack + kGrpProg;  // doubles (two int arrays of kGrpProg = kGrpProg doubles)
 
 template <int NT>
-__global__ void __launch_bounds__(NT == 32 ? 128 : NT) fwd_kernel(SolveArgs a) {
+__global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 6 : 4) fwd_kernel(SolveArgs a) {
   __shared__ int s_ticket;
   extern __shared__ double s_sol[];
   const int tid = NT == 32 ? (threadIdx.x & 31) : threadIdx.x;
@@ -1177,7 +1374,7 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT) fwd_kernel(SolveArgs a) {
 
 // tickets in reverse order (roots first); no leaf chunking
 template <int NT>
-__global__ void __launch_bounds__(NT == 32 ? 128 : NT) bwd_kernel(SolveArgs a) {
+__global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 6 : 4) bwd_kernel(SolveArgs a) {
   __shared__ int s_ticket;
   extern __shared__ double s_sol[];
   const int tid = NT == 32 ? (threadIdx.x & 31) : threadIdx.x;
