@@ -622,6 +622,9 @@ __device__ __forceinline__ void factor_task_smem(const FactorArgs& a, int s, int
   }
 }
 
+// cb_col in 32-bit arithmetic for the warp fronts (nr <= 32)
+__device__ __forceinline__ int cb32(int j, int m) { return j * m - ((j * (j + 1)) >> 1); }
+
 // Small front (nr <= 32) by one warp from the packed metadata: lane i owns
 // row i; children's metadata is fetched lane-parallel; the relative row map
 // of a child sits in registers (lane i holds rel[i]) and its CB columns are
@@ -640,7 +643,7 @@ __device__ __forceinline__ void small_task(const FactorArgs& a, int s, int lane,
   __syncwarp();
   for (int e = lane; e < m.na; e += 32) {
     const int off = __ldg(S.aoff + m.a0 + e);
-    F[cb_col(off / nr, nr) + off % nr] = __ldg(a.kvals + __ldg(S.asrc + m.a0 + e));
+    F[cb32(off / nr, nr) + off % nr] = __ldg(a.kvals + __ldg(S.asrc + m.a0 + e));
   }
   __syncwarp();
   for (int q0 = m.c0; q0 < m.c1; q0 += 32) {
@@ -660,38 +663,43 @@ __device__ __forceinline__ void small_task(const FactorArgs& a, int s, int lane,
       const long long rlk = __shfl_sync(kFull, static_cast<long long>(crel), k);
       const int reli = lane < m2c ? __ldg(S.relp + rlk + lane) : 0;
       const double* Cc = a.CB + cbk;
+      int co = 0;
       for (int j = 0; j < m2c; ++j) {
         const int relj = __shfl_sync(kFull, reli, j);
-        if (lane >= j && lane < m2c) F[cb_col(relj, nr) + reli] += __ldcg(Cc + cb_col(j, m2c) + lane);
+        if (lane >= j && lane < m2c) F[cb32(relj, nr) + reli] += __ldcg(Cc + co + lane);
+        co += m2c - j - 1;
       }
       __syncwarp();
     }
   }
   const int i = lane;
   for (int c = 0; c < w; ++c) {
-    const double d = F[cb_col(c, nr) + c];
+    const int offc = cb32(c, nr);
+    const double d = F[offc + c];
     if (i == 0) {
       a.D[f + c] = d;
       if (fabs(d) <= thresh) atomicMin(a.zp, f + c);
     }
     double l = 0.0;
     if (i > c && i < nr) {
-      l = divz(F[cb_col(c, nr) + i], d);
-      F[cb_col(c, nr) + i] = l;
+      l = divz(F[offc + i], d);
+      F[offc + i] = l;
     }
     const double dl = d * l;
+    int off2 = cb32(c + 1, nr);  // column c2's offset, advanced incrementally
     for (int c2 = c + 1; c2 < nr; ++c2) {
       const double lc2 = __shfl_sync(kFull, dl, c2);
-      if (i >= c2 && i < nr) F[cb_col(c2, nr) + i] -= l * lc2;
+      if (i >= c2 && i < nr) F[off2 + i] -= l * lc2;
+      off2 += nr - c2 - 1;
     }
     __syncwarp();
   }
   double* P = a.L + m.loff;
   double* C = a.CB + m.cboff;
-  for (int c = 0; c < w; ++c)
-    if (lane < nr) P[c * nr + lane] = lane >= c ? F[cb_col(c, nr) + lane] : 0.0;
-  for (int j = 0; j < m2; ++j)
-    if (lane >= j && lane < m2) C[cb_col(j, m2) + lane] = F[cb_col(w + j, nr) + w + lane];
+  for (int c = 0, fo = 0; c < w; fo += nr - c - 1, ++c)
+    if (lane < nr) P[c * nr + lane] = lane >= c ? F[fo + lane] : 0.0;
+  for (int j = 0, co = 0, fo = cb32(w, nr) + w; j < m2; co += m2 - j - 1, fo += nr - w - j - 1, ++j)
+    if (lane >= j && lane < m2) C[co + lane] = F[fo + lane];
   __syncwarp();
   if (publish && lane == 0) {
     __threadfence();
@@ -705,13 +713,12 @@ __device__ __forceinline__ void small_task(const FactorArgs& a, int s, int lane,
 // postorder), and only panels and the group root's CB go to global memory.
 // Per node the arithmetic is exactly small_task's.
 __device__ __forceinline__ void group_task(const FactorArgs& a, int g, int lane, double thresh, double* F,
-                                           double* ST, int* PG) {
+                                           double* ST) {
   const DevSymb& S = a.S;
-  const int* gp = a.prog + __ldg(a.gpo + g);
-  const int len = __ldg(gp + 3);
-  for (int k = lane; k < len; k += 32) PG[k] = __ldg(gp + k);
-  __syncwarp();
-  const int nnodes = PG[0], nA = PG[1];
+  // the program is read in place (read-only, L1-cached broadcast loads):
+  // shared memory holds only the front and the stack, so more warps fit
+  const int* __restrict__ PG = a.prog + __ldg(a.gpo + g);
+  const int nnodes = __ldg(PG), nA = __ldg(PG + 1);
   for (int e = lane; e < nA; e += 32) ST[e] = __ldg(a.kvals + PG[4 + nA + e]);
   __syncwarp();
   const int* aoffs = PG + 4;
@@ -734,38 +741,43 @@ __device__ __forceinline__ void group_task(const FactorArgs& a, int g, int lane,
       const int m2c = PG[p], off = PG[p + 1];
       const int reli = lane < m2c ? PG[p + 2 + lane] : 0;
       const double* Cc = stack + off;
+      int co = 0;
       for (int j = 0; j < m2c; ++j) {
         const int relj = __shfl_sync(kFull, reli, j);
-        if (lane >= j && lane < m2c) F[cb_col(relj, nr) + reli] += Cc[cb_col(j, m2c) + lane];
+        if (lane >= j && lane < m2c) F[cb32(relj, nr) + reli] += Cc[co + lane];
+        co += m2c - j - 1;
       }
       p += 2 + m2c;
       __syncwarp();
     }
     const int i = lane;
     for (int c = 0; c < w; ++c) {
-      const double d = F[cb_col(c, nr) + c];
+      const int offc = cb32(c, nr);
+      const double d = F[offc + c];
       if (i == 0) {
         a.D[f + c] = d;
         if (fabs(d) <= thresh) atomicMin(a.zp, f + c);
       }
       double l = 0.0;
       if (i > c && i < nr) {
-        l = divz(F[cb_col(c, nr) + i], d);
-        F[cb_col(c, nr) + i] = l;
+        l = divz(F[offc + i], d);
+        F[offc + i] = l;
       }
       const double dl = d * l;
+      int off2 = cb32(c + 1, nr);  // column c2's offset, advanced incrementally
       for (int c2 = c + 1; c2 < nr; ++c2) {
         const double lc2 = __shfl_sync(kFull, dl, c2);
-        if (i >= c2 && i < nr) F[cb_col(c2, nr) + i] -= l * lc2;
+        if (i >= c2 && i < nr) F[off2 + i] -= l * lc2;
+        off2 += nr - c2 - 1;
       }
       __syncwarp();
     }
     double* P = a.L + loff;
-    for (int c = 0; c < w; ++c)
-      if (lane < nr) P[c * nr + lane] = lane >= c ? F[cb_col(c, nr) + lane] : 0.0;
+    for (int c = 0, fo = 0; c < w; fo += nr - c - 1, ++c)
+      if (lane < nr) P[c * nr + lane] = lane >= c ? F[fo + lane] : 0.0;
     double* C = push >= 0 ? stack + push : a.CB + cboff;
-    for (int j = 0; j < m2; ++j)
-      if (lane >= j && lane < m2) C[cb_col(j, m2) + lane] = F[cb_col(w + j, nr) + w + lane];
+    for (int j = 0, co = 0, fo = cb32(w, nr) + w; j < m2; co += m2 - j - 1, fo += nr - w - j - 1, ++j)
+      if (lane >= j && lane < m2) C[co + lane] = F[fo + lane];
     __syncwarp();
     if (push < 0 && lane == 0) {  // the group root publishes its CB
       __threadfence();
@@ -776,15 +788,14 @@ __device__ __forceinline__ void group_task(const FactorArgs& a, int g, int lane,
 
 
 template <int NT>
-__global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 5 : 2) factor_kernel(FactorArgs a) {
+__global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 6 : 2) factor_kernel(FactorArgs a) {
   __shared__ int s_ticket;
   extern __shared__ double s_front[];
   const int tid = NT == 32 ? (threadIdx.x & 31) : threadIdx.x;
   constexpr int kFrontPk = kGrpFront * (kGrpFront + 1) / 2;              // packed lower 32 x 32
-  constexpr int kWarpSmem = kFrontPk + kGrpStack + kGrpProg / 2;          // doubles per warp
+  constexpr int kWarpSmem = kFrontPk + kGrpStack;                         // doubles per warp
   double* F = NT == 32 ? s_front + (threadIdx.x >> 5) * kWarpSmem : s_front;
   double* gST = F + kFrontPk;
-  int* gPG = reinterpret_cast<int*>(gST + kGrpStack);
   const double thresh = __ldcg(a.thresh);
   Claim<NT> cl;
   for (;;) {
@@ -796,7 +807,7 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 5 : 2) factor_
     if (a.trace && tid == 0) a.trace[2 * t] = gtimer();
     if constexpr (NT == 32) {
       if (group && a.prog) {
-        group_task(a, t, tid, thresh, F, gST, gPG);
+        group_task(a, t, tid, thresh, F, gST);
         if (a.trace && tid == 0) a.trace[2 * t + 1] = gtimer();
         continue;
       }
@@ -907,13 +918,10 @@ __device__ __forceinline__ int64_t rec64(const int* r) {
 // come from a shared-memory stack (at the factor's CB stack offsets), only
 // x (pivot rows) and the root's CV go to global memory. Same arithmetic as
 // fwd_task<32>.
-__device__ void fwd_group(const SolveArgs& a, int g, int lane, double* VS, double* ST, int* PG) {
+__device__ void fwd_group(const SolveArgs& a, int g, int lane, double* VS, double* ST) {
   const DevSymb& S = a.S;
-  const int* gp = a.prog + __ldg(a.gpo + g);
-  const int len = __ldg(gp + 3);
-  for (int k = lane; k < len; k += 32) PG[k] = __ldg(gp + k);
-  __syncwarp();
-  const int nnodes = PG[0], nA = PG[1];
+  const int* __restrict__ PG = a.prog + __ldg(a.gpo + g);  // read in place (see group_task)
+  const int nnodes = __ldg(PG), nA = __ldg(PG + 1);
   int p = 4 + 2 * nA;
   for (int v = 0; v < nnodes; ++v) {
     const int* R = PG + p;
@@ -960,13 +968,10 @@ __device__ void fwd_group(const SolveArgs& a, int g, int lane, double* VS, doubl
 
 // Backward solve of a group (reverse postorder; the root waits for its
 // parent, which lies outside the group). Same arithmetic as bwd_task<32>.
-__device__ void bwd_group(const SolveArgs& a, int g, int lane, int* PG, int* OFF) {
+__device__ void bwd_group(const SolveArgs& a, int g, int lane, int* OFF) {
   const DevSymb& S = a.S;
-  const int* gp = a.prog + __ldg(a.gpo + g);
-  const int len = __ldg(gp + 3);
-  for (int k = lane; k < len; k += 32) PG[k] = __ldg(gp + k);
-  __syncwarp();
-  const int nnodes = PG[0], nA = PG[1];
+  const int* __restrict__ PG = a.prog + __ldg(a.gpo + g);  // read in place (see group_task)
+  const int nnodes = __ldg(PG), nA = __ldg(PG + 1);
   if (lane == 0) {  // record offsets of the nodes (variable-length records)
     int p = 4 + 2 * nA;
     for (int v = 0; v < nnodes; ++v) {
@@ -1351,11 +1356,14 @@ __device__ __forceinline__ void bwd_task(const SolveArgs& a, int s, int tid) {
   }
 }
 
-// per warp: VS[32] + stack[kGrpStack] + program[kGrpProg ints] + record offsets[kGrpProg ints]
-constexpr int kSolWarp = 32 + kGrpStack + kGrpProg;  // doubles (two int arrays of kGrpProg = kGrpProg doubles)
+// per warp: VS[32] + stack[kGrpStack] + record offsets[kGrpOff ints]; a
+// group has at most kGrpProg / 14 nodes (14-int records)
+constexpr int kGrpOff = 64;
+static_assert(kGrpProg / 14 <= kGrpOff, "record offsets");
+constexpr int kSolWarp = 32 + kGrpStack + kGrpOff / 2;  // doubles
 
 template <int NT>
-__global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 6 : 4) fwd_kernel(SolveArgs a) {
+__global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 8 : 4) fwd_kernel(SolveArgs a) {
   __shared__ int s_ticket;
   extern __shared__ double s_sol[];
   const int tid = NT == 32 ? (threadIdx.x & 31) : threadIdx.x;
@@ -1365,7 +1373,7 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 6 : 4) fwd_ker
     if (t < 0) break;
     if (NT == 32 && a.prog && t < a.nleaf) {
       double* VS = s_sol + (threadIdx.x >> 5) * kSolWarp;
-      fwd_group(a, t, tid, VS, VS + 32, reinterpret_cast<int*>(VS + 32 + kGrpStack));
+      fwd_group(a, t, tid, VS, VS + 32);
       continue;
     }
     for (int k = __ldg(a.tptr + t); k < __ldg(a.tptr + t + 1); ++k) fwd_task<NT>(a, __ldg(a.tasks + k), tid);
@@ -1374,7 +1382,7 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 6 : 4) fwd_ker
 
 // tickets in reverse order (roots first); no leaf chunking
 template <int NT>
-__global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 6 : 4) bwd_kernel(SolveArgs a) {
+__global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 8 : 4) bwd_kernel(SolveArgs a) {
   __shared__ int s_ticket;
   extern __shared__ double s_sol[];
   const int tid = NT == 32 ? (threadIdx.x & 31) : threadIdx.x;
@@ -1394,8 +1402,7 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 6 : 4) bwd_ker
     if (k < a.t0) break;
     if (NT == 32 && a.prog && k < a.nleaf) {
       double* VS = s_sol + (threadIdx.x >> 5) * kSolWarp;
-      int* PG = reinterpret_cast<int*>(VS + 32 + kGrpStack);
-      bwd_group(a, k, tid, PG, PG + kGrpProg);
+      bwd_group(a, k, tid, reinterpret_cast<int*>(VS + 32 + kGrpStack));
       continue;
     }
     for (int j = __ldg(a.tptr + k + 1) - 1; j >= __ldg(a.tptr + k); --j) bwd_task<NT>(a, __ldg(a.tasks + j), tid);
@@ -1515,7 +1522,7 @@ int persistent_grid(K fn, int threads, int ntasks, int smem = 0) {
 unsigned long long* g_task_trace = nullptr;  // NCL_TASK_TRACE debugging
 constexpr int kSolSmem = 4 * kSolWarp * sizeof(double);
 static int g_fg = 0, g_fg2 = 0, g_sf = 0, g_sf2 = 0, g_sb = 0, g_sb2 = 0;
-constexpr int kFacSmem1 = 4 * (kGrpFront * (kGrpFront + 1) / 2 + kGrpStack + kGrpProg / 2) * sizeof(double);
+constexpr int kFacSmem1 = 4 * (kGrpFront * (kGrpFront + 1) / 2 + kGrpStack) * sizeof(double);
 constexpr int kFacSmem2 = kCtaFront * (kCtaFront + 1) / 2 * sizeof(double);  // packed lower front
 static void init_grids() {
   if (g_fg) return;
