@@ -631,8 +631,14 @@ __device__ __forceinline__ int cb32(int j, int m) { return j * m - ((j * (j + 1)
 // read contiguously. Inside a subtree group the children were produced by
 // this very warp, so there is no flag wait, and only the group's root
 // publishes (fence + release). Arithmetic is identical to factor_task_smem<32>.
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 __device__ __forceinline__ void small_task(const FactorArgs& a, int s, int lane, double thresh, double* F,
-                                           bool wait_children, bool publish) {
+                                           bool wait_children, bool publish, double* stg) {
   const DevSymb& S = a.S;
   const SnMeta m = S.meta[s];
   const int nr = m.nr, w = m.w, f = m.f, m2 = nr - w;
@@ -663,10 +669,19 @@ __device__ __forceinline__ void small_task(const FactorArgs& a, int s, int lane,
       const long long rlk = __shfl_sync(kFull, static_cast<long long>(crel), k);
       const int reli = lane < m2c ? __ldg(S.relp + rlk + lane) : 0;
       const double* Cc = a.CB + cbk;
+      const int ne = m2c * (m2c + 1) / 2;
+      if (ne <= kGrpStack) {
+        // stage the child's CB in shared memory with async copies (all in
+        // flight at once) instead of one dependent global read per column
+        for (int e = lane; e < ne; e += 32) cp_async8(stg + e, Cc + e);
+        cp_async_wait_all();
+        __syncwarp();
+        Cc = stg;
+      }
       int co = 0;
       for (int j = 0; j < m2c; ++j) {
         const int relj = __shfl_sync(kFull, reli, j);
-        if (lane >= j && lane < m2c) F[cb32(relj, nr) + reli] += __ldcg(Cc + co + lane);
+        if (lane >= j && lane < m2c) F[cb32(relj, nr) + reli] += Cc[co + lane];
         co += m2c - j - 1;
       }
       __syncwarp();
@@ -702,6 +717,120 @@ __device__ __forceinline__ void small_task(const FactorArgs& a, int s, int lane,
     if (lane >= j && lane < m2) C[co + lane] = F[fo + lane];
   __syncwarp();
   if (publish && lane == 0) {
+    __threadfence();
+    st_release(a.flags + s, a.epoch);
+  }
+}
+
+// Mid-size front (32 < nr <= kMidFront) by one warp in its shared-memory
+// region (packed front over the warp's front + stack space): lane l owns rows
+// l and l + 32. Children's contribution blocks are read flat (coalesced,
+// four loads in flight per lane) with their relative row maps in registers;
+// per entry the order is the same as small_task's: A value, then children in
+// ascending order, then the column updates in pivot order.
+constexpr int kMidFront = 45;  // 45 * 46 / 2 = 1035 <= kGrpFront * (kGrpFront + 1) / 2 + kGrpStack
+__device__ __forceinline__ int rel_at(int x, int r0, int r1) {
+  const int a = __shfl_sync(kFull, r0, x & 31), b = __shfl_sync(kFull, r1, x & 31);
+  return x < 32 ? a : b;
+}
+__device__ __forceinline__ void mid_task(const FactorArgs& a, int s, int lane, double thresh, double* F) {
+  const DevSymb& S = a.S;
+  const SnMeta m = S.meta[s];
+  const int nr = m.nr, w = m.w, f = m.f, m2 = nr - w;
+  for (int q = m.c0 + lane; q < m.c1; q += 32) wait_flag(a.flags + __ldg(S.child + q), a.epoch);
+  for (int k = lane; k < nr * (nr + 1) / 2; k += 32) F[k] = 0.0;
+  __syncwarp();
+  for (int e0 = 0; e0 < m.na; e0 += 128) {
+    int off[4];
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + lane + 32 * u;
+      off[u] = e < m.na ? __ldg(S.aoff + m.a0 + e) : 0;
+      v[u] = e < m.na ? __ldg(a.kvals + __ldg(S.asrc + m.a0 + e)) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (e0 + lane + 32 * u < m.na) F[cb32(off[u] / nr, nr) + off[u] % nr] = v[u];
+  }
+  __syncwarp();
+  for (int q = m.c0; q < m.c1; ++q) {
+    const SnMeta cm = S.meta[__ldg(S.child + q)];
+    const int m2c = cm.nr - cm.w;
+    const int64_t rl = cm.rptr + cm.w;
+    const int r0 = lane < m2c ? __ldg(S.relp + rl + lane) : 0;
+    const int r1 = lane + 32 < m2c ? __ldg(S.relp + rl + lane + 32) : 0;
+    const double* Cc = a.CB + cm.cboff;
+    const int ne = m2c * (m2c + 1) / 2;
+    int j = 0, i = lane;  // packed position lane -> (column j, row i)
+    while (i >= m2c && j < m2c) {
+      const int ex = i - m2c;
+      ++j;
+      i = j + ex;
+    }
+    for (int e0 = 0; e0 < ne; e0 += 128) {
+      double v[4];
+      int jj[4], ii[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + lane + 32 * u;
+        v[u] = e < ne ? __ldcg(Cc + e) : 0.0;
+        jj[u] = j;
+        ii[u] = i;
+        i += 32;
+        while (i >= m2c && j < m2c) {
+          const int ex = i - m2c;
+          ++j;
+          i = j + ex;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int rj = rel_at(min(jj[u], 63), r0, r1), ri = rel_at(min(ii[u], 63), r0, r1);
+        if (e0 + lane + 32 * u < ne) F[cb32(rj, nr) + ri] += v[u];
+      }
+    }
+    __syncwarp();
+  }
+  const int i0 = lane, i1 = lane + 32;
+  for (int c = 0; c < w; ++c) {
+    const int offc = cb32(c, nr);
+    const double d = F[offc + c];
+    if (lane == 0) {
+      a.D[f + c] = d;
+      if (fabs(d) <= thresh) atomicMin(a.zp, f + c);
+    }
+    double y0 = 0.0, y1 = 0.0;
+    if (i0 > c && i0 < nr) {
+      y0 = divz(F[offc + i0], d);
+      F[offc + i0] = y0;
+    }
+    if (i1 > c && i1 < nr) {
+      y1 = divz(F[offc + i1], d);
+      F[offc + i1] = y1;
+    }
+    const double dl0 = d * y0, dl1 = d * y1;
+    int off2 = cb32(c + 1, nr);
+    for (int c2 = c + 1; c2 < nr; ++c2) {
+      const double lc2 = c2 < 32 ? __shfl_sync(kFull, dl0, c2) : __shfl_sync(kFull, dl1, c2 - 32);
+      if (i0 >= c2 && i0 < nr) F[off2 + i0] -= y0 * lc2;
+      if (i1 >= c2 && i1 < nr) F[off2 + i1] -= y1 * lc2;
+      off2 += nr - c2 - 1;
+    }
+    __syncwarp();
+  }
+  double* P = a.L + m.loff;
+  double* C = a.CB + m.cboff;
+  for (int c = 0, fo = 0; c < w; fo += nr - c - 1, ++c) {
+    if (i0 < nr) P[c * nr + i0] = i0 >= c ? F[fo + i0] : 0.0;
+    if (i1 < nr) P[c * nr + i1] = i1 >= c ? F[fo + i1] : 0.0;
+  }
+  for (int jc = 0, co = 0, fo = cb32(w, nr) + w; jc < m2; co += m2 - jc - 1, fo += nr - w - jc - 1, ++jc) {
+    if (i0 >= jc && i0 < m2) C[co + i0] = F[fo + i0];
+    if (i1 >= jc && i1 < m2) C[co + i1] = F[fo + i1];
+  }
+  __syncwarp();
+  if (lane == 0) {
     __threadfence();
     st_release(a.flags + s, a.epoch);
   }
@@ -817,7 +946,8 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 6 : 2) factor_
       const int s = __ldg(a.tasks + k);
       const int nr = static_cast<int>(__ldg(a.S.sn_rptr + s + 1) - __ldg(a.S.sn_rptr + s));
       if (a.skip_big && __ldg(a.S.big + s)) continue;  // runs on the large-front path
-      if (NT == 32 && nr <= kWarpFront) small_task(a, s, tid, thresh, F, !group, !group || k == k1 - 1);
+      if (NT == 32 && nr <= kWarpFront) small_task(a, s, tid, thresh, F, !group, !group || k == k1 - 1, F + kFrontPk);
+      else if (NT == 32 && !group && nr <= kMidFront) mid_task(a, s, tid, thresh, F);
       else if (NT != 32 && nr <= kCtaFront) factor_task_smem<NT>(a, s, tid, thresh, F);
       else factor_task<NT>(a, s, tid, thresh, !group, !group || k == k1 - 1);
     }

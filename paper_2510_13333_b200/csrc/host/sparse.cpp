@@ -535,7 +535,8 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
   }
   // phase split: the narrow top of the tree (at most kTopTasks supernodes)
   // runs with a whole CTA per supernode, everything below with a warp each.
-  constexpr int kTopTasks = 8192;
+  static const char* top_env = std::getenv("NCL_TOP_TASKS");  // tuning experiments only
+  const int kTopTasks = top_env ? std::atoi(top_env) : 8192;
   Z.nsplit = nsn;
   for (int h = Z.max_height; h >= 0; --h) {
     if (nsn - hc[h] > kTopTasks) break;

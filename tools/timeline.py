@@ -68,3 +68,31 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def singles_by_size(path, grid="activsg500", K=256):
+    """Singles (warp tasks outside groups): count and mean duration by nr range."""
+    raw = open(path, "rb").read()
+    ntask, nleaf, split, _ = np.frombuffer(raw[:16], np.int32)
+    o = 16
+    tr = np.frombuffer(raw[o:o + 16 * ntask], np.uint64).reshape(ntask, 2).astype(np.int64)
+    o += 16 * ntask
+    tptr = np.frombuffer(raw[o:o + 4 * (ntask + 1)], np.int32)
+    o += 4 * (ntask + 1)
+    nodes = np.frombuffer(raw[o:], np.int32)
+    from paper_2510_13333_b200 import sparse as ps
+    from paper_2510_13333_b200.kkt import Kkt
+    from paper_2510_13333_b200.scopf import Scopf
+    S = ps.analyze(Kkt(Scopf(grid, K, seed=2510).build_model()).matrix)
+    d = ps.supernodes(S)
+    nr = np.diff(d["rptr"])
+    w = np.diff(d["first"])
+    du = (tr[:, 1] - tr[:, 0]) / 1e3
+    idx = np.arange(nleaf, split)
+    nn = np.array([nr[nodes[tptr[t]]] for t in idx])
+    ww = np.array([w[nodes[tptr[t]]] for t in idx])
+    for lo, hi in ((0, 16), (16, 32), (32, 48), (48, 64), (64, 100), (100, 200)):
+        m = (nn > lo) & (nn <= hi)
+        if m.any():
+            print(f"  nr in ({lo},{hi}]: {m.sum():6d} singles, mean w {ww[m].mean():5.1f}, mean dur {du[idx[m]].mean():6.2f} us, "
+                  f"sum {du[idx[m]].sum() / 1e3:8.1f} ms-warp")
