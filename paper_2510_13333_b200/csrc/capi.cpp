@@ -496,9 +496,11 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
     const int h = Z.height[node_of(i)];
     int e = i;
     std::vector<BigDesc> big;
+    int lvl_max_nr = 0;
     while (e < ntask && Z.height[node_of(e)] == h) {
       const int s = node_of(e);
       const int nr = static_cast<int>(Z.sn_rptr[s + 1] - Z.sn_rptr[s]);
+      if (!Z.big[s]) lvl_max_nr = std::max(lvl_max_nr, nr);
       if (Z.big[s]) {
         BigDesc b{};
         b.s = s;
@@ -524,13 +526,18 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
     // merge levels without large fronts into one segment (one persistent
     // launch, flags order them); a segment closes at a level holding large
     // fronts, which run (as one batch) after that level's small fronts
-    if (!t.lvl_begin.empty() && t.big.back().empty()) {
+    // Levels whose fronts all fit kCtaFrontS rows form their own segments
+    // (small CTAs, several per SM).
+    const char small = lvl_max_nr <= kCtaFrontS;
+    if (small) t.any_small = true;
+    if (!t.lvl_begin.empty() && t.big.back().empty() && t.small.back() == small) {
       t.lvl_end.back() = e;
       t.big.back() = std::move(big);
     } else {
       t.lvl_begin.push_back(i);
       t.lvl_end.push_back(e);
       t.big.push_back(std::move(big));
+      t.small.push_back(small);
     }
     i = e;
   }

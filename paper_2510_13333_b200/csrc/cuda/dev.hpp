@@ -30,11 +30,13 @@ struct BigDesc {
   int64_t g0, g1;             // gather-map entry range
   int64_t foff, woff;         // offsets of its scratch front (nr^2) and W (nr * pw)
 };
+constexpr int kCtaFrontS = 80;  // front cap of the small-CTA segments (packed lower: 25.9 KB)
 struct TopSched {
   std::vector<int> lvl_begin, lvl_end;   // segments of the CTA part (task index ranges)
   std::vector<std::vector<BigDesc>> big;  // per segment: its large fronts (run as one batch)
   std::vector<const BigDesc*> big_dev;    // per segment: device copy of `big`
-  bool any_big = false;
+  std::vector<char> small;                // per segment: every front <= kCtaFrontS rows (128-thread CTAs)
+  bool any_big = false, any_small = false;
   int max_nr = 0;
   int64_t scratch_f = 0, scratch_w = 0;   // largest per-segment scratch (doubles)
 };

@@ -334,12 +334,13 @@ template <int NT>
 __device__ __forceinline__ void gather4(const DevSymb& S, const double* __restrict__ kvals,
                                         const double* __restrict__ CB, int64_t g0, int64_t g1, int tid, double* F,
                                         int nr) {
-  for (int64_t kb = g0 + tid; kb < g1; kb += 4 * NT) {
-    int64_t q[4], q1[4];
-    double acc[4];
+  constexpr int kU = 8;  // front entries in flight per thread
+  for (int64_t kb = g0 + tid; kb < g1; kb += kU * NT) {
+    int64_t q[kU], q1[kU];
+    double acc[kU];
     int cmax = 0;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kU; ++u) {
       const int64_t k = kb + u * NT;
       q[u] = k < g1 ? __ldg(S.gsp + k) : 0;
       q1[u] = k < g1 ? __ldg(S.gsp + k + 1) : 0;
@@ -348,14 +349,14 @@ __device__ __forceinline__ void gather4(const DevSymb& S, const double* __restri
     }
     for (int c = 0; c < cmax; ++c) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < kU; ++u)
         if (q[u] + c < q1[u]) {
           const int64_t src = __ldg(S.gsrc + q[u] + c);
           acc[u] += src < 0 ? __ldg(kvals + ~src) : __ldcg(CB + src);
         }
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kU; ++u) {
       const int64_t k = kb + u * NT;
       if (k < g1) {
         const int d = __ldg(S.gdst + k);  // full-layout position rj * nr + ri -> packed lower
@@ -490,8 +491,9 @@ __device__ __forceinline__ void cta_dense(double* F, int nr, int w, int f, doubl
         // tile rows ti dealt to the warps in snake order (row ti holds ti + 1
         // tiles); per row the A fragments stay in registers and four tiles
         // are in flight at a time (loads, 8 DMMAs, then the read-modify-writes)
-        for (int r = 0; r * 8 < T; ++r) {
-          const int ti = (r & 1) ? r * 8 + 7 - warp : r * 8 + warp;
+        constexpr int nw = NT / 32;
+        for (int r = 0; r * nw < T; ++r) {
+          const int ti = (r & 1) ? r * nw + nw - 1 - warp : r * nw + warp;
           if (ti >= T) continue;
           const int i = c1 + ti * 8 + g;
           double a0 = 0.0, a1 = 0.0;
@@ -917,7 +919,7 @@ __device__ __forceinline__ void group_task(const FactorArgs& a, int g, int lane,
 
 
 template <int NT>
-__global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 6 : 2) factor_kernel(FactorArgs a) {
+__global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 6 : NT == 128 ? 6 : 2) factor_kernel(FactorArgs a) {
   __shared__ int s_ticket;
   extern __shared__ double s_front[];
   const int tid = NT == 32 ? (threadIdx.x & 31) : threadIdx.x;
@@ -948,7 +950,7 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 6 : 2) factor_
       if (a.skip_big && __ldg(a.S.big + s)) continue;  // runs on the large-front path
       if (NT == 32 && nr <= kWarpFront) small_task(a, s, tid, thresh, F, !group, !group || k == k1 - 1, F + kFrontPk);
       else if (NT == 32 && !group && nr <= kMidFront) mid_task(a, s, tid, thresh, F);
-      else if (NT != 32 && nr <= kCtaFront) factor_task_smem<NT>(a, s, tid, thresh, F);
+      else if (NT != 32 && nr <= (NT == 128 ? kCtaFrontS : kCtaFront)) factor_task_smem<NT>(a, s, tid, thresh, F);
       else factor_task<NT>(a, s, tid, thresh, !group, !group || k == k1 - 1);
     }
     if (a.trace && tid == 0) a.trace[2 * t + 1] = gtimer();
@@ -1651,15 +1653,18 @@ int persistent_grid(K fn, int threads, int ntasks, int smem = 0) {
 
 unsigned long long* g_task_trace = nullptr;  // NCL_TASK_TRACE debugging
 constexpr int kSolSmem = 4 * kSolWarp * sizeof(double);
-static int g_fg = 0, g_fg2 = 0, g_sf = 0, g_sf2 = 0, g_sb = 0, g_sb2 = 0;
+static int g_fg = 0, g_fg2 = 0, g_fg3 = 0, g_sf = 0, g_sf2 = 0, g_sb = 0, g_sb2 = 0;
 constexpr int kFacSmem1 = 4 * (kGrpFront * (kGrpFront + 1) / 2 + kGrpStack) * sizeof(double);
 constexpr int kFacSmem2 = kCtaFront * (kCtaFront + 1) / 2 * sizeof(double);  // packed lower front
+constexpr int kFacSmem3 = kCtaFrontS * (kCtaFrontS + 1) / 2 * sizeof(double);  // small-CTA segments
 static void init_grids() {
   if (g_fg) return;
   cudaFuncSetAttribute(factor_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFacSmem1);
   cudaFuncSetAttribute(factor_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFacSmem2);
   g_fg = persistent_grid(factor_kernel<32>, 128, 1 << 30, kFacSmem1);
   g_fg2 = persistent_grid(factor_kernel<256>, 256, 1 << 30, kFacSmem2);
+  cudaFuncSetAttribute(factor_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFacSmem3);
+  g_fg3 = persistent_grid(factor_kernel<128>, 128, 1 << 30, kFacSmem3);
   cudaFuncSetAttribute(fwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSolSmem);
   cudaFuncSetAttribute(bwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSolSmem);
   g_sf = persistent_grid(fwd_kernel<32>, 128, 1 << 30, kSolSmem);
@@ -1698,9 +1703,10 @@ void dev_factor_list(const DevSymb& S, DevFactor& F, const double* kvals, const 
     COUNT(1);
     factor_kernel<32><<<g_fg, 128, kFacSmem1, st>>>(a);
   }
-  if (T.top && T.top->any_big) {
-    // level by level: small fronts of the level in one persistent launch,
-    // then its large fronts on the blocked DMMA path
+  if (T.top && (T.top->any_big || T.top->any_small)) {
+    // segment by segment (merged levels): the segment's fronts in one
+    // persistent launch (128-thread CTAs when they all fit kCtaFrontS rows),
+    // then its large fronts on the multi-CTA path
     const TopSched& ts = *T.top;
     a.skip_big = 1;
     a.nleaf = 0;
@@ -1713,7 +1719,8 @@ void dev_factor_list(const DevSymb& S, DevFactor& F, const double* kvals, const 
         a.t0 = b;
         a.t1 = e;
         COUNT(1);
-        factor_kernel<256><<<std::min(g_fg2, e - b), 256, kFacSmem2, st>>>(a);
+        if (ts.small[L]) factor_kernel<128><<<std::min(g_fg3, e - b), 128, kFacSmem3, st>>>(a);
+        else factor_kernel<256><<<std::min(g_fg2, e - b), 256, kFacSmem2, st>>>(a);
       }
       if (!ts.big[L].empty()) dev_factor_big_batch(S, F, kvals, ts.big[L], ts.big_dev[L], st);
     }
