@@ -434,15 +434,18 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
     }
     L.nodes.insert(L.nodes.end(), post.begin(), post.end());
     L.tptr.push_back(static_cast<int>(L.nodes.size()));
-    // program: [nnodes, nA, 0, len] [aoff x nA] [asrc x nA] then per node
+    // program: [nnodes, nA, tab, len] [aoff x nA] [asrc x nA] then per node
     // [s, f, w, nr, nch, push_off(-1 = root), a_first, a_cnt, loff lo/hi, cboff lo/hi, rptr lo/hi] and per child
-    // [m2c, stack_off, rel x m2c]; stack offsets from a postorder simulation
+    // [m2c, stack_off, rel x m2c], then the record offsets [tab .. tab + nnodes);
+    // stack offsets from a postorder simulation
     const size_t base = L.prog.size();
     const int nA = static_cast<int>(na[r]);
     L.prog.insert(L.prog.end(), {static_cast<int>(post.size()), nA, 0, 0});
     const size_t aoff0 = L.prog.size();
     L.prog.resize(aoff0 + 2 * static_cast<size_t>(nA));
     int top = 0, afirst = 0;
+    std::vector<int> rec_off;  // node record offsets (table appended after the records)
+    rec_off.reserve(post.size());
     for (int s : post) {
       const int acnt = static_cast<int>(Z.a_ptr[s + 1] - Z.a_ptr[s]);
       for (int e = 0; e < acnt; ++e) {
@@ -454,6 +457,7 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
       for (int q = Z.cptr[s]; q < Z.cptr[s + 1]; ++q) pop += static_cast<int>(cbof(Z.child[q]));
       const int push = s == r ? -1 : top - pop;
       const int64_t lo = Z.sn_loff[s], cbo = Z.cb_off[s], rp = Z.sn_rptr[s];
+      rec_off.push_back(static_cast<int>(L.prog.size() - base));
       L.prog.insert(L.prog.end(), {s, Z.sn_first[s], wof(s), nrof(s), Z.cptr[s + 1] - Z.cptr[s], push, afirst, acnt,
                                    static_cast<int>(lo & 0xffffffff), static_cast<int>(lo >> 32),
                                    static_cast<int>(cbo & 0xffffffff), static_cast<int>(cbo >> 32),
@@ -472,6 +476,8 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
       }
       afirst += acnt;
     }
+    L.prog[base + 2] = static_cast<int>(L.prog.size() - base);  // [2]: offset of the record-offset table
+    L.prog.insert(L.prog.end(), rec_off.begin(), rec_off.end());
     L.prog[base + 3] = static_cast<int>(L.prog.size() - base);
     L.gpo.push_back(static_cast<int64_t>(L.prog.size()));
   }

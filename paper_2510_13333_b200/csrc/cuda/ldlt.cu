@@ -18,6 +18,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
+#include <vector>
 #include <cstdlib>
 
 #include "dev.hpp"
@@ -1040,6 +1042,7 @@ struct SolveArgs {
   const int* prog;
   const int64_t* gpo;
   int nleaf;
+  unsigned long long* trace;  // optional (NCL_SOLVE_TRACE): globaltimer start/end per task
 };
 
 __device__ __forceinline__ int64_t rec64(const int* r) {
@@ -1101,20 +1104,11 @@ __device__ void fwd_group(const SolveArgs& a, int g, int lane, double* VS, doubl
 
 // Backward solve of a group (reverse postorder; the root waits for its
 // parent, which lies outside the group). Same arithmetic as bwd_task<32>.
-__device__ void bwd_group(const SolveArgs& a, int g, int lane, int* OFF) {
+__device__ void bwd_group(const SolveArgs& a, int g, int lane) {
   const DevSymb& S = a.S;
   const int* __restrict__ PG = a.prog + __ldg(a.gpo + g);  // read in place (see group_task)
-  const int nnodes = __ldg(PG), nA = __ldg(PG + 1);
-  if (lane == 0) {  // record offsets of the nodes (variable-length records)
-    int p = 4 + 2 * nA;
-    for (int v = 0; v < nnodes; ++v) {
-      OFF[v] = p;
-      const int nch = PG[p + 4];
-      p += 14;
-      for (int q = 0; q < nch; ++q) p += 2 + PG[p];
-    }
-  }
-  __syncwarp();
+  const int nnodes = __ldg(PG);
+  const int* OFF = PG + __ldg(PG + 2);  // record offsets of the nodes (table after the records)
   for (int v = nnodes - 1; v >= 0; --v) {
     const int* R = PG + OFF[v];
     const int s = R[0], f = R[1], w = R[2], nr = R[3];
@@ -1232,13 +1226,59 @@ __device__ __forceinline__ void fwd_task(const SolveArgs& a, int s, int tid) {
   double* xs = a.xp + f;
   const int64_t v0 = NT == 32 ? 0 : __ldg(S.cv_ptr + s), v1 = NT == 32 ? 0 : __ldg(S.cv_ptr + s + 1);
   if (v1 > v0) {
-    // gather per row: b (pivot rows) then the children's CV entries in
-    // child order — the sequential extend-add's summation order
-    for (int k = tid; k < nr; k += NT) {
-      double acc = k < w ? __ldcg(a.b + __ldg(S.perm + f + k)) : 0.0;
-      for (int64_t q = __ldg(S.cvsp + v0 + k); q < __ldg(S.cvsp + v0 + k + 1); ++q) acc += __ldcg(a.CV + __ldg(S.cvsrc + q));
-      if (k < w) xs[k] = acc;
-      else cv[k] = acc;
+    if (NT != 32 && __ldg(S.cvsp + v1) - __ldg(S.cvsp + v0) > 8 * static_cast<int64_t>(nr)) {
+      // many children (the separator roots): a warp per row, lanes over its
+      // sources, fixed xor-butterfly combine, then b (deterministic)
+      // (four rows per warp interleaved: their loads are in flight together)
+      const int lane = tid & 31, warp = tid >> 5;
+      for (int k0 = 4 * warp; k0 < nr; k0 += 4 * (NT / 32)) {
+        int64_t qa[4], qb[4];
+        double acc[4];
+        int64_t len = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = k0 + u;
+          qa[u] = k < nr ? __ldg(S.cvsp + v0 + k) : 0;
+          qb[u] = k < nr ? __ldg(S.cvsp + v0 + k + 1) : 0;
+          acc[u] = 0.0;
+          len = max(len, qb[u] - qa[u]);
+        }
+        for (int64_t o = lane; o < len; o += 64) {  // two sources per row per lane in flight
+          int64_t src[8];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            src[u] = qa[u] + o < qb[u] ? __ldg(S.cvsrc + qa[u] + o) : -1;
+            src[u + 4] = qa[u] + o + 32 < qb[u] ? __ldg(S.cvsrc + qa[u] + o + 32) : -1;
+          }
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = src[u] >= 0 ? __ldcg(a.CV + src[u]) : 0.0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (src[u] >= 0) acc[u] += v[u];
+            if (src[u + 4] >= 0) acc[u] += v[u + 4];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          for (int o = 16; o > 0; o >>= 1) acc[u] += __shfl_xor_sync(kFull, acc[u], o);
+          const int k = k0 + u;
+          if (lane == 0 && k < nr) {
+            if (k < w) xs[k] = __ldcg(a.b + __ldg(S.perm + f + k)) + acc[u];
+            else cv[k] = acc[u];
+          }
+        }
+      }
+    } else {
+      // gather per row: b (pivot rows) then the children's CV entries in
+      // child order — the sequential extend-add's summation order
+      for (int k = tid; k < nr; k += NT) {
+        double acc = k < w ? __ldcg(a.b + __ldg(S.perm + f + k)) : 0.0;
+        for (int64_t q = __ldg(S.cvsp + v0 + k); q < __ldg(S.cvsp + v0 + k + 1); ++q)
+          acc += __ldcg(a.CV + __ldg(S.cvsrc + q));
+        if (k < w) xs[k] = acc;
+        else cv[k] = acc;
+      }
     }
     team_sync<NT>();
   } else {
@@ -1285,13 +1325,13 @@ __device__ __forceinline__ void fwd_task(const SolveArgs& a, int s, int tid) {
       if (tid < 32) {
         const int i = c0 + lane;
         double y = i < c1 ? xs[i] : 0.0;
-        for (int c = c0; c < c1; c += 4) {
-          double pv[4];
+        for (int c = c0; c < c1; c += 8) {
+          double pv[8];
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
+          for (int u = 0; u < 8; ++u)
             pv[u] = (c + u < c1 && i > c + u && i < c1) ? __ldg(P + static_cast<int64_t>(c + u) * nr + i) : 0.0;
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < 8; ++u) {
             if (c + u < c1) {
               const double xc = __shfl_sync(kFull, y, c + u - c0);
               if (i > c + u && i < c1) y -= pv[u] * xc;
@@ -1446,15 +1486,15 @@ __device__ __forceinline__ void bwd_task(const SolveArgs& a, int s, int tid) {
         const bool in = c2 < c1;
         double Tl = in ? T[c2] : 0.0, xl = in ? xs[c2] : 0.0;
         const double dl = in ? __ldg(a.D + f + c2) : 1.0;
-        for (int cb = c1 - 1; cb >= c0; cb -= 4) {
-          double pu[4];
+        for (int cb = c1 - 1; cb >= c0; cb -= 8) {
+          double pu[8];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < 8; ++u) {
             const int c = cb - u;
             pu[u] = (c >= c0 && c2 < c) ? __ldg(P + static_cast<int64_t>(c2) * nr + c) : 0.0;
           }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < 8; ++u) {
             const int c = cb - u;
             if (c >= c0) {
               double v = 0.0;
@@ -1489,11 +1529,8 @@ __device__ __forceinline__ void bwd_task(const SolveArgs& a, int s, int tid) {
   }
 }
 
-// per warp: VS[32] + stack[kGrpStack] + record offsets[kGrpOff ints]; a
-// group has at most kGrpProg / 14 nodes (14-int records)
-constexpr int kGrpOff = 64;
-static_assert(kGrpProg / 14 <= kGrpOff, "record offsets");
-constexpr int kSolWarp = 32 + kGrpStack + kGrpOff / 2;  // doubles
+// per warp: VS[32] + stack[kGrpStack] (forward groups)
+constexpr int kSolWarp = 32 + kGrpStack;  // doubles
 
 template <int NT>
 __global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 8 : 4) fwd_kernel(SolveArgs a) {
@@ -1504,12 +1541,14 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 8 : 4) fwd_ker
   for (;;) {
     const int t = cl.next(a.ticket, a.t0, a.t1, a.nleaf, tid, &s_ticket);
     if (t < 0) break;
+    if (a.trace && tid == 0) a.trace[2 * t] = gtimer();
     if (NT == 32 && a.prog && t < a.nleaf) {
       double* VS = s_sol + (threadIdx.x >> 5) * kSolWarp;
       fwd_group(a, t, tid, VS, VS + 32);
-      continue;
+    } else {
+      for (int k = __ldg(a.tptr + t); k < __ldg(a.tptr + t + 1); ++k) fwd_task<NT>(a, __ldg(a.tasks + k), tid);
     }
-    for (int k = __ldg(a.tptr + t); k < __ldg(a.tptr + t + 1); ++k) fwd_task<NT>(a, __ldg(a.tasks + k), tid);
+    if (a.trace && tid == 0) a.trace[2 * t + 1] = gtimer();
   }
 }
 
@@ -1533,12 +1572,14 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 8 : 4) bwd_ker
     }
     const int k = a.t1 - 1 - t;
     if (k < a.t0) break;
+    if (a.trace && tid == 0) a.trace[2 * k] = gtimer();
     if (NT == 32 && a.prog && k < a.nleaf) {
       double* VS = s_sol + (threadIdx.x >> 5) * kSolWarp;
-      bwd_group(a, k, tid, reinterpret_cast<int*>(VS + 32 + kGrpStack));
-      continue;
+      bwd_group(a, k, tid);
+    } else {
+      for (int j = __ldg(a.tptr + k + 1) - 1; j >= __ldg(a.tptr + k); --j) bwd_task<NT>(a, __ldg(a.tasks + j), tid);
     }
-    for (int j = __ldg(a.tptr + k + 1) - 1; j >= __ldg(a.tptr + k); --j) bwd_task<NT>(a, __ldg(a.tasks + j), tid);
+    if (a.trace && tid == 0) a.trace[2 * k + 1] = gtimer();
   }
 }
 
@@ -1653,6 +1694,7 @@ int persistent_grid(K fn, int threads, int ntasks, int smem = 0) {
 }
 
 unsigned long long* g_task_trace = nullptr;  // NCL_TASK_TRACE debugging
+static unsigned long long* g_solve_trace = nullptr;  // NCL_SOLVE_TRACE debugging
 constexpr int kSolSmem = 4 * kSolWarp * sizeof(double);
 static int g_fg = 0, g_fg2 = 0, g_fg3 = 0, g_sf = 0, g_sf2 = 0, g_sb = 0, g_sb2 = 0;
 constexpr int kFacSmem1 = 4 * (kGrpFront * (kGrpFront + 1) / 2 + kGrpStack) * sizeof(double);
@@ -1760,7 +1802,7 @@ void dev_solve_fwd_list(const DevSymb& S, DevFactor& F, const double* b, const D
                         cudaStream_t st) {
   if (T.n == 0) return;
   SolveArgs fa{S, F.L, F.D, F.CV, F.xp, b, nullptr, S.flags + S.nsn, S.tickets + 2 * slot, S.epoch, 0, T.split,
-               T.ids, T.tptr, T.prog, T.gpo, T.nleaf};
+               T.ids, T.tptr, T.prog, T.gpo, T.nleaf, g_solve_trace};
   if (T.split > 0) COUNT(1), fwd_kernel<32><<<g_sf, 128, kSolSmem, st>>>(fa);
   if (T.split < T.n) {
     fa.ticket = S.tickets + 2 * slot + 1;
@@ -1775,7 +1817,7 @@ void dev_solve_fwd_list(const DevSymb& S, DevFactor& F, const double* b, const D
 void dev_solve_bwd_list(const DevSymb& S, DevFactor& F, double* x, const DevTasks& T, int slot, cudaStream_t st) {
   if (T.n == 0) return;
   SolveArgs ba{S, F.L, F.D, F.CV, F.xp, nullptr, x, S.flags + 2 * S.nsn, S.tickets + 2 * slot, S.epoch, T.split,
-               T.n, T.ids, T.tptr, T.prog, T.gpo, T.nleaf};
+               T.n, T.ids, T.tptr, T.prog, T.gpo, T.nleaf, g_solve_trace ? g_solve_trace + 2 * T.n : nullptr};
   if (T.split < T.n) COUNT(1), bwd_kernel<256><<<std::min(g_sb2, T.n - T.split), 256, 0, st>>>(ba);
   if (T.split > 0) {
     ba.ticket = S.tickets + 2 * slot + 1;
@@ -1788,9 +1830,31 @@ void dev_solve_bwd_list(const DevSymb& S, DevFactor& F, double* x, const DevTask
 
 void dev_solve(const DevSymb& S, DevFactor& F, const double* b, double* x, cudaStream_t st) {
   if (S.n == 0) return;
+  // NCL_SOLVE_TRACE=<file>: per-task globaltimer start/end of the 3rd solve
+  // (forward then backward, 4 x tasks uint64; debug timeline)
+  static const char* trace_path = std::getenv("NCL_SOLVE_TRACE");
+  static int traced = 0;
+  const bool tr = trace_path && traced++ == 2;
+  if (tr) {
+    cudaMalloc(&g_solve_trace, 4 * sizeof(unsigned long long) * S.tasks.n);
+    cudaMemsetAsync(g_solve_trace, 0, 4 * sizeof(unsigned long long) * S.tasks.n, st);
+  }
   dev_solve_begin(S, st);
   dev_solve_fwd_list(S, F, b, S.tasks, 0, st);
   dev_solve_bwd_list(S, F, x, S.tasks, 2, st);
+  if (tr) {
+    std::vector<unsigned long long> h(4 * static_cast<size_t>(S.tasks.n));
+    cudaMemcpyAsync(h.data(), g_solve_trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    cudaFree(g_solve_trace);
+    g_solve_trace = nullptr;
+    if (FILE* fp = std::fopen(trace_path, "wb")) {
+      const int hdr[4] = {S.tasks.n, S.tasks.nleaf, S.tasks.split, 0};
+      std::fwrite(hdr, sizeof(int), 4, fp);
+      std::fwrite(h.data(), sizeof(unsigned long long), h.size(), fp);
+      std::fclose(fp);
+    }
+  }
 }
 
 void dev_spmv(const DevPattern& P, const double* kvals, const double* x, double* y, cudaStream_t st) {

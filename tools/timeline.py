@@ -96,3 +96,33 @@ def singles_by_size(path, grid="activsg500", K=256):
         if m.any():
             print(f"  nr in ({lo},{hi}]: {m.sum():6d} singles, mean w {ww[m].mean():5.1f}, mean dur {du[idx[m]].mean():6.2f} us, "
                   f"sum {du[idx[m]].sum() / 1e3:8.1f} ms-warp")
+
+
+def solve_timeline(solve_path, factor_path, grid="activsg500", K=256):
+    """Forward/backward solve phases from NCL_SOLVE_TRACE (task layout from the factor trace)."""
+    raw = open(factor_path, "rb").read()
+    ntask, nleaf, split, _ = np.frombuffer(raw[:16], np.int32)
+    o = 16 + 16 * ntask
+    tptr = np.frombuffer(raw[o:o + 4 * (ntask + 1)], np.int32)
+    o += 4 * (ntask + 1)
+    nodes = np.frombuffer(raw[o:], np.int32)
+    sr = open(solve_path, "rb").read()
+    n2 = np.frombuffer(sr[:16], np.int32)[0]
+    assert n2 == ntask
+    tr = np.frombuffer(sr[16:], np.uint64).reshape(2, ntask, 2).astype(np.int64)
+    from paper_2510_13333_b200 import sparse as ps
+    from paper_2510_13333_b200.kkt import Kkt
+    from paper_2510_13333_b200.scopf import Scopf
+    S = ps.analyze(Kkt(Scopf(grid, K, seed=2510).build_model()).matrix)
+    h = ps.supernodes(S)["height"]
+    t0 = tr[0][tr[0][:, 0] > 0, 0].min()
+    for name, T in (("forward", tr[0]), ("backward", tr[1])):
+        st, en = (T[:, 0] - t0) / 1e3, (T[:, 1] - t0) / 1e3
+        print(f"{name}: start {st[T[:, 0] > 0].min():.1f} end {en[T[:, 0] > 0].max():.1f} us")
+        for pn, a, b in (("groups", 0, nleaf), ("singles", nleaf, split), ("cta", split, ntask)):
+            sl = slice(a, b)
+            print(f"  {pn:8s} start {st[sl].min():8.1f} end {en[sl].max():8.1f} mean dur {np.mean(en[sl] - st[sl]):7.2f}")
+        hl = np.array([h[nodes[tptr[t + 1] - 1]] for t in range(split, ntask)])
+        for lv in np.unique(hl):
+            idx = np.arange(split, ntask)[hl == lv]
+            print(f"    h={lv:2d} {len(idx):5d} {st[idx].min():8.1f} {en[idx].max():8.1f} dur {np.mean(en[idx] - st[idx]):7.2f}")
