@@ -1045,6 +1045,8 @@ struct SolveArgs {
   unsigned long long* trace;  // optional (NCL_SOLVE_TRACE): globaltimer start/end per task
 };
 
+__device__ __forceinline__ void prefetch_l2(const double* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 __device__ __forceinline__ int64_t rec64(const int* r) {
   return static_cast<int64_t>(static_cast<uint32_t>(r[0])) | (static_cast<int64_t>(r[1]) << 32);
 }
@@ -1222,6 +1224,8 @@ __device__ __forceinline__ void fwd_task(const SolveArgs& a, int s, int tid) {
   const int64_t rb = __ldg(S.sn_rptr + s);
   const int nr = static_cast<int>(__ldg(S.sn_rptr + s + 1) - rb);
   const double* P = a.L + __ldg(S.sn_loff + s);
+  if (NT != 32 && nr * w >= 4096)  // wide panels (the separator roots): pull the panel into L2 up front
+    for (int64_t e = 16 * static_cast<int64_t>(tid); e < static_cast<int64_t>(nr) * w; e += 16 * NT) prefetch_l2(P + e);
   double* cv = a.CV + rb;
   double* xs = a.xp + f;
   const int64_t v0 = NT == 32 ? 0 : __ldg(S.cv_ptr + s), v1 = NT == 32 ? 0 : __ldg(S.cv_ptr + s + 1);
@@ -1442,6 +1446,8 @@ __device__ __forceinline__ void bwd_task(const SolveArgs& a, int s, int tid) {
   const int nr = static_cast<int>(__ldg(S.sn_rptr + s + 1) - rb);
   const int* Rs = S.rows + rb;
   const double* P = a.L + __ldg(S.sn_loff + s);
+  if (NT != 32 && nr * w >= 4096)  // wide panels (the separator roots): pull the panel into L2 up front
+    for (int64_t e = 16 * static_cast<int64_t>(tid); e < static_cast<int64_t>(nr) * w; e += 16 * NT) prefetch_l2(P + e);
   double* T = a.CV + rb;  // the first w CV slots are free during the backward sweep
   double* xs = a.xp + f;
   const int lane = tid & 31, warp = tid >> 5;
@@ -1486,6 +1492,7 @@ __device__ __forceinline__ void bwd_task(const SolveArgs& a, int s, int tid) {
         const bool in = c2 < c1;
         double Tl = in ? T[c2] : 0.0, xl = in ? xs[c2] : 0.0;
         const double dl = in ? __ldg(a.D + f + c2) : 1.0;
+        const int pl = in ? __ldg(S.perm + f + c2) : 0;  // loaded up front: off the column chain
         for (int cb = c1 - 1; cb >= c0; cb -= 8) {
           double pu[8];
 #pragma unroll
@@ -1501,7 +1508,7 @@ __device__ __forceinline__ void bwd_task(const SolveArgs& a, int s, int tid) {
               if (c2 == c) {
                 v = divz(xl, dl) - Tl;
                 xl = v;
-                a.x[__ldg(S.perm + f + c)] = v;
+                a.x[pl] = v;
               }
               v = __shfl_sync(kFull, v, c - c0);
               if (c2 < c) Tl += pu[u] * v;
