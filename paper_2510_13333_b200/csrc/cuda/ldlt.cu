@@ -638,6 +638,47 @@ __device__ __forceinline__ void prefetch_prog(const int* PG, int lane) {
 // cb_col in 32-bit arithmetic for the warp fronts (nr <= 32)
 __device__ __forceinline__ int cb32(int j, int m) { return j * m - ((j * (j + 1)) >> 1); }
 
+// Flat walks over a packed lower m x m triangle (column j holds rows j..m-1,
+// contiguous): advance (column j, row i) by `step` positions.
+__device__ __forceinline__ void tri_adv(int& j, int& i, int step, int m) {
+  i += step;
+  while (i >= m && j < m) {
+    const int ex = i - m;
+    ++j;
+    i = j + ex;
+  }
+}
+// zero a packed front with 16-byte stores (warp regions are 16-byte aligned)
+__device__ __forceinline__ void zero_front(double* F, int np, int lane) {
+  double2* F2 = reinterpret_cast<double2*>(F);
+  for (int k = lane; k < (np >> 1); k += 32) F2[k] = make_double2(0.0, 0.0);
+  if ((np & 1) && lane == 0) F[np - 1] = 0.0;
+}
+// lanes copy the Schur complement (front rows/cols >= w, packed nr) to a packed
+// m2 block flat: ceil(m2 (m2 + 1) / 64) rounds instead of m2
+__device__ __forceinline__ void copy_cb(const double* F, int nr, int w, double* C, int lane) {
+  const int m2 = nr - w, ne = m2 * (m2 + 1) / 2;
+  int j = 0, i = lane;
+  tri_adv(j, i, 0, m2);
+  for (int e = lane; e < ne; e += 32) {
+    C[e] = F[cb32(w + j, nr) + w + i];
+    tri_adv(j, i, 32, m2);
+  }
+}
+// extend-add of a child's packed m2c block (m2c <= 32, relative rows in lane
+// registers `reli`) into the packed front, flat; every front entry receives
+// one addition per child, so the order over children is unchanged
+__device__ __forceinline__ void extend_add_flat(double* F, int nr, const double* Cc, int m2c, int reli, int lane) {
+  const int ne = m2c * (m2c + 1) / 2;
+  int j = 0, i = lane;
+  tri_adv(j, i, 0, m2c);
+  for (int e0 = 0; e0 < ne; e0 += 32) {
+    const int rj = __shfl_sync(kFull, reli, min(j, 31)), ri = __shfl_sync(kFull, reli, min(i, 31));
+    if (e0 + lane < ne) F[cb32(rj, nr) + ri] += Cc[e0 + lane];
+    tri_adv(j, i, 32, m2c);
+  }
+}
+
 // Small front (nr <= 32) by one warp from the packed metadata: lane i owns
 // row i; children's metadata is fetched lane-parallel; the relative row map
 // of a child sits in registers (lane i holds rel[i]) and its CB columns are
@@ -658,7 +699,7 @@ __device__ __forceinline__ void small_task(const FactorArgs& a, int s, int lane,
   if (wait_children)
     for (int q = m.c0 + lane; q < m.c1; q += 32) wait_flag(a.flags + __ldg(S.child + q), a.epoch);
   // the front is PACKED lower (column c at cb_col(c, nr)): half the shared memory
-  for (int k = lane; k < nr * (nr + 1) / 2; k += 32) F[k] = 0.0;
+  zero_front(F, nr * (nr + 1) / 2, lane);
   __syncwarp();
   for (int e = lane; e < m.na; e += 32) {
     const int off = __ldg(S.aoff + m.a0 + e);
@@ -691,11 +732,15 @@ __device__ __forceinline__ void small_task(const FactorArgs& a, int s, int lane,
         __syncwarp();
         Cc = stg;
       }
-      int co = 0;
-      for (int j = 0; j < m2c; ++j) {
-        const int relj = __shfl_sync(kFull, reli, j);
-        if (lane >= j && lane < m2c) F[cb32(relj, nr) + reli] += Cc[co + lane];
-        co += m2c - j - 1;
+      if (ne <= kGrpStack) {  // staged in shared memory
+        extend_add_flat(F, nr, stg, m2c, reli, lane);
+      } else {
+        int co = 0;
+        for (int j = 0; j < m2c; ++j) {
+          const int relj = __shfl_sync(kFull, reli, j);
+          if (lane >= j && lane < m2c) F[cb32(relj, nr) + reli] += __ldcg(Cc + co + lane);
+          co += m2c - j - 1;
+        }
       }
       __syncwarp();
     }
@@ -726,8 +771,7 @@ __device__ __forceinline__ void small_task(const FactorArgs& a, int s, int lane,
   double* C = a.CB + m.cboff;
   for (int c = 0, fo = 0; c < w; fo += nr - c - 1, ++c)
     if (lane < nr) P[c * nr + lane] = lane >= c ? F[fo + lane] : 0.0;
-  for (int j = 0, co = 0, fo = cb32(w, nr) + w; j < m2; co += m2 - j - 1, fo += nr - w - j - 1, ++j)
-    if (lane >= j && lane < m2) C[co + lane] = F[fo + lane];
+  copy_cb(F, nr, w, C, lane);
   __syncwarp();
   if (publish && lane == 0) {
     __threadfence();
@@ -876,20 +920,14 @@ __device__ __forceinline__ void group_task(const FactorArgs& a, int g, int lane,
                           (static_cast<int64_t>(PG[p + 11]) << 32);
     p += 14;
     const int m2 = nr - w;
-    for (int k = lane; k < nr * (nr + 1) / 2; k += 32) F[k] = 0.0;  // packed lower front
+    zero_front(F, nr * (nr + 1) / 2, lane);  // packed lower front
     __syncwarp();
     for (int e = lane; e < ac; e += 32) F[aoffs[af + e]] = ST[af + e];  // program holds packed offsets
     __syncwarp();
     for (int q = 0; q < nch; ++q) {
       const int m2c = PG[p], off = PG[p + 1];
       const int reli = lane < m2c ? PG[p + 2 + lane] : 0;
-      const double* Cc = stack + off;
-      int co = 0;
-      for (int j = 0; j < m2c; ++j) {
-        const int relj = __shfl_sync(kFull, reli, j);
-        if (lane >= j && lane < m2c) F[cb32(relj, nr) + reli] += Cc[co + lane];
-        co += m2c - j - 1;
-      }
+      extend_add_flat(F, nr, stack + off, m2c, reli, lane);
       p += 2 + m2c;
       __syncwarp();
     }
@@ -919,8 +957,7 @@ __device__ __forceinline__ void group_task(const FactorArgs& a, int g, int lane,
     for (int c = 0, fo = 0; c < w; fo += nr - c - 1, ++c)
       if (lane < nr) P[c * nr + lane] = lane >= c ? F[fo + lane] : 0.0;
     double* C = push >= 0 ? stack + push : a.CB + cboff;
-    for (int j = 0, co = 0, fo = cb32(w, nr) + w; j < m2; co += m2 - j - 1, fo += nr - w - j - 1, ++j)
-      if (lane >= j && lane < m2) C[co + lane] = F[fo + lane];
+    copy_cb(F, nr, w, C, lane);
     __syncwarp();
     if (push < 0 && lane == 0) {  // the group root publishes its CB
       __threadfence();
