@@ -37,6 +37,8 @@ def main():
     valid = tr[:, 0] > 0
     t0 = tr[valid, 0].min()
     st, en = (tr[:, 0] - t0) / 1e3, (tr[:, 1] - t0) / 1e3  # us
+    st[~valid] = np.nan  # tasks run outside the persistent kernels (large fronts) carry no stamps
+    en[~valid] = np.nan
     task_of = np.full(len(par), -1, np.int64)
     for t in range(ntask):
         task_of[nodes[tptr[t]:tptr[t + 1]]] = t
@@ -52,13 +54,18 @@ def main():
         if b <= a:
             continue
         sl = slice(a, b)
-        print(f"{name:8s} start {st[sl].min():8.1f} end {en[sl].max():8.1f} mean dur {np.mean(en[sl] - st[sl]):7.2f} "
-              f"mean wait {np.mean(np.maximum(0, st[sl] - ready[sl])):7.2f}")
+        print(f"{name:8s} start {np.nanmin(st[sl]):8.1f} end {np.nanmax(en[sl]):8.1f} "
+              f"mean dur {np.nanmean(en[sl] - st[sl]):7.2f} mean wait {np.nanmean(np.maximum(0, st[sl] - ready[sl])):7.2f}")
     print("cta part by height of the task's last node: n, start, end, mean dur, p90 dur, mean nr, mean w, mean start-ready")
     hl = np.array([h[nodes[tptr[t + 1] - 1]] for t in range(split, ntask)])
     lastn = np.array([nodes[tptr[t + 1] - 1] for t in range(split, ntask)])
     for lv in np.unique(hl):
         m = hl == lv
+        idx = np.arange(split, ntask)[m]
+        if not valid[idx].any():
+            print(f"  h={lv:2d} {m.sum():5d} (large-front path, not stamped)")
+            continue
+        m = m & valid[split:]
         idx = np.arange(split, ntask)[m]
         du = en[idx] - st[idx]
         print(f"  h={lv:2d} {m.sum():5d} {st[idx].min():8.1f} {en[idx].max():8.1f} {du.mean():7.2f} "
