@@ -362,8 +362,7 @@ __device__ __forceinline__ void gather4(const DevSymb& S, const double* __restri
     for (int u = 0; u < kU; ++u) {
       const int64_t k = kb + u * NT;
       if (k < g1) {
-        const int d = __ldg(S.gdst + k);  // full-layout position rj * nr + ri -> packed lower
-        F[cb_col(d / nr, nr) + d % nr] = acc[u];
+        F[__ldg(S.gdst + k)] = acc[u];  // packed lower position (host-encoded for nr <= kCtaFront)
       }
     }
   }
@@ -1015,9 +1014,8 @@ __global__ void __launch_bounds__(256) big_cta_kernel(DevSymb S, const BigDesc* 
   const BigDesc b = d[blockIdx.x];
   if (b.npan != 0) return;
   const int nr = b.nr, tid = threadIdx.x;
-  const double* G = Fs + b.foff;
-  for (int c = tid >> 5; c < nr; c += 8)
-    for (int i = c + (tid & 31); i < nr; i += 32) s_front[cb_col(c, nr) + i] = __ldcg(G + static_cast<int64_t>(c) * nr + i);
+  const double* G = Fs + b.foff;  // assembled in the packed layout (gdst, nr <= kCtaFront)
+  for (int k = tid; k < nr * (nr + 1) / 2; k += 256) s_front[k] = __ldcg(G + k);
   __syncthreads();
   cta_dense<256>(s_front, nr, b.w, b.f, __ldcg(thresh_p), D, zp, L + __ldg(S.sn_loff + b.s), CB + __ldg(S.cb_off + b.s),
                  tid);

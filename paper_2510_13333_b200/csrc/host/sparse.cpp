@@ -632,9 +632,14 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
           for (int i = j; i < m2c; ++i) Z.gsrc[base + fill[static_cast<size_t>(rel[j]) * nr + rel[i]]++] = colb + i;
         }
       }
+      // destination: packed lower offset for fronts that fit the CTA path
+      // (shared-memory and one-CTA large fronts), full column-major
+      // rj * nr + ri for the wider ones (blocked DMMA path)
       for (size_t d = 0; d < static_cast<size_t>(nr) * nr; ++d)
         if (cnt[d + 1]) {
-          Z.gdst.push_back(static_cast<int>(d));
+          const int rj = static_cast<int>(d / nr), ri = static_cast<int>(d % nr);
+          const int packed = rj * nr - rj * (rj + 1) / 2 + ri;  // cb_col(rj, nr) + ri
+          Z.gdst.push_back(nr <= kSmemFront ? packed : static_cast<int>(d));
           Z.gsp.push_back(base + start[d]);
         }
       Z.gm_ptr[sn + 1] = static_cast<int64_t>(Z.gdst.size());
