@@ -73,6 +73,9 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double av, double b
                : "d"(av), "d"(bv));
 }
 
+template <typename T>
+__device__ __forceinline__ void prefetch_l2d(const T* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
   // non-negative doubles order like their bit patterns
   atomicMax(reinterpret_cast<unsigned long long*>(addr), static_cast<unsigned long long>(__double_as_longlong(v)));
@@ -551,6 +554,15 @@ __device__ __forceinline__ void cta_dense(double* F, int nr, int w, int f, doubl
 template <int NT>
 __device__ __forceinline__ void factor_task_smem(const FactorArgs& a, int s, int tid, double thresh, double* F) {
   const DevSymb& S = a.S;
+  const int64_t g0 = NT == 32 ? 0 : __ldg(S.gm_ptr + s), g1 = NT == 32 ? 0 : __ldg(S.gm_ptr + s + 1);
+  if (g1 > g0) {
+    // pull this front's gather map into L2 while the children finish: the
+    // assembly then walks it at L2 instead of HBM latency
+    const int64_t q0 = __ldg(S.gsp + g0), q1 = __ldg(S.gsp + g1);
+    for (int64_t k = g0 + 16 * static_cast<int64_t>(tid); k <= g1; k += 16 * NT) prefetch_l2d(S.gsp + k);
+    for (int64_t k = g0 + 32 * static_cast<int64_t>(tid); k < g1; k += 32 * NT) prefetch_l2d(S.gdst + k);
+    for (int64_t k = q0 + 16 * static_cast<int64_t>(tid); k < q1; k += 16 * NT) prefetch_l2d(S.gsrc + k);
+  }
   for (int q = __ldg(S.cptr + s) + tid; q < __ldg(S.cptr + s + 1); q += NT) wait_flag(a.flags + __ldg(S.child + q), a.epoch);
   const int f = __ldg(S.sn_first + s);
   const int w = __ldg(S.sn_first + s + 1) - f;
@@ -561,7 +573,6 @@ __device__ __forceinline__ void factor_task_smem(const FactorArgs& a, int s, int
   // fit in 100 KB, two CTAs per SM
   for (int k = tid; k < nr * (nr + 1) / 2; k += NT) F[k] = 0.0;
   team_sync<NT>();
-  const int64_t g0 = NT == 32 ? 0 : __ldg(S.gm_ptr + s), g1 = NT == 32 ? 0 : __ldg(S.gm_ptr + s + 1);
   if (g1 > g0) {
     // gather-sum per front entry: A value first, then the children's CB
     // entries in ascending child order (the extend-add order)
