@@ -1274,18 +1274,25 @@ __device__ __forceinline__ void fwd_warp_reg(const double* __restrict__ P, int n
 template <int NT>
 __device__ __forceinline__ void fwd_task(const SolveArgs& a, int s, int tid) {
   const DevSymb& S = a.S;
-  for (int q = __ldg(S.cptr + s) + tid; q < __ldg(S.cptr + s + 1); q += NT) wait_flag(a.flags + __ldg(S.child + q), a.epoch);
-  team_sync<NT>();
   const int f = __ldg(S.sn_first + s);
   const int w = __ldg(S.sn_first + s + 1) - f;
   const int64_t rb = __ldg(S.sn_rptr + s);
   const int nr = static_cast<int>(__ldg(S.sn_rptr + s + 1) - rb);
   const double* P = a.L + __ldg(S.sn_loff + s);
-  if (NT != 32 && nr * w >= 4096)  // wide panels (the separator roots): pull the panel into L2 up front
+  const int64_t v0 = NT == 32 ? 0 : __ldg(S.cv_ptr + s), v1 = NT == 32 ? 0 : __ldg(S.cv_ptr + s + 1);
+  if (NT != 32) {
+    // pull the panel and the gather map into L2 while the children finish
     for (int64_t e = 16 * static_cast<int64_t>(tid); e < static_cast<int64_t>(nr) * w; e += 16 * NT) prefetch_l2(P + e);
+    if (v1 > v0) {
+      const int64_t q0 = __ldg(S.cvsp + v0), q1 = __ldg(S.cvsp + v1);
+      for (int64_t k = v0 + 16 * static_cast<int64_t>(tid); k <= v1; k += 16 * NT) prefetch_l2d(S.cvsp + k);
+      for (int64_t k = q0 + 16 * static_cast<int64_t>(tid); k < q1; k += 16 * NT) prefetch_l2d(S.cvsrc + k);
+    }
+  }
+  for (int q = __ldg(S.cptr + s) + tid; q < __ldg(S.cptr + s + 1); q += NT) wait_flag(a.flags + __ldg(S.child + q), a.epoch);
+  team_sync<NT>();
   double* cv = a.CV + rb;
   double* xs = a.xp + f;
-  const int64_t v0 = NT == 32 ? 0 : __ldg(S.cv_ptr + s), v1 = NT == 32 ? 0 : __ldg(S.cv_ptr + s + 1);
   if (v1 > v0) {
     if (NT != 32 && __ldg(S.cvsp + v1) - __ldg(S.cvsp + v0) > 8 * static_cast<int64_t>(nr)) {
       // many children (the separator roots): a warp per row, lanes over its
@@ -1495,16 +1502,18 @@ template <int NT>
 __device__ __forceinline__ void bwd_task(const SolveArgs& a, int s, int tid) {
   const DevSymb& S = a.S;
   const int ps = __ldg(S.sn_parent + s);
-  if (tid == 0 && ps >= 0) wait_flag(a.flags + ps, a.epoch);
-  team_sync<NT>();
   const int f = __ldg(S.sn_first + s);
   const int w = __ldg(S.sn_first + s + 1) - f;
   const int64_t rb = __ldg(S.sn_rptr + s);
   const int nr = static_cast<int>(__ldg(S.sn_rptr + s + 1) - rb);
   const int* Rs = S.rows + rb;
   const double* P = a.L + __ldg(S.sn_loff + s);
-  if (NT != 32 && nr * w >= 4096)  // wide panels (the separator roots): pull the panel into L2 up front
+  if (NT != 32) {  // pull the panel and the row list into L2 while the parent finishes
     for (int64_t e = 16 * static_cast<int64_t>(tid); e < static_cast<int64_t>(nr) * w; e += 16 * NT) prefetch_l2(P + e);
+    for (int k = 32 * tid; k < nr; k += 32 * NT) prefetch_l2d(Rs + k);
+  }
+  if (tid == 0 && ps >= 0) wait_flag(a.flags + ps, a.epoch);
+  team_sync<NT>();
   double* T = a.CV + rb;  // the first w CV slots are free during the backward sweep
   double* xs = a.xp + f;
   const int lane = tid & 31, warp = tid >> 5;
