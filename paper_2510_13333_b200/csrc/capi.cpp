@@ -791,12 +791,16 @@ void run_factor(ncl_fact* f, ncl_sym_t M, double tol) {
   // factorization (debug timeline of the persistent schedule)
   static const char* trace_path = std::getenv("NCL_TASK_TRACE");
   static int traced = 0;
-  static DevBuf<unsigned long long> tbuf;
+  static DevBuf<unsigned long long> tbuf, pbuf;
   const int ntask = f->S->d.tasks.n;
+  const int64_t nsn = static_cast<int64_t>(f->S->Z.sn_first.size()) - 1;
   if (trace_path && traced == 2) {
     tbuf.alloc(2 * static_cast<int64_t>(ntask));
     ck(cudaMemsetAsync(tbuf.p, 0, 2 * ntask * sizeof(unsigned long long), g_stream), "memset");
     g_task_trace = tbuf.p;
+    pbuf.alloc(4 * nsn);
+    ck(cudaMemsetAsync(pbuf.p, 0, 4 * nsn * sizeof(unsigned long long), g_stream), "memset");
+    dev_phase_trace(pbuf.p);
   }
   dev_factor(f->S->d, M->dp, f->F, M->vals.p, tol, g_stream, nullptr);
   if (trace_path && traced++ == 2) {
@@ -809,6 +813,13 @@ void run_factor(ncl_fact* f, ncl_sym_t M, double tol) {
       std::fwrite(h.data(), sizeof(unsigned long long), h.size(), fp);
       std::fwrite(f->S->lay.tptr.data(), sizeof(int), f->S->lay.tptr.size(), fp);
       std::fwrite(f->S->lay.nodes.data(), sizeof(int), f->S->lay.nodes.size(), fp);
+      std::fclose(fp);
+    }
+    dev_phase_trace(nullptr);
+    std::vector<unsigned long long> hp;
+    pbuf.download(hp, 4 * nsn);
+    if (FILE* fp = std::fopen((std::string(trace_path) + ".phase").c_str(), "wb")) {
+      std::fwrite(hp.data(), sizeof(unsigned long long), hp.size(), fp);
       std::fclose(fp);
     }
   }

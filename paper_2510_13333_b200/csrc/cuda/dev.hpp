@@ -146,6 +146,7 @@ constexpr int kGrpProg = 640;       // ints: the group program
 constexpr int kTickets = 40;  // ticket counters per symbolic handle
 
 extern unsigned long long* g_task_trace;  // device buffer [2 * tasks] or nullptr
+void dev_phase_trace(unsigned long long* buf);  // device buffer [4 * nsn] or nullptr
 
 // all launches are asynchronous on `st`
 // sharded pieces: begin (threshold, epoch, tickets) -> list(s) -> inertia

@@ -551,6 +551,8 @@ __device__ __forceinline__ void cta_dense(double* F, int nr, int w, int f, doubl
   DPROF(4)
 }
 
+__device__ unsigned long long* g_phase = nullptr;  // NCL_TASK_TRACE: per-supernode CTA phase stamps [4 * nsn]
+
 template <int NT>
 __device__ __forceinline__ void factor_task_smem(const FactorArgs& a, int s, int tid, double thresh, double* F) {
   const DevSymb& S = a.S;
@@ -563,12 +565,14 @@ __device__ __forceinline__ void factor_task_smem(const FactorArgs& a, int s, int
     for (int64_t k = g0 + 32 * static_cast<int64_t>(tid); k < g1; k += 32 * NT) prefetch_l2d(S.gdst + k);
     for (int64_t k = q0 + 16 * static_cast<int64_t>(tid); k < q1; k += 16 * NT) prefetch_l2d(S.gsrc + k);
   }
+  unsigned long long* ph = g_phase ? g_phase + 4 * static_cast<int64_t>(s) : nullptr;
   for (int q = __ldg(S.cptr + s) + tid; q < __ldg(S.cptr + s + 1); q += NT) wait_flag(a.flags + __ldg(S.child + q), a.epoch);
   const int f = __ldg(S.sn_first + s);
   const int w = __ldg(S.sn_first + s + 1) - f;
   const int64_t rb = __ldg(S.sn_rptr + s);
   const int nr = static_cast<int>(__ldg(S.sn_rptr + s + 1) - rb);
   const int m2 = nr - w;
+  if (ph && tid == 0) ph[0] = gtimer();
   // the front is PACKED lower-triangular (column c at cb_col(c, nr)): 160 rows
   // fit in 100 KB, two CTAs per SM
   for (int k = tid; k < nr * (nr + 1) / 2; k += NT) F[k] = 0.0;
@@ -629,11 +633,14 @@ __device__ __forceinline__ void factor_task_smem(const FactorArgs& a, int s, int
     __syncthreads();
   }
   }  // scatter / extend-add path
+  if (ph && tid == 0) ph[1] = gtimer();
   cta_dense<NT>(F, nr, w, f, thresh, a.D, a.zp, a.L + __ldg(S.sn_loff + s), a.CB + __ldg(S.cb_off + s), tid);
   team_sync<NT>();
+  if (ph && tid == 0) ph[2] = gtimer();
   if (tid == 0) {
     __threadfence();
     st_release(a.flags + s, a.epoch);
+    if (ph) ph[3] = gtimer();
   }
 }
 
@@ -1850,6 +1857,10 @@ void dev_factor_list(const DevSymb& S, DevFactor& F, const double* kvals, const 
     factor_kernel<256><<<std::min(g_fg2, T.n - T.split), 256, kFacSmem2, st>>>(a);
   }
 }
+
+// NCL_TASK_TRACE: per-supernode phase stamps of the CTA smem path
+// (after the wait, after the assembly, after the dense factor, after publish)
+void dev_phase_trace(unsigned long long* buf) { cudaMemcpyToSymbol(g_phase, &buf, sizeof(buf)); }
 
 void dev_factor(const DevSymb& S, const DevPattern& P, DevFactor& F, const double* kvals, double pivot_tol,
                 cudaStream_t st, const TopSched* top) {

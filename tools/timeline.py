@@ -133,3 +133,34 @@ def solve_timeline(solve_path, factor_path, grid="activsg500", K=256):
         for lv in np.unique(hl):
             idx = np.arange(split, ntask)[hl == lv]
             print(f"    h={lv:2d} {len(idx):5d} {st[idx].min():8.1f} {en[idx].max():8.1f} dur {np.mean(en[idx] - st[idx]):7.2f}")
+
+
+def cta_phases(path, grid="activsg500", K=256):
+    """CTA-path phase split per height: claim->after wait, assembly, dense+writeout, fence+publish (us)."""
+    raw = open(path, "rb").read()
+    ntask, nleaf, split, _ = np.frombuffer(raw[:16], np.int32)
+    o = 16
+    tr = np.frombuffer(raw[o:o + 16 * ntask], np.uint64).reshape(ntask, 2).astype(np.int64)
+    o += 16 * ntask
+    tptr = np.frombuffer(raw[o:o + 4 * (ntask + 1)], np.int32)
+    o += 4 * (ntask + 1)
+    nodes = np.frombuffer(raw[o:], np.int32)
+    ph = np.fromfile(path + ".phase", np.uint64).reshape(-1, 4).astype(np.int64)
+    from paper_2510_13333_b200 import sparse as ps
+    from paper_2510_13333_b200.kkt import Kkt
+    from paper_2510_13333_b200.scopf import Scopf
+    S = ps.analyze(Kkt(Scopf(grid, K, seed=2510).build_model()).matrix)
+    h = ps.supernodes(S)["height"]
+    rows = []
+    for t in range(split, ntask):
+        s = nodes[tptr[t]]
+        if ph[s, 0] == 0:
+            continue
+        rows.append((h[s], (ph[s, 0] - tr[t, 0]) / 1e3, (ph[s, 1] - ph[s, 0]) / 1e3, (ph[s, 2] - ph[s, 1]) / 1e3,
+                     (ph[s, 3] - ph[s, 2]) / 1e3))
+    rows = np.array(rows)
+    print("height  n   wait   assembly   dense+writeout   publish  (mean us)")
+    for lv in np.unique(rows[:, 0]):
+        m = rows[:, 0] == lv
+        print(f"  h={int(lv):2d} {m.sum():5d} {rows[m, 1].mean():7.2f} {rows[m, 2].mean():9.2f} {rows[m, 3].mean():12.2f} "
+              f"{rows[m, 4].mean():9.2f}")
