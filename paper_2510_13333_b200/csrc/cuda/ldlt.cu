@@ -340,7 +340,7 @@ template <int NT>
 __device__ __forceinline__ void gather4(const DevSymb& S, const double* __restrict__ kvals,
                                         const double* __restrict__ CB, int64_t g0, int64_t g1, int tid, double* F,
                                         int nr) {
-  constexpr int kU = 8;  // front entries in flight per thread
+  constexpr int kU = NT == 128 ? 4 : 8;  // front entries in flight per thread (register budget)
   for (int64_t kb = g0 + tid; kb < g1; kb += kU * NT) {
     int64_t q[kU], q1[kU];
     double acc[kU];
@@ -353,13 +353,24 @@ __device__ __forceinline__ void gather4(const DevSymb& S, const double* __restri
       acc[u] = 0.0;
       cmax = max(cmax, static_cast<int>(q1[u] - q[u]));
     }
-    for (int c = 0; c < cmax; ++c) {
+    for (int c = 0; c < cmax; c += 2) {  // two sources per entry in flight (same summation order)
+      int64_t sa[kU], sb[kU];
 #pragma unroll
-      for (int u = 0; u < kU; ++u)
-        if (q[u] + c < q1[u]) {
-          const int64_t src = __ldg(S.gsrc + q[u] + c);
-          acc[u] += src < 0 ? __ldg(kvals + ~src) : __ldcg(CB + src);
-        }
+      for (int u = 0; u < kU; ++u) {
+        sa[u] = q[u] + c < q1[u] ? __ldg(S.gsrc + q[u] + c) : 0;
+        sb[u] = q[u] + c + 1 < q1[u] ? __ldg(S.gsrc + q[u] + c + 1) : 0;
+      }
+      double va[kU], vb[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        va[u] = q[u] + c < q1[u] ? (sa[u] < 0 ? __ldg(kvals + ~sa[u]) : __ldcg(CB + sa[u])) : 0.0;
+        vb[u] = q[u] + c + 1 < q1[u] ? (sb[u] < 0 ? __ldg(kvals + ~sb[u]) : __ldcg(CB + sb[u])) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (q[u] + c < q1[u]) acc[u] += va[u];
+        if (q[u] + c + 1 < q1[u]) acc[u] += vb[u];
+      }
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
