@@ -341,6 +341,7 @@ __device__ __forceinline__ void gather4(const DevSymb& S, const double* __restri
                                         const double* __restrict__ CB, int64_t g0, int64_t g1, int tid, double* F,
                                         int nr) {
   constexpr int kU = NT == 128 ? 4 : 8;  // front entries in flight per thread (register budget)
+  constexpr int kC = 2;                  // sources per entry in flight
   for (int64_t kb = g0 + tid; kb < g1; kb += kU * NT) {
     int64_t q[kU], q1[kU];
     double acc[kU];
@@ -353,24 +354,23 @@ __device__ __forceinline__ void gather4(const DevSymb& S, const double* __restri
       acc[u] = 0.0;
       cmax = max(cmax, static_cast<int>(q1[u] - q[u]));
     }
-    for (int c = 0; c < cmax; c += 2) {  // two sources per entry in flight (same summation order)
-      int64_t sa[kU], sb[kU];
+    for (int c = 0; c < cmax; c += kC) {  // kC sources per entry in flight (same summation order)
+      int64_t sv[kC][kU];
 #pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        sa[u] = q[u] + c < q1[u] ? __ldg(S.gsrc + q[u] + c) : 0;
-        sb[u] = q[u] + c + 1 < q1[u] ? __ldg(S.gsrc + q[u] + c + 1) : 0;
-      }
-      double va[kU], vb[kU];
+      for (int r = 0; r < kC; ++r)
 #pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        va[u] = q[u] + c < q1[u] ? (sa[u] < 0 ? __ldg(kvals + ~sa[u]) : __ldcg(CB + sa[u])) : 0.0;
-        vb[u] = q[u] + c + 1 < q1[u] ? (sb[u] < 0 ? __ldg(kvals + ~sb[u]) : __ldcg(CB + sb[u])) : 0.0;
-      }
+        for (int u = 0; u < kU; ++u) sv[r][u] = q[u] + c + r < q1[u] ? __ldg(S.gsrc + q[u] + c + r) : 0;
+      double vv[kC][kU];
 #pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        if (q[u] + c < q1[u]) acc[u] += va[u];
-        if (q[u] + c + 1 < q1[u]) acc[u] += vb[u];
-      }
+      for (int r = 0; r < kC; ++r)
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+          vv[r][u] = q[u] + c + r < q1[u] ? (sv[r][u] < 0 ? __ldg(kvals + ~sv[r][u]) : __ldcg(CB + sv[r][u])) : 0.0;
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+#pragma unroll
+        for (int r = 0; r < kC; ++r)
+          if (q[u] + c + r < q1[u]) acc[u] += vv[r][u];
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
