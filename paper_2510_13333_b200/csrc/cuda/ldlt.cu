@@ -436,45 +436,50 @@ __device__ __forceinline__ void cta_dense(double* F, int nr, int w, int f, doubl
     //      trailing lower triangle on the FP64 tensor cores (mma.m8n8k4.f64,
     //      8 x 8 tiles, two k-steps), tiles dealt round-robin to the warps.
     constexpr int kPb = 8;
+    constexpr int nw = NT / 32;
     const int lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, tg = lane & 3;
-    for (int c0 = 0; c0 < w; c0 += kPb) {
+    // (a) the kb x kb diagonal block of the panel at c0, by warp 0
+    auto diag_block = [&](int c0) {
       const int kb = min(kPb, w - c0);
-      if (warp == 0) {
-        double x[kPb];
-        const int i = c0 + lane;
+      double x[kPb];
+      const int i = c0 + lane;
 #pragma unroll
-        for (int k = 0; k < kPb; ++k) x[k] = (k < kb && k <= lane && lane < kb) ? F[cb_col(c0 + k, nr) + i] : 0.0;
+      for (int k = 0; k < kPb; ++k) x[k] = (k < kb && k <= lane && lane < kb) ? F[cb_col(c0 + k, nr) + i] : 0.0;
 #pragma unroll
-        for (int k = 0; k < kPb; ++k) {
-          if (k < kb) {
-            const double d = __shfl_sync(kFull, x[k], k);
-            if (lane > k && lane < kb) x[k] = divz(x[k], d);
-            const double dlo = d * x[k];  // lane k2: d * L(c0 + k2, c0 + k)
+      for (int k = 0; k < kPb; ++k) {
+        if (k < kb) {
+          const double d = __shfl_sync(kFull, x[k], k);
+          if (lane > k && lane < kb) x[k] = divz(x[k], d);
+          const double dlo = d * x[k];  // lane k2: d * L(c0 + k2, c0 + k)
 #pragma unroll
-            for (int k2 = 0; k2 < kPb; ++k2) {  // full range: unrolls with k
-              if (k2 > k && k2 < kb) {
-                const double dl = __shfl_sync(kFull, dlo, k2);
-                if (lane >= k2 && lane < kb) x[k2] -= x[k] * dl;
-              }
+          for (int k2 = 0; k2 < kPb; ++k2) {  // full range: unrolls with k
+            if (k2 > k && k2 < kb) {
+              const double dl = __shfl_sync(kFull, dlo, k2);
+              if (lane >= k2 && lane < kb) x[k2] -= x[k] * dl;
             }
           }
         }
+      }
+#pragma unroll
+      for (int k = 0; k < kPb; ++k)
+        if (k < kb && k <= lane && lane < kb) F[cb_col(c0 + k, nr) + i] = x[k];
+      if (lane < kb) {  // lane k's diagonal entry is the pivot d_k
+        double dk = 0.0;
 #pragma unroll
         for (int k = 0; k < kPb; ++k)
-          if (k < kb && k <= lane && lane < kb) F[cb_col(c0 + k, nr) + i] = x[k];
-        if (lane < kb) {  // lane k's diagonal entry is the pivot d_k
-          double dk = 0.0;
-#pragma unroll
-          for (int k = 0; k < kPb; ++k)
-            if (k == lane) dk = x[k];
-          D[f + c0 + lane] = dk;
-          if (fabs(dk) <= thresh) atomicMin(zp, f + c0 + lane);
-        }
+          if (k == lane) dk = x[k];
+        D[f + c0 + lane] = dk;
+        if (fabs(dk) <= thresh) atomicMin(zp, f + c0 + lane);
       }
+    };
+    if (warp == 0 && w > 0) diag_block(0);
+    __syncthreads();
+    for (int c0 = 0; c0 < w; c0 += kPb) {
+      const int kb = min(kPb, w - c0);
       DPROF(0)
-      __syncthreads();
       DPROF(1)
+      // (b) rows below the diagonal block, one per thread
       for (int i = c0 + kb + tid; i < nr; i += NT) {
         double x[kPb];
 #pragma unroll
@@ -496,7 +501,11 @@ __device__ __forceinline__ void cta_dense(double* F, int nr, int w, int f, doubl
       }
       __syncthreads();
       DPROF(2)
+      // (c) trailing update of [c1, nr)^2 on the tensor cores; the strip of
+      // the next panel (tile column 0) first, then — look-ahead — warp 0
+      // factors the next diagonal block while the other warps finish the rest
       const int c1 = c0 + kb, m = nr - c1;
+      const bool ahead = c1 < w;
       if (m > 0) {
         const int T = (m + 7) >> 3;
         const int ka = tg, kc = tg + 4;  // this lane's two k indices (A column / B row)
@@ -504,25 +513,21 @@ __device__ __forceinline__ void cta_dense(double* F, int nr, int w, int f, doubl
         const double* Lc = F + cb_col(c0 + kc, nr);
         const double da = ka < kb ? La[c0 + ka] : 0.0;
         const double dc = kc < kb ? Lc[c0 + kc] : 0.0;
-        // tile rows ti dealt to the warps in snake order (row ti holds ti + 1
-        // tiles); per row the A fragments stay in registers and four tiles
-        // are in flight at a time (loads, 8 DMMAs, then the read-modify-writes)
-        constexpr int nw = NT / 32;
-        for (int r = 0; r * nw < T; ++r) {
-          const int ti = (r & 1) ? r * nw + nw - 1 - warp : r * nw + warp;
-          if (ti >= T) continue;
+        // tiles (ti, tj), tj in [tj_lo, ti]: A fragments in registers, four
+        // tiles in flight (loads, 8 DMMAs, then the read-modify-writes)
+        auto tile_row = [&](int ti, int tj_lo, int tj_hi) {
           const int i = c1 + ti * 8 + g;
           double a0 = 0.0, a1 = 0.0;
           if (i < nr) {
             if (ka < kb) a0 = La[i];
             if (kc < kb) a1 = Lc[i];
           }
-          for (int tj0 = 0; tj0 <= ti; tj0 += 4) {
+          for (int tj0 = tj_lo; tj0 <= tj_hi; tj0 += 4) {
             double b0[4], b1[4], acc[4][2];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const int j = c1 + (tj0 + u) * 8 + g;
-              const bool ok = tj0 + u <= ti && j < nr;
+              const bool ok = tj0 + u <= tj_hi && j < nr;
               b0[u] = ok && ka < kb ? da * La[j] : 0.0;
               b1[u] = ok && kc < kb ? dc * Lc[j] : 0.0;
             }
@@ -535,13 +540,31 @@ __device__ __forceinline__ void cta_dense(double* F, int nr, int w, int f, doubl
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const int jj = c1 + (tj0 + u) * 8 + 2 * tg;
-              if (tj0 + u <= ti && i < nr) {
+              if (tj0 + u <= tj_hi && i < nr) {
                 if (jj < nr && i >= jj) F[cb_col(jj, nr) + i] -= acc[u][0];
                 if (jj + 1 < nr && i >= jj + 1) F[cb_col(jj + 1, nr) + i] -= acc[u][1];
               }
             }
           }
+        };
+        if (ahead) {
+          for (int ti = warp; ti < T; ti += nw) tile_row(ti, 0, 0);  // the next panel's columns
+          __syncthreads();
         }
+        const int tj_lo = ahead ? 1 : 0;
+        if (ahead && warp == 0) {
+          diag_block(c1);
+        } else {
+          // remaining tile rows dealt in snake order to the working warps
+          const int nwk = ahead ? nw - 1 : nw, wk = ahead ? warp - 1 : warp;
+          for (int r = 0; r * nwk < T; ++r) {
+            const int ti = (r & 1) ? r * nwk + nwk - 1 - wk : r * nwk + wk;
+            if (ti >= T || ti < tj_lo) continue;
+            tile_row(ti, tj_lo, ti);
+          }
+        }
+      } else if (ahead && warp == 0) {
+        diag_block(c1);
       }
       __syncthreads();
       DPROF(3)
