@@ -141,7 +141,7 @@ struct TaskLayout {
 // per-warp shared-memory budget of a group task (csrc/cuda/ldlt.cu)
 constexpr int kGrpFront = 32;       // fronts of group nodes: nr <= 32 (packed lower: 528 doubles)
 constexpr int kGrpStack = 512;      // doubles: A values + contribution-block stack
-constexpr int kGrpProg = 640;       // ints: the group program
+constexpr int kGrpProg = 1280;      // ints: the group program (read in place: bounds group size only)
 
 constexpr int kTickets = 40;  // ticket counters per symbolic handle
 
