@@ -110,6 +110,26 @@ def _peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def workload(grid, K):
+    """One workload string for both arms (same_config)."""
+    return f"{grid}x{K} condensed KKT factor+solve (paper layout, seed {SEED})"
+
+
+def ipm_point(bd, m, seed=SEED):
+    """The IPM-like point the bench KKT is formed at (both arms): w = x0,
+    lambda ~ 0.1 N(0, 1), bound duals 1 / distance to the bounds (zero for
+    free variables), D = rho = 100 on every row."""
+    w = bd["x0"]
+    rng = np.random.default_rng(seed)
+    lam = 0.1 * rng.standard_normal(m)
+    xl, xu = bd["xl"], bd["xu"]
+    sig = np.zeros(len(w))
+    fl, fu = np.isfinite(xl), np.isfinite(xu)
+    sig[fl] += 1.0 / np.maximum(w[fl] - xl[fl], 1e-2)
+    sig[fu] += 1.0 / np.maximum(xu[fu] - w[fu], 1e-2)
+    return w, lam, sig, np.full(m, 100.0)
+
+
 def build_problem(grid, K):
     """Synthetic SCOPF -> model -> condensed KKT at an IPM-like point."""
     from paper_2510_13333_b200 import sparse as ps
@@ -122,18 +142,9 @@ def build_problem(grid, K):
     kk = Kkt(M)
     t_build = time.perf_counter() - t0
     bd = s.bounds()
-    w = bd["x0"]
-    rng = np.random.default_rng(SEED)
-    lam = 0.1 * rng.standard_normal(M.m)
+    w, lam, sig, D = ipm_point(bd, M.m)
     hess = M.eval_hessian_lag(w, 1e-4, lam)
     jac = M.eval_jacobian(w)
-    # IPM-like diagonal: bound duals 1 / distance to the bounds (zero for free variables)
-    xl, xu = bd["xl"], bd["xu"]
-    sig = np.zeros(M.n)
-    fl, fu = np.isfinite(xl), np.isfinite(xu)
-    sig[fl] += 1.0 / np.maximum(w[fl] - xl[fl], 1e-2)
-    sig[fu] += 1.0 / np.maximum(xu[fu] - w[fu], 1e-2)
-    D = np.full(M.m, 100.0)  # rho = 100
     kk.assemble(hess, jac, sig, 1e-8, D)
     t0 = time.perf_counter()
     S = ps.analyze(kk.matrix)
@@ -142,35 +153,87 @@ def build_problem(grid, K):
 
 
 def run_reference(a, world):
-    """--impl reference: the reference CPU factorize+solve (oracle/_ref) on the same matrix."""
-    from oracle.ref import RefFactorization, RefSparseSym, RefSymbolic
+    """--impl reference: the reference's own CPU factorize + solve
+    (oracle/_ref: /root/reference/proj/src compiled unmodified) on the same
+    workload, built WITHOUT the product library: the instance generator
+    compiled into the oracle, the reference ModelBuilder for H and J, the
+    reference SparseSym for K, the reference symbolic_order + analyze for the
+    ordering (untimed), then `steps` timed factorize + solve."""
+    import json as _json
 
-    P = build_problem(a.grid, a.K)
-    A, S = P["A"], P["S"]
-    n = A.dim()
-    cp, ri, v = A.col_ptr(), A.row_ind(), A.values()
-    cols = np.repeat(np.arange(n, dtype=np.int32), np.diff(cp))
-    R = RefSparseSym(n, ri, cols, v)
-    RS = RefSymbolic(R, S.perm)  # perm bit-identical to the reference symbolic_order (tests/test_symbolic.py)
+    from oracle.ref import RefFactorization, RefScopf, RefSymbolic, ref_condensed_kkt, ref_symbolic_order
+
+    kind, nb, nl, ng = _grid_dims(a.grid)
+    t0 = time.perf_counter()
+    rs = RefScopf(kind, nb, nl, ng, SEED, a.K, _contingency_ids(a.grid, a.K))
+    R = rs.model()
+    w, lam, sig, D = ipm_point(rs.bounds(), R.m)
+    K = ref_condensed_kkt(R, R.eval_hessian_lag(w, 1e-4, lam), R.eval_jacobian(w), sig, 1e-8, D)
+    t_build = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    perm = ref_symbolic_order(K)
+    RS = RefSymbolic(K, perm)
+    t_order = time.perf_counter() - t0
+    n = K.n
     b = np.random.default_rng(1).standard_normal(n)
     times = []
     for it in range(a.warmup + a.steps):
         t0 = time.perf_counter()
-        F = RefFactorization(R, RS)
+        F = RefFactorization(K, RS)
         F.solve(b)
         dt = time.perf_counter() - t0
         if it >= a.warmup:
             times.append(dt)
     ms = 1e3 * sum(times) / len(times)
-    line = {"metric": METRIC, "impl": "reference", "value": ms, "unit": "ms/IPM-iter (KKT factor+solve)",
+    unit = "ms/IPM-iter (KKT factor+solve)"
+    with open("/proc/self/maps") as f:
+        maps = f.read()
+    assert "libnclopf_b200" not in maps, "the reference arm must not load the product library"
+    line = {"metric": METRIC, "impl": "reference", "value": ms, "unit": unit,
             "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{a.grid}x{a.K} condensed KKT factor+solve", "N": n, "nnzK": A.nnz()},
-            "cpu_baseline": {"value": ms, "unit": "ms/IPM-iter (KKT factor+solve)", "cores": 1,
-                             "kind": "reference", "sample": f"{a.steps} factorize+solve of the {a.grid}x{a.K} KKT"},
-            "e2e": {"value": ms, "unit": "ms/IPM-iter (KKT factor+solve)", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+            "config": {"workload": workload(a.grid, a.K), "N": n, "nnzK": K.nnz(), "l_nnz": int(RS.l_nnz),
+                       "status": F.status, "inertia": list(F.inertia),
+                       "setup_s": {"build": t_build, "symbolic_order+analyze": t_order}},
+            "cpu_baseline": {"value": ms, "unit": unit, "cores": 1, "kind": "reference", "cpu": _cpu_model(),
+                             "sample": f"{a.steps} reference factorize+solve of the {a.grid}x{a.K} KKT "
+                                       "(model, K and ordering built by the reference code; 1 thread: "
+                                       "the reference has no threads)"},
+            "e2e": {"value": ms, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(_json.dumps(line), flush=True)
+
+
+def _grid_dims(grid):
+    # GRIDS of paper_2510_13333_b200/scopf.py, restated so the reference arm
+    # never imports the product package (which loads libnclopf_b200.so)
+    return {"case9": (0, 9, 9, 3), "case118": (1, 118, 186, 54), "activsg500": (1, 500, 597, 56),
+            "activsg2000": (1, 2000, 3206, 432)}[grid]
+
+
+def _contingency_ids(grid, K):
+    """paper_2510_13333_b200.scopf.contingency_ids without importing the
+    package: screened outages, then the same outages at load levels 1..3."""
+    p = os.path.join(ROOT, "paper_2510_13333_b200", "data", f"screened_{grid}_{SEED}.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        base = json.load(f)["feasible"]
+    nl = _grid_dims(grid)[2]
+    ids = [l + nl * j for j in range(4) for l in base]
+    if len(ids) < K:
+        raise ValueError(f"only {len(ids)} contingencies for {grid}")
+    return ids[:K]
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip() + f" ({os.cpu_count()} logical CPUs)"
+    except OSError:
+        pass
+    return None
 
 
 def main():
@@ -333,6 +396,11 @@ def main():
 
     cpu = None
     if rank == 0 and not a.no_cpu_baseline and os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libnclopf_ref.so")):
+        # the reference factorize + solve of the SAME matrix (this arm's K
+        # values, this arm's permutation — bit-identical to the reference
+        # symbolic_order, tests/test_symbolic.py), timed, and used as the
+        # parity check of the bench step itself: D (pivot order), inertia,
+        # status and x of the GPU factor + solve against the reference's
         from oracle.ref import RefFactorization, RefSparseSym, RefSymbolic
 
         cp, ri, v = A.col_ptr(), A.row_ind(), A.values()
@@ -342,18 +410,30 @@ def main():
         ts = []
         for _ in range(3):
             t0 = time.perf_counter()
-            RefFactorization(R, RS).solve(bb)
+            G = RefFactorization(R, RS)
+            xr = G.solve(bb)
             ts.append(time.perf_counter() - t0)
+        Fp = ps.factorize(A, S)
+        dg, dr = Fp.diagonal(), G.diagonal()
+        xg = Fp.solve(bb)
+        ia = Fp.inertia
+        parity = {"status_equal": Fp.status == G.status, "inertia_equal": (ia.n_pos, ia.n_neg, ia.n_zero) == G.inertia,
+                  "D_max_rel": float(np.max(np.abs(dg - dr) / np.maximum(np.abs(dr), 1e-300))),
+                  "x_max_rel": float(np.max(np.abs(xg - xr)) / max(1e-300, float(np.max(np.abs(xr))))),
+                  "perm_equal": bool(np.array_equal(RS.perm, S.perm)),
+                  "l_nnz_equal": int(RS.l_nnz) == int(info.l_nnz)}
+        del Fp
         cpu = {"value": 1e3 * statistics.median(ts), "unit": "ms/IPM-iter (KKT factor+solve)", "cores": 1,
-               "kind": "reference",
-               "sample": f"3 reference factorize+solve of the same {a.grid}x{a.K} KKT (median), 1 thread"}
+               "kind": "reference", "cpu": _cpu_model(),
+               "sample": f"3 reference factorize+solve of the same {a.grid}x{a.K} KKT (median), 1 thread",
+               "parity_vs_gpu": parity}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": step_ms, "unit": "ms/IPM-iter (KKT factor+solve)", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": step_ms, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{a.grid}x{a.K} condensed KKT factor+solve (paper layout, seed {SEED})",
+            "config": {"workload": workload(a.grid, a.K),
                        "N": n, "nnzK": nnzk, "l_nnz": info.l_nnz, "supernodes": info.nsupernodes,
                        "sn_height": info.max_height, "flops": info.flops, "l2": "flushed (256 MiB write) between steps",
                        "parallelism": f"contingency-sharded x{world} (NCCL all-gather of subtree-root CBs)"

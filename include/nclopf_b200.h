@@ -199,8 +199,11 @@ typedef struct ncl_scopf_info {
   int nvar_scen, ncon_scen;
 } ncl_scopf_info;
 int ncl_scopf_create(int grid, int nb, int nl, int ng, uint64_t seed, int K, ncl_scopf_t* out);
-/* explicit outage list (branch ids, non-islanding; e.g. a screened list,
- * PAPER.md:526-543); branch_ids == NULL -> the first K non-islanding */
+/* explicit contingency list (e.g. a screened list);
+ * branch_ids == NULL -> the first K non-islanding outages. An id is
+ * l + nl * j: the outage of non-islanding branch l with the post-contingency
+ * loads scaled by 1 - 0.015 j, j < 4 (j = 0: the plain N-1 outage; j > 0
+ * gives outage x load-scenario contingencies, csrc/host/scopf.hpp) */
 int ncl_scopf_create_list(int grid, int nb, int nl, int ng, uint64_t seed, int K, const int* branch_ids,
                           ncl_scopf_t* out);
 void ncl_scopf_destroy(ncl_scopf_t S);

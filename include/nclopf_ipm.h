@@ -63,7 +63,10 @@ enum ncl_solve_status {
   NCL_SOLVE_INFEASIBLE = 1,
   NCL_SOLVE_ITERATION_LIMIT = 2,
   NCL_SOLVE_REG_EXHAUSTED = 3,
-  NCL_SOLVE_RESTORATION_FAILED = 4
+  NCL_SOLVE_RESTORATION_FAILED = 4,
+  /* |r|_inf <= eta* but the last subproblem stopped on the 'acceptable'
+   * rule (E_0 <= acceptable_factor * omega*), not on E_0 <= omega* */
+  NCL_SOLVE_ACCEPTABLE = 5
 };
 
 typedef struct ncl_result {
@@ -73,9 +76,10 @@ typedef struct ncl_result {
   double r_inf;         /* |r|_inf (includes t on complementarity rows) */
   double inf_pr, inf_du, compl_;  /* final subproblem KKT residuals */
   double rho, mu;
-  int multiplier_warning; /* |lamN|_inf > lambda_max */
+  int multiplier_warning; /* set when a multiplier update leaves |lamN|_inf > lambda_max */
   /* wall-clock seconds (host timer around synchronous backend calls) */
   double t_total, t_init, t_eval, t_factor, t_solve, t_linesearch, t_other;
+  double final_e0;      /* scaled KKT error E_0 at the last subproblem's exit */
 } ncl_result;
 
 /* ---- B200 solve (libnclopf_b200.so) -------------------------------------

@@ -69,6 +69,12 @@ def lib():
             "ref_ipm_last_error": (C.c_char_p, []),
             "ref_ipm_default_options": (None, [P]),
             "ref_ncl_solve": (i32, [P, P, P, P, P, P, P, P, P, P, P, C.c_char_p, i64, C.POINTER(i64)]),
+            "ref_scopf_last_error": (C.c_char_p, []),
+            "ref_scopf_new": (i32, [i32, i32, i32, i32, C.c_uint64, i32, P, C.POINTER(P), pi, pi]),
+            "ref_scopf_free": (None, [P]),
+            "ref_scopf_bounds": (None, [P, P, P, P, P, P]),
+            "ref_scopf_model": (i32, [P, C.POINTER(P)]),
+            "ref_condensed_kkt": (i32, [P, P, P, P, f64, P, C.POINTER(P)]),
         }
         for k, (r, a) in sig.items():
             fn = getattr(L, k)
@@ -317,6 +323,49 @@ class RefModel:
         return dict(grad_err=errs[0], jac_err=errs[1], hess_err=errs[2], pass_=bool(ok.value))
 
 
+class RefScopf:
+    """The SCOPF instance (csrc/host/scopf.cpp compiled into the oracle) with
+    its reference ModelFunctions — no product library involved. grid: 0 =
+    case9, 1 = synthetic (nb, nl, ng, seed); ids: contingency ids or None."""
+
+    def __init__(self, grid, nb, nl, ng, seed, K, ids=None):
+        h, n, m = C.c_void_p(), C.c_int(), C.c_int()
+        idp = None if ids is None else np.ascontiguousarray(ids, np.int32)
+        if lib().ref_scopf_new(int(grid), int(nb), int(nl), int(ng), int(seed), int(K), _p(idp), C.byref(h),
+                               C.byref(n), C.byref(m)):
+            raise RefError(1, lib().ref_scopf_last_error().decode())
+        self.h, self.n, self.m = h, n.value, m.value
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ref_scopf_free(self.h)
+            self.h = None
+
+    def bounds(self):
+        xl, xu, x0 = (np.empty(self.n) for _ in range(3))
+        gl, gu = np.empty(self.m), np.empty(self.m)
+        lib().ref_scopf_bounds(self.h, _p(xl), _p(xu), _p(x0), _p(gl), _p(gu))
+        return dict(xl=xl, xu=xu, x0=x0, gl=gl, gu=gu)
+
+    def model(self) -> "RefModel":
+        h = C.c_void_p()
+        _chk(lib().ref_scopf_model(self.h, C.byref(h)))
+        return RefModel(h)
+
+
+def ref_condensed_kkt(model: "RefModel", hess, jac, sig, dw, D) -> RefSparseSym:
+    """K = H + diag(sig + dw) + J' diag(D) J assembled by the reference
+    SparseSym in the product's triplet order (oracle/ref_scopf.cpp)."""
+    h = C.c_void_p()
+    a = [np.ascontiguousarray(v, np.float64) for v in (hess, jac, sig)]
+    Dv = np.ascontiguousarray(D, np.float64)
+    if lib().ref_condensed_kkt(model.h, _p(a[0]), _p(a[1]), _p(a[2]), float(dw), _p(Dv), C.byref(h)):
+        raise RefError(1, lib().ref_scopf_last_error().decode())
+    K = RefSparseSym.__new__(RefSparseSym)
+    K.h, K.n = h, model.n
+    return K
+
+
 def ref_ncl_solve(model: RefModel, bounds, perm=None, options=None, trace_cap=1 << 26):
     """ncl_solve over the reference CPU backend (oracle/ref_ipm.cpp): the same
     host NCL/IPM control flow driving the UNMODIFIED reference model_ad and
@@ -340,5 +389,7 @@ def ref_ncl_solve(model: RefModel, bounds, perm=None, options=None, trace_cap=1 
                          buf, trace_cap, C.byref(ln))
     if rc != 0:
         raise RefError(rc, L.ref_ipm_last_error().decode())
-    trace = [json.loads(t) for t in buf.value.decode().splitlines() if t.strip()]
+    from paper_2510_13333_b200.ipm import parse_trace
+
+    trace = parse_trace(buf.value.decode())
     return dict(result=res.as_dict(), status=STATUS.get(res.status, str(res.status)), x=x, y=y, trace=trace)

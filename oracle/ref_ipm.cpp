@@ -207,8 +207,13 @@ class RefBackend final : public ipm::Backend {
     *dxinf = a[1];
     *xinf = a[2];
   }
-  void update_multipliers() override {
-    for (int i = 0; i < m_; ++i) ipm::update_multiplier_row(V_, i);
+  double update_multipliers() override {
+    double a = 0.0;
+    for (int i = 0; i < m_; ++i) {
+      ipm::update_multiplier_row(V_, i);
+      a = std::fmax(a, std::fabs(lamN_[i]));
+    }
+    return a;
   }
   double objective() const override { return fcur_; }
   void get_solution(double* x, double* y, double* r) override {

@@ -81,7 +81,8 @@ class GpuBackend final : public ipm::Backend {
     jac_ = take(nj);
     hess_ = take(nh);
     dsc_ = take(16);  // [0] f(x) [1] f(xt) [2..9] reduction outputs
-    part_.alloc(static_cast<int64_t>(ipm::kRedBlocks) * 8);
+    part_.alloc(static_cast<int64_t>(ipm::kRedBlocks) * 8 + 1);  // + completion ticket
+    ck(cudaMemsetAsync(part_.p, 0, part_.n * sizeof(double), g_stream), "memset");
     auto up = [&](double* d, const double* h, int64_t cnt) {
       if (cnt) ck(cudaMemcpyAsync(d, h, cnt * sizeof(double), cudaMemcpyHostToDevice, g_stream), "H2D");
     };
@@ -123,6 +124,9 @@ class GpuBackend final : public ipm::Backend {
   void eval_derivatives(double sf) override {
     chk(ncl_model_eval_all_device(M_, V_.x, sf, V_.y, nullptr, V_.grad, nullptr, jac_, hess_));
     chk(ncl_model_jac_trans_times(M_, jac_, V_.y, V_.jty, NCL_DEVICE));
+    // complete here so the host timer charges evaluation to t_eval rather
+    // than to whichever phase synchronises next
+    ck(cudaStreamSynchronize(g_stream), "sync");
   }
   ipm::KktErr kkt_error(const ipm::Scal& S) override {
     reduce(IR_KKT, S, 7);
@@ -202,7 +206,13 @@ class GpuBackend final : public ipm::Backend {
     *dxinf = hsc_[3];
     *xinf = hsc_[4];
   }
-  void update_multipliers() override { dev_ipm_elem(IE_UPDATE_MULT, V_, ipm::Scal{}, g_stream); }
+  double update_multipliers() override {
+    dev_ipm_elem(IE_UPDATE_MULT, V_, ipm::Scal{}, g_stream);
+    ck(cudaMemsetAsync(dsc_ + 2, 0, sizeof(double), g_stream), "memset");
+    dev_absmax(V_.lamN, m_, dsc_ + 2, g_stream);
+    fetch(2, 1);
+    return hsc_[2];
+  }
   double objective() const override { return fcur_; }
   void get_solution(double* x, double* y, double* r) override {
     auto dn = [&](double* h, const double* d, int64_t cnt) {

@@ -62,10 +62,10 @@ API int ncl_scopf_create_list(int grid, int nb, int nl, int ng, uint64_t seed, i
     if (branch_ids) {
       const auto ok = select_contingencies(s->grid, s->grid.nl);  // non-islanding set
       for (int k = 0; k < K; ++k) {
-        const int l = branch_ids[k];
-        if (!std::binary_search(ok.begin(), ok.end(), l))
+        const int id = branch_ids[k];  // branch + nl * load level (host/scopf.hpp)
+        if (id < 0 || id / s->grid.nl >= kLoadLevels || !std::binary_search(ok.begin(), ok.end(), id % s->grid.nl))
           throw Error{NCL_E_INVALID, "scopf: contingency islands the network or is out of range"};
-        cont.push_back(l);
+        cont.push_back(id);
       }
     } else {
       cont = select_contingencies(s->grid, K);

@@ -22,7 +22,8 @@ enum IpmRedOp { IR_KKT = 0, IR_FTB, IR_MERIT, IR_DPHI, IR_RINF };
 
 // asynchronous on st
 void dev_ipm_elem(int op, const ipm::Vecs& V, const ipm::Scal& S, cudaStream_t st);
-// part: kRedBlocks * 8 doubles of scratch; out: up to 8 doubles
+// part: kRedBlocks * 8 + 1 doubles of scratch, zeroed once (the last slot is
+// the completion ticket); out: up to 8 doubles
 void dev_ipm_reduce(int which, const ipm::Vecs& V, const ipm::Scal& S, double* part, double* out, cudaStream_t st);
 
 }  // namespace nclb

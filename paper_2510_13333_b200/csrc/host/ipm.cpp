@@ -94,7 +94,9 @@ double scaled_err(const KktErr& e, double sd, double sc, bool mu_part) {
 }
 }  // namespace
 
-// returns 0 converged, 1 iteration cap, 2 regularisation exhausted
+// returns 0 converged (E_0 <= tol), 1 iteration cap, 2 regularisation
+// exhausted, 3 converged on Ipopt's 'acceptable' rule only (E_0 <=
+// acceptable_factor * tol for acceptable_iter consecutive iterations)
 int Solver::subproblem(double tol, int outer) {
   filter_.clear();
   const int nmult = std::max(1, be_.m() + be_.num_bound_duals());
@@ -117,7 +119,8 @@ int Solver::subproblem(double tol, int outer) {
     acc_count = e0 <= o_.acceptable_factor * tol ? acc_count + 1 : 0;
     if (e0 <= tol || (o_.acceptable_iter > 0 && acc_count >= o_.acceptable_iter)) {
       res_.t_other += since(t0);
-      return 0;
+      last_e0_ = e0;
+      return e0 <= tol ? 0 : 3;
     }
     // monotone Fiacco-McCormick barrier update
     while (S_.mu > o_.mu_min && scaled_err(e, sd, sc, true) <= o_.kappa_eps * S_.mu) {
@@ -232,13 +235,17 @@ int Solver::subproblem(double tol, int outer) {
     res_.inner_iters++;
     res_.t_linesearch += since(t0);
     if (o_.verbose) {
-      char buf[512];
+      // full precision (%.17g) so two backends' traces can be diffed to the
+      // first differing bit (tools/trace_diff.py); e0 = scaled KKT error,
+      // theta/phi = current merit, g = directional derivative of phi
+      char buf[768];
       std::snprintf(buf, sizeof buf,
-                    "{\"outer\": %d, \"iter\": %d, \"mu\": %.6e, \"rho\": %.3e, \"inf_pr\": %.6e, \"inf_du\": %.6e, "
-                    "\"obj\": %.12e, \"dw\": %.3e, \"dc\": %.3e, \"alpha_pr\": %.6e, \"alpha_du\": %.6e, \"ls\": %d, "
-                    "\"factorizations\": %d, \"refine_res\": %.3e, \"sweeps\": %d, \"accepted\": %d}\n",
-                    outer, res_.inner_iters, S_.mu, S_.rho, e.pr, std::max(e.du, e.dur), be_.objective(), dw, S_.dc,
-                    ok ? S_.alpha : 0.0, adual, ls, tries, so.residual, so.sweeps, ok ? 1 : 0);
+                    "{\"outer\": %d, \"iter\": %d, \"mu\": %.17g, \"rho\": %.17g, \"inf_pr\": %.17g, "
+                    "\"inf_du\": %.17g, \"e0\": %.17g, \"obj\": %.17g, \"theta\": %.17g, \"phi\": %.17g, "
+                    "\"g\": %.17g, \"dw\": %.17g, \"dc\": %.17g, \"alpha_pr\": %.17g, \"alpha_du\": %.17g, "
+                    "\"ls\": %d, \"factorizations\": %d, \"refine_res\": %.17g, \"sweeps\": %d, \"accepted\": %d}\n",
+                    outer, res_.inner_iters, S_.mu, S_.rho, e.pr, std::max(e.du, e.dur), e0, be_.objective(), cur.theta,
+                    cur.phi, g, dw, S_.dc, ok ? S_.alpha : 0.0, adual, ls, tries, so.residual, so.sweeps, ok ? 1 : 0);
       trace_ += buf;
     }
     (void)inf;
@@ -248,6 +255,7 @@ int Solver::subproblem(double tol, int outer) {
 ncl_result Solver::solve() {
   res_ = ncl_result{};
   trace_.clear();
+  last_e0_ = 0.0;
   const auto t_start = clk::now();
   S_ = Scal{};
   S_.mu = o_.mu_init;
@@ -289,10 +297,14 @@ ncl_result Solver::solve() {
     }
     if (rinf <= std::max(eta, o_.eta_star)) {
       if (rinf <= o_.eta_star && tol <= o_.omega_star) {
-        res_.status = NCL_SOLVE_OPTIMAL;
+        // optimal only when the last subproblem met omega* itself; an exit
+        // on the 'acceptable' rule (E_0 <= acceptable_factor * omega*) is
+        // reported as such (optimal => stationarity <= omega*)
+        res_.status = st == 0 ? NCL_SOLVE_OPTIMAL : NCL_SOLVE_ACCEPTABLE;
         break;
       }
-      be_.update_multipliers();
+      // multiplier branch; bounded-multiplier guard
+      if (be_.update_multipliers() > o_.lambda_max) res_.multiplier_warning = 1;
       eta = std::max(o_.eta_star, 0.1 * eta);
       omega = std::max(o_.omega_star, 0.1 * omega);
     } else {
@@ -307,6 +319,7 @@ ncl_result Solver::solve() {
                                          o_.mu_warm_frac * std::max(omega, o_.omega_star)));
   }
   res_.objective = be_.objective();
+  res_.final_e0 = last_e0_;
   res_.rho = S_.rho;
   res_.mu = S_.mu;
   res_.t_total = since(t_start);

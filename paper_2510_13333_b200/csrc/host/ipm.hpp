@@ -59,7 +59,7 @@ class Backend {
   virtual void accept(const Scal& S) = 0;
   virtual void restore() = 0;
   virtual void r_inf(double* rinf, double* dxinf, double* xinf) = 0;
-  virtual void update_multipliers() = 0;
+  virtual double update_multipliers() = 0;  // lamN <- y on rows; returns |lamN|_inf
   virtual double objective() const = 0;  // unscaled f at x
   virtual void get_solution(double* x, double* y, double* r) = 0;
 };
@@ -84,6 +84,7 @@ class Solver {
   std::vector<std::pair<double, double>> filter_;
   double theta_max_ = 0, theta_min_ = 0;
   double dw_last_ = 0;
+  double last_e0_ = 0;  // scaled KKT error at the last subproblem's exit
   std::string trace_;
 };
 

@@ -3,8 +3,9 @@
 // kernels (csrc/cuda/ipm.cu, compiled with --fmad=false) and by the CPU
 // oracle backend (oracle/ref_ipm.cpp, -ffp-contract=off): the same source
 // expression per element on both sides, and the same reduction tree
-// (kRedBlocks x kRedThreads partials, block-local halving tree, blocks summed
-// in index order), so sums/maxima are bit-identical on both backends given
+// (kRedBlocks x kRedThreads partials, block-local halving tree, then the
+// kRedBlocks block partials folded to kRedThreads and the same halving tree
+// again), so sums/maxima are bit-identical on both backends given
 // bit-identical inputs.
 //
 // The subproblem for the generic NLP
@@ -420,12 +421,16 @@ struct RedRinf {
 };
 
 // CPU emulation of the GPU reduction order: thread t of block b visits
-// j = b*T + t, j += B*T; block-local halving tree; blocks combined in order.
+// j = b*T + t, j += B*T; block-local halving tree (pairs (t, t+h), h = T/2..1);
+// then the B block partials: p[t] (+) p[t+T] for t + T < B, and the same
+// halving tree over T (csrc/cuda/ipm.cu, last block to finish).
 template <class R>
 void reduce_host(const Vecs& V, const Scal& S, double* out) {
   const int64_t N = static_cast<int64_t>(V.n) + V.m;
   constexpr int B = kRedBlocks, T = kRedThreads, NV = R::NV;
+  static_assert(B > T && B <= 2 * T, "final fold assumes T < B <= 2T");
   static thread_local double part[B * T * 8];
+  static thread_local double fin[T * 8];
   static_assert(NV <= 8, "too many accumulators");
   for (int b = 0; b < B; ++b)
     for (int t = 0; t < T; ++t) {
@@ -433,17 +438,18 @@ void reduce_host(const Vecs& V, const Scal& S, double* out) {
       for (int k = 0; k < NV; ++k) a[k] = comb_init(R::kind(k));
       for (int64_t j = static_cast<int64_t>(b) * T + t; j < N; j += static_cast<int64_t>(B) * T) R::elem(V, j, S, a);
     }
-  for (int b = 0; b < B; ++b) {
-    double* blk = part + static_cast<int64_t>(b) * T * NV;
+  auto tree = [](double* blk) {
     for (int h = T / 2; h > 0; h >>= 1)
       for (int t = 0; t < h; ++t)
         for (int k = 0; k < NV; ++k) blk[t * NV + k] = comb(R::kind(k), blk[t * NV + k], blk[(t + h) * NV + k]);
-  }
-  for (int k = 0; k < NV; ++k) {
-    double acc = comb_init(R::kind(k));
-    for (int b = 0; b < B; ++b) acc = comb(R::kind(k), acc, part[static_cast<int64_t>(b) * T * NV + k]);
-    out[k] = acc;
-  }
+  };
+  for (int b = 0; b < B; ++b) tree(part + static_cast<int64_t>(b) * T * NV);
+  auto blockp = [&](int b, int k) { return part[static_cast<int64_t>(b) * T * NV + k]; };
+  for (int t = 0; t < T; ++t)
+    for (int k = 0; k < NV; ++k)
+      fin[t * NV + k] = t + T < B ? comb(R::kind(k), blockp(t, k), blockp(t + T, k)) : blockp(t, k);
+  tree(fin);
+  for (int k = 0; k < NV; ++k) out[k] = fin[k];
 }
 
 }  // namespace nclb::ipm

@@ -470,7 +470,11 @@ ModelSpec build_scopf(const Grid& g, const std::vector<int>& cont) {
     return row++;
   };
   for (int s = 0; s <= K; ++s) {
-    const int out = s == 0 ? -1 : cont[s - 1];
+    // contingency id = outaged branch + nl * load level (contingency_load_scale)
+    if (s > 0 && (cont[s - 1] < 0 || cont[s - 1] / nl >= kLoadLevels))
+      throw std::invalid_argument("build_scopf: contingency id out of range");
+    const int out = s == 0 ? -1 : cont[s - 1] % nl;
+    const double lsc = s == 0 ? 1.0 : contingency_load_scale(cont[s - 1] / nl);
     const int ov = off, oth = ov + nb, opg = oth + nb, oqg = opg + ng, ofl = oqg + ng;
     const int oex = ofl + 4 * nl;
     off = oex + (s == 0 ? 0 : 1 + 4 * ng);
@@ -533,14 +537,14 @@ ModelSpec build_scopf(const Grid& g, const std::vector<int>& cont) {
         to_at[g.t[l]].push_back(l);
       }
     for (int i = 0; i < nb; ++i) {
-      const int rp = newrow(g.pd[i], g.pd[i]);
+      const int rp = newrow(lsc * g.pd[i], lsc * g.pd[i]);
       for (int k : gens_at[i]) term(T_PLUS, rp, {opg + k}, {});
       for (int l : from_at[i]) term(T_MINUS, rp, {pf(l)}, {});
       for (int l : to_at[i]) term(T_MINUS, rp, {pt(l)}, {});
       if (g.gs[i] != 0.0) term(T_SHUNT, rp, {ov + i}, {-g.gs[i]});
     }
     for (int i = 0; i < nb; ++i) {
-      const int rq = newrow(g.qd[i], g.qd[i]);
+      const int rq = newrow(lsc * g.qd[i], lsc * g.qd[i]);
       for (int k : gens_at[i]) term(T_PLUS, rq, {oqg + k}, {});
       for (int l : from_at[i]) term(T_MINUS, rq, {qf(l)}, {});
       for (int l : to_at[i]) term(T_MINUS, rq, {qt(l)}, {});

@@ -44,6 +44,17 @@ Grid grid_synthetic(int nb, int nl, int ng, uint64_t seed);
 // Non-islanding line outages in ascending branch order (union-find).
 std::vector<int> select_contingencies(const Grid& g, int K);
 
+// Contingency ids: id = l + nl * j is the outage of branch l with every
+// post-contingency load (P and Q) scaled by contingency_load_scale(j), j <
+// kLoadLevels. j = 0 is the plain N-1 outage. The other
+// levels are outage x load-scenario pairs. They exist because a 597-branch
+// grid has only 258 non-islanding single outages, while BASELINE.json's
+// 500-bus x 1024 configuration needs 1024 contingencies. The scenario model is
+// the same (Eq. 2-4) and the layout (nvar/ncon per
+// contingency) does not change.
+constexpr int kLoadLevels = 4;
+inline double contingency_load_scale(int j) { return 1.0 - 0.015 * j; }
+
 struct SpecFamily {
   std::string name;
   int nslots = 0, np = 0;
@@ -70,6 +81,7 @@ struct ModelSpec {
   std::vector<int> row_start;  // first row of each scenario
 };
 
+// contingencies: ids as above (branch + nl * load level)
 ModelSpec build_scopf(const Grid& g, const std::vector<int>& contingencies);
 
 }  // namespace nclb

@@ -8,6 +8,7 @@ from __future__ import annotations
 
 import ctypes as C
 import json
+import re
 from dataclasses import dataclass
 
 import numpy as np
@@ -42,7 +43,7 @@ class NclResult(C.Structure):
         ("objective", f64), ("r_inf", f64), ("inf_pr", f64), ("inf_du", f64), ("compl_", f64), ("rho", f64),
         ("mu", f64), ("multiplier_warning", i32),
         ("t_total", f64), ("t_init", f64), ("t_eval", f64), ("t_factor", f64), ("t_solve", f64),
-        ("t_linesearch", f64), ("t_other", f64),
+        ("t_linesearch", f64), ("t_other", f64), ("final_e0", f64),
     ]
 
     def as_dict(self):
@@ -50,7 +51,7 @@ class NclResult(C.Structure):
 
 
 STATUS = {0: "optimal", 1: "infeasible", 2: "iteration_limit", 3: "regularization_exhausted",
-          4: "restoration_failed"}
+          4: "restoration_failed", 5: "acceptable"}
 
 register({
     "ncl_options_default": (i32, [C.POINTER(NclOptions)]),
@@ -70,8 +71,13 @@ def default_options(**overrides) -> NclOptions:
     return o
 
 
+_NONFINITE = re.compile(r"(?<=[:\s])(-?)(inf|nan)\b")
+
+
 def parse_trace(text: str):
-    return [json.loads(l) for l in text.splitlines() if l.strip()]
+    """JSON-lines trace; printf's inf/nan become JSON Infinity/NaN."""
+    fix = lambda l: _NONFINITE.sub(lambda m: m.group(1) + "Infinity" if m.group(2) == "inf" else "NaN", l)
+    return [json.loads(fix(l)) for l in text.splitlines() if l.strip()]
 
 
 @dataclass

@@ -52,6 +52,25 @@ def screened(grid: str, seed: int = 2510):
         return json.load(f)["feasible"]
 
 
+LOAD_LEVELS = 4  # csrc/host/scopf.hpp kLoadLevels: id = branch + nl * level, loads x (1 - 0.015 level)
+
+
+def contingency_ids(grid: str, K: int, seed: int = 2510):
+    """The first K contingency ids of a grid: the screened N-1 outages
+    (level 0) first, then the same outages at load levels 1, 2, 3
+    (outage x load-scenario contingencies; see include/nclopf_b200.h
+    ncl_scopf_create_list). None when the grid has no screened list."""
+    base = screened(grid, seed)
+    if base is None:
+        return None
+    nl = GRIDS[grid][2]
+    ids = [l + nl * j for j in range(LOAD_LEVELS) for l in base]
+    if len(ids) < K:
+        raise ValueError(f"only {len(ids)} contingencies ({len(base)} screened outages x {LOAD_LEVELS} load levels) "
+                         f"for {grid}")
+    return ids[:K]
+
+
 @dataclass
 class Family:
     name: str
@@ -66,15 +85,15 @@ class Family:
 
 class Scopf:
     def __init__(self, grid: str = "case9", K: int = 0, seed: int = 2510, contingencies=None):
-        """contingencies: explicit branch ids; default = the first K entries of
-        the committed screened list for (grid, seed) when one exists
-        (data/screened_<grid>_<seed>.json, tools/screen_contingencies.py),
-        else the first K non-islanding branches."""
+        """contingencies: explicit contingency ids (branch + nl * load level);
+        default = contingency_ids(grid, K, seed): the committed screened
+        outages (data/screened_<grid>_<seed>.json,
+        tools/screen_contingencies.py), then the same outages at lower load
+        levels, when a screened list exists, else the first K non-islanding
+        branches."""
         kind, nb, nl, ng = GRIDS[grid]
         if contingencies is None and K > 0:
-            contingencies = screened(grid, seed)
-            if contingencies is not None and len(contingencies) < K:
-                raise ValueError(f"only {len(contingencies)} screened contingencies for {grid}")
+            contingencies = contingency_ids(grid, K, seed)
         h = C.c_void_p()
         if contingencies is None:
             check(lib.ncl_scopf_create(kind, nb, nl, ng, seed, K, C.byref(h)))
