@@ -82,6 +82,23 @@ typedef struct ncl_result {
   double final_e0;      /* scaled KKT error E_0 at the last subproblem's exit */
 } ncl_result;
 
+/* One Newton step of the NCL subproblem at a caller-given interior state
+ * (assemble_newton + recover_directions; acceptance
+ * criterion 6). Host arrays: x, zl, zu (n), r, s, y, vl, vu,
+ * lamN (m); s is ignored (held at gl) on equality rows, bound duals of
+ * infinite bounds must be 0. */
+typedef struct ncl_ipm_state {
+  const double *x, *zl, *zu, *r, *s, *y, *vl, *vu, *lamN;
+  double mu, rho, sf, dw, dc;
+} ncl_ipm_state;
+/* outputs: dx, dzl, dzu (n), dr, ds, dy, dvl, dvu (m) — any may be NULL */
+typedef struct ncl_newton_step {
+  double *dx, *dzl, *dzu, *dr, *ds, *dy, *dvl, *dvu;
+  double residual;      /* solve_refined's final relative residual */
+  int sweeps, converged;
+  int status, npos, nneg, nzero;  /* factorization of the condensed K */
+} ncl_newton_step;
+
 /* ---- B200 solve (libnclopf_b200.so) -------------------------------------
  * ncl_solve over a ModelFunctions handle (nclopf_b200.h)
  * with variable bounds xl/xu, start x0 (n) and row bounds gl/gu (m; gl == gu
@@ -96,6 +113,11 @@ void ncl_solver_destroy(ncl_solver_t S);
 int ncl_solver_solve(ncl_solver_t S, const ncl_options* opt, ncl_result* res);
 /* final x (n), y (m), r (m); any may be NULL */
 int ncl_solver_solution(ncl_solver_t S, double* x, double* y, double* r);
+/* one Newton step (see ncl_ipm_state) at the given state; opt supplies
+ * pivot_tol / refine_target / refine_max_sweeps (NULL = defaults). Runs the
+ * same device path as an IPM iteration: eval -> newton -> K2 assembly -> K3
+ * factor -> K4 refined solve -> recovery. */
+int ncl_solver_newton_step(ncl_solver_t S, const ncl_ipm_state* st, const ncl_options* opt, ncl_newton_step* out);
 /* JSON-lines trace; *len = full size */
 int ncl_solver_trace(ncl_solver_t S, char* buf, int64_t cap, int64_t* len);
 

@@ -15,7 +15,10 @@ import subprocess
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB = os.path.join(HERE, "_ref", "libnclopf_ref.so")
+# NCL_REF_VARIANT=fma loads oracle/_ref_fma (the same reference sources built
+# with FMA contraction, oracle/Makefile) — used only by tools/oracle_solve.py
+_VARIANT = os.environ.get("NCL_REF_VARIANT", "")
+LIB = os.path.join(HERE, "_ref" + (f"_{_VARIANT}" if _VARIANT else ""), "libnclopf_ref.so")
 
 
 def build(force: bool = False) -> str:
@@ -23,7 +26,8 @@ def build(force: bool = False) -> str:
     if force or not os.path.exists(LIB):
         if not os.path.isdir("/root/reference/proj/src"):
             raise RuntimeError("oracle/_ref missing and /root/reference absent: cannot build the oracle here")
-        subprocess.run(["make", "-C", HERE, "-j8"], check=True, capture_output=True)
+        subprocess.run(["make", "-C", HERE, "-j8"] + ([f"VARIANT={_VARIANT}"] if _VARIANT else []), check=True,
+                       capture_output=True)
     return LIB
 
 
@@ -364,6 +368,30 @@ def ref_condensed_kkt(model: "RefModel", hess, jac, sig, dw, D) -> RefSparseSym:
     K = RefSparseSym.__new__(RefSparseSym)
     K.h, K.n = h, model.n
     return K
+
+
+def ref_newton_step(model: RefModel, bounds, state: dict, options=None) -> dict:
+    """One Newton step at `state` on the reference CPU backend (the oracle side
+    of ncl_solver_newton_step)."""
+    from paper_2510_13333_b200.ipm import NclOptions, NewtonStep, IpmState, alloc_step, pack_state
+
+    L = lib()
+    if not hasattr(L, "_ns_sig"):
+        L.ref_newton_step.restype = C.c_int
+        L.ref_newton_step.argtypes = [C.c_void_p] * 6 + [C.POINTER(IpmState), C.POINTER(NclOptions),
+                                                         C.POINTER(NewtonStep)]
+        L._ns_sig = True
+    if options is None:
+        options = NclOptions()
+        L.ref_ipm_default_options(C.byref(options))
+    arrs = [np.ascontiguousarray(bounds[k], np.float64) for k in ("xl", "xu", "x0", "gl", "gu")]
+    st, keep = pack_state(state, model.n, model.m)
+    out, res = alloc_step(model.n, model.m)
+    rc = L.ref_newton_step(model.h, *[_p(a) for a in arrs], C.byref(st), C.byref(options), C.byref(out))
+    if rc != 0:
+        raise RefError(rc, L.ref_ipm_last_error().decode())
+    del keep
+    return res | {k: getattr(out, k) for k in ("residual", "sweeps", "converged", "status", "npos", "nneg", "nzero")}
 
 
 def ref_ncl_solve(model: RefModel, bounds, perm=None, options=None, trace_cap=1 << 26):

@@ -216,6 +216,22 @@ class RefBackend final : public ipm::Backend {
     return a;
   }
   double objective() const override { return fcur_; }
+  void set_state(const ncl_ipm_state& st) override {
+    std::copy(st.x, st.x + n_, x_.begin()), std::copy(st.zl, st.zl + n_, zl_.begin());
+    std::copy(st.zu, st.zu + n_, zu_.begin());
+    std::copy(st.r, st.r + m_, r_.begin()), std::copy(st.s, st.s + m_, s_.begin());
+    std::copy(st.y, st.y + m_, y_.begin()), std::copy(st.vl, st.vl + m_, vl_.begin());
+    std::copy(st.vu, st.vu + m_, vu_.begin()), std::copy(st.lamN, st.lamN + m_, lamN_.begin());
+    fcur_ = M_.eval_objective(x_);
+    M_.eval_constraints(x_, c_);
+  }
+  void get_step(ncl_newton_step& o) override {
+    auto dn = [](double* h, const std::vector<double>& v) {
+      if (h) std::copy(v.begin(), v.end(), h);
+    };
+    dn(o.dx, dx_), dn(o.dzl, dzl_), dn(o.dzu, dzu_), dn(o.dr, dr_), dn(o.ds, ds_), dn(o.dy, dy_);
+    dn(o.dvl, dvl_), dn(o.dvu, dvu_);
+  }
   void get_solution(double* x, double* y, double* r) override {
     if (x) std::copy(x_.begin(), x_.end(), x);
     if (y) std::copy(y_.begin(), y_.end(), y);
@@ -275,6 +291,22 @@ REF_API int ref_ncl_solve(void* model, const double* xl, const double* xu, const
       std::memcpy(trace, t.data(), k);
       trace[k] = 0;
     }
+    return 0;
+  } catch (const std::exception& e) {
+    g_ipm_err = e.what();
+    return -5;
+  }
+}
+
+// one Newton step at a caller-given state (ncl_solver_newton_step on the
+// reference CPU backend)
+REF_API int ref_newton_step(void* model, const double* xl, const double* xu, const double* x0, const double* gl,
+                            const double* gu, const ncl_ipm_state* st, const ncl_options* opt, ncl_newton_step* out) {
+  try {
+    const auto& M = *static_cast<const nclopf::ModelFunctions*>(model);
+    RefBackend be(M, xl, xu, x0, gl, gu, nullptr);
+    const ncl_options o = opt ? *opt : ipm::default_options();
+    ipm::newton_step(be, *st, o, *out);
     return 0;
   } catch (const std::exception& e) {
     g_ipm_err = e.what();

@@ -214,6 +214,25 @@ class GpuBackend final : public ipm::Backend {
     return hsc_[2];
   }
   double objective() const override { return fcur_; }
+  void set_state(const ncl_ipm_state& st) override {
+    auto up = [&](double* d, const double* h, int64_t cnt) {
+      if (cnt) ck(cudaMemcpyAsync(d, h, cnt * sizeof(double), cudaMemcpyHostToDevice, g_stream), "H2D");
+    };
+    up(V_.x, st.x, n_), up(V_.zl, st.zl, n_), up(V_.zu, st.zu, n_);
+    up(V_.r, st.r, m_), up(V_.s, st.s, m_), up(V_.y, st.y, m_), up(V_.vl, st.vl, m_), up(V_.vu, st.vu, m_);
+    up(V_.lamN, st.lamN, m_);
+    chk(ncl_model_eval_values_device(M_, V_.x, dsc_, V_.c));
+    fetch(0, 1);
+    fcur_ = hsc_[0];
+  }
+  void get_step(ncl_newton_step& o) override {
+    auto dn = [&](double* h, const double* d, int64_t cnt) {
+      if (h && cnt) ck(cudaMemcpyAsync(h, d, cnt * sizeof(double), cudaMemcpyDeviceToHost, g_stream), "D2H");
+    };
+    dn(o.dx, V_.dx, n_), dn(o.dzl, V_.dzl, n_), dn(o.dzu, V_.dzu, n_);
+    dn(o.dr, V_.dr, m_), dn(o.ds, V_.ds, m_), dn(o.dy, V_.dy, m_), dn(o.dvl, V_.dvl, m_), dn(o.dvu, V_.dvu, m_);
+    ck(cudaStreamSynchronize(g_stream), "sync");
+  }
   void get_solution(double* x, double* y, double* r) override {
     auto dn = [&](double* h, const double* d, int64_t cnt) {
       if (h && cnt) ck(cudaMemcpyAsync(h, d, cnt * sizeof(double), cudaMemcpyDeviceToHost, g_stream), "D2H");
@@ -280,6 +299,13 @@ API int ncl_solver_solve(ncl_solver_t S, const ncl_options* opt, ncl_result* res
     S->last = sol.solve();
     S->trace = sol.trace();
     *res = S->last;
+  });
+}
+API int ncl_solver_newton_step(ncl_solver_t S, const ncl_ipm_state* st, const ncl_options* opt,
+                               ncl_newton_step* out) {
+  GUARD({
+    const ncl_options o = opt ? *opt : ipm::default_options();
+    ipm::newton_step(*S->be, *st, o, *out);
   });
 }
 API int ncl_solver_solution(ncl_solver_t S, double* x, double* y, double* r) { GUARD(S->be->get_solution(x, y, r)); }

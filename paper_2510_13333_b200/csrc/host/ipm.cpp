@@ -326,4 +326,35 @@ ncl_result Solver::solve() {
   return res_;
 }
 
+void newton_step(Backend& be, const ncl_ipm_state& st, const ncl_options& o, ncl_newton_step& out) {
+  Scal S;
+  S.mu = st.mu;
+  S.rho = st.rho;
+  S.sf = st.sf;
+  S.kappa_sigma = o.kappa_sigma;
+  S.push = o.bound_push;
+  S.frac = o.bound_frac;
+  double f0 = 0, gmax = 0;
+  be.init_point(S, &f0, &gmax);
+  be.set_state(st);
+  be.eval_derivatives(S.sf);
+  S.dc = st.dc;
+  be.form_newton(S);
+  const FactorOut f = be.factor(st.dw, o.pivot_tol);
+  out.status = f.status;
+  out.npos = f.npos;
+  out.nneg = f.nneg;
+  out.nzero = f.nzero;
+  out.residual = 0;
+  out.sweeps = 0;
+  out.converged = 0;
+  if (f.status == 0) {
+    const SolveOut so = be.solve(S, o.refine_target, o.refine_max_sweeps);
+    out.residual = so.residual;
+    out.sweeps = so.sweeps;
+    out.converged = so.converged ? 1 : 0;
+    be.get_step(out);
+  }
+}
+
 }  // namespace nclb::ipm

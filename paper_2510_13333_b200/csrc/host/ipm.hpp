@@ -62,7 +62,17 @@ class Backend {
   virtual double update_multipliers() = 0;  // lamN <- y on rows; returns |lamN|_inf
   virtual double objective() const = 0;  // unscaled f at x
   virtual void get_solution(double* x, double* y, double* r) = 0;
+  // newton_step() only: overwrite the primal-dual state (then f, c at x are
+  // re-evaluated) and read the last step back
+  virtual void set_state(const ncl_ipm_state& st) = 0;
+  virtual void get_step(ncl_newton_step& out) = 0;
 };
+
+// One Newton step at a caller-given state (ncl_solver_newton_step): the
+// symbolic analysis (init_point), then exactly the per-iteration sequence of
+// Solver::subproblem — eval_derivatives, form_newton, factor, solve (with
+// recovery) — without inertia correction.
+void newton_step(Backend& be, const ncl_ipm_state& st, const ncl_options& o, ncl_newton_step& out);
 
 class Solver {
  public:

@@ -50,6 +50,42 @@ class NclResult(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class IpmState(C.Structure):
+    """ncl_ipm_state: a primal-dual point of the NCL subproblem (host arrays)."""
+    _fields_ = [(k, C.c_void_p) for k in ("x", "zl", "zu", "r", "s", "y", "vl", "vu", "lamN")] + [
+        (k, f64) for k in ("mu", "rho", "sf", "dw", "dc")]
+
+
+class NewtonStep(C.Structure):
+    """ncl_newton_step: the recovered Newton direction + solve/factor report."""
+    _fields_ = [(k, C.c_void_p) for k in ("dx", "dzl", "dzu", "dr", "ds", "dy", "dvl", "dvu")] + [
+        ("residual", f64), ("sweeps", i32), ("converged", i32), ("status", i32), ("npos", i32), ("nneg", i32),
+        ("nzero", i32)]
+
+
+STEP_X = ("dx", "dzl", "dzu")
+STEP_ROW = ("dr", "ds", "dy", "dvl", "dvu")
+
+
+def pack_state(state: dict, n: int, m: int):
+    """(IpmState, keep-alive arrays) from a dict with x, zl, zu (n), r, s, y,
+    vl, vu, lamN (m) and scalars mu, rho, sf, dw, dc."""
+    keep = {k: _f64(state[k]) for k in ("x", "zl", "zu", "r", "s", "y", "vl", "vu", "lamN")}
+    for k in ("x", "zl", "zu"):
+        assert keep[k].shape == (n,), k
+    for k in ("r", "s", "y", "vl", "vu", "lamN"):
+        assert keep[k].shape == (m,), k
+    st = IpmState(**{k: keep[k].ctypes.data for k in keep},
+                  **{k: float(state.get(k, d)) for k, d in (("mu", 0.1), ("rho", 100.0), ("sf", 1.0),
+                                                             ("dw", 0.0), ("dc", 0.0))})
+    return st, keep
+
+
+def alloc_step(n: int, m: int):
+    arrs = {k: np.zeros(n) for k in STEP_X} | {k: np.zeros(m) for k in STEP_ROW}
+    return NewtonStep(**{k: a.ctypes.data for k, a in arrs.items()}), arrs
+
+
 STATUS = {0: "optimal", 1: "infeasible", 2: "iteration_limit", 3: "regularization_exhausted",
           4: "restoration_failed", 5: "acceptable"}
 
@@ -60,6 +96,7 @@ register({
     "ncl_solver_solve": (i32, [P, C.POINTER(NclOptions), C.POINTER(NclResult)]),
     "ncl_solver_solution": (i32, [P, P, P, P]),
     "ncl_solver_trace": (i32, [P, C.c_char_p, i64, C.POINTER(i64)]),
+    "ncl_solver_newton_step": (i32, [P, C.POINTER(IpmState), C.POINTER(NclOptions), C.POINTER(NewtonStep)]),
 })
 
 
@@ -120,6 +157,18 @@ class NclSolver:
         check(lib.ncl_solver_trace(self._h, buf, ln.value + 1, C.byref(ln)))
         d = res.as_dict()
         return SolveOutput(d, STATUS.get(res.status, str(res.status)), x, y, r, parse_trace(buf.value.decode()))
+
+
+    def newton_step(self, state: dict, options: NclOptions | None = None) -> dict:
+        """One Newton step at `state` (ncl_solver_newton_step): the recovered
+        direction dx, dzl, dzu, dr, ds, dy, dvl, dvu plus the factor/solve report."""
+        o = options if options is not None else default_options()
+        st, keep = pack_state(state, self.n, self.m)
+        out, arrs = alloc_step(self.n, self.m)
+        check(lib.ncl_solver_newton_step(self._h, C.byref(st), C.byref(o), C.byref(out)))
+        del keep
+        return arrs | {k: getattr(out, k) for k in ("residual", "sweeps", "converged", "status", "npos", "nneg",
+                                                     "nzero")}
 
 
 def solve_scopf(scopf, options: NclOptions | None = None) -> SolveOutput:
