@@ -6,9 +6,11 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <sstream>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/nclopf_b200.h"
@@ -352,10 +354,24 @@ API int ncl_sym_write_matrix_market(ncl_sym_t M, char* buf, int64_t cap, int64_t
 // ---------------------------------------------------------------------------
 // Symbolic analysis
 // ---------------------------------------------------------------------------
+// device copy of one TaskLayout
+struct LayoutDev {
+  DevBuf<int> nodes, tptr, prog, bamap;
+  DevBuf<uint8_t> bcmap;
+  DevBuf<uint32_t> bcmapw;
+  DevBuf<int64_t> bccb;
+  DevBuf<int> bcid;
+  DevBuf<RegChunk> bchunks;
+  DevBuf<RegInst> binst;
+  DevBuf<int64_t> gpo;
+  std::vector<DevBuf<BigDesc>> top;
+};
+
 struct ncl_symb {
   SymbolicCore core;
   Supernodal Z;
-  TaskLayout lay;  // default task layout (subtree groups + singles) and its level schedule
+  TaskLayout lay;   // default task layout (subtree groups + singles) and its level schedule (solves)
+  TaskLayout flay;  // the same list with its batched subtrees split off (factor)
   uint64_t hash = 0;
   int nnz = 0;
   DevSymb d;
@@ -365,23 +381,142 @@ struct ncl_symb {
   DevBuf<uint8_t> big;
   DevBuf<int> lay_nodes, lay_tptr, lay_prog;
   DevBuf<int64_t> lay_gpo;
+  LayoutDev fdev;  // device copy of flay
+  DevBuf<int> aoffp;
   DevBuf<SnMeta> meta;
+  DevBuf<ChildRec> chrec;
   std::vector<DevBuf<BigDesc>> top_dev;
   bool dev_ready = false;
 };
 
 namespace {
+void build_batches(const Supernodal& Z, const std::vector<int>& list, int split, const std::vector<uint8_t>& inlist,
+                   std::vector<uint8_t>& batched, BatchSched& B) {
+  const int nsn = Z.nsn;
+  auto wof = [&](int s) { return Z.sn_first[s + 1] - Z.sn_first[s]; };
+  auto nrof = [&](int s) { return static_cast<int>(Z.sn_rptr[s + 1] - Z.sn_rptr[s]); };
+  auto shape_of = [&](int s) {
+    for (int k = 0; k < kNumRegShapes; ++k)
+      if (kRegShapes[k][0] == nrof(s) && kRegShapes[k][1] == wof(s)) return k;  // first match
+    return -1;
+  };
+  // levels of the register-front forest (list order: children before
+  // parents); tier 1 (shapes < kRegTier1) is closed under children on its own
+  std::vector<int> lev(nsn, -1), shp(nsn, -1), tier(nsn, 0);
+  int nlev = 0;
+  for (int i = 0; i < split; ++i) {
+    const int s = list[i], k = shape_of(s);
+    if (k < 0) continue;
+    int l = 0, t = k < kRegTier1 ? 1 : 2;
+    bool ok = true;
+    for (int q = Z.cptr[s]; q < Z.cptr[s + 1] && ok; ++q) {
+      const int c = Z.child[q];
+      if (!inlist[c]) continue;  // finished by an earlier phase (sharded lists): its standard CB
+      if (lev[c] < 0) ok = false;
+      else l = std::max(l, lev[c] + 1), t = std::max(t, tier[c]);
+    }
+    if (ok) lev[s] = l, shp[s] = k, tier[s] = t, nlev = std::max(nlev, l + 1);
+  }
+  std::vector<std::vector<std::vector<int>>> bucket(2 * nlev, std::vector<std::vector<int>>(kNumRegShapes));
+  for (int i = 0; i < split; ++i)
+    if (lev[list[i]] >= 0) bucket[(tier[list[i]] - 1) * nlev + lev[list[i]]][shp[list[i]]].push_back(list[i]);
+  nlev *= 2;
+  for (int l = 0; l < nlev; ++l) {
+    for (int k = 0; k < kNumRegShapes; ++k) {
+      auto& v = bucket[l][k];
+      if (v.empty()) continue;
+      // same child count next to each other: the child loop stays converged
+      std::stable_sort(v.begin(), v.end(),
+                       [&](int x, int y) { return Z.cptr[x + 1] - Z.cptr[x] < Z.cptr[y + 1] - Z.cptr[y]; });
+      const int nr = kRegShapes[k][0], per = 32 / kRegShapes[k][2];
+      const int np = nr * (nr + 1) / 2, npad = (np + 3) & ~3;
+      const int R = kRegShapes[k][2], nw = npad / 4;
+      for (size_t x = 0; x < v.size(); x += per)
+        B.chunks.push_back(RegChunk{k, static_cast<int>(std::min<size_t>(per, v.size() - x)),
+                                    static_cast<int>(B.inst.size() + x), 0});
+      int64_t abase = 0, wbase = 0;  // R == 1: per-chunk blocks interleaved over the 32 lanes
+      for (size_t x = 0; x < v.size(); ++x) {
+        const int s = v[x];
+        const int ix = static_cast<int>(x % 32);
+        if (R == 1 && ix == 0) {
+          int maxnch = 0;
+          for (size_t y = x; y < std::min(v.size(), x + 32); ++y) maxnch = std::max(maxnch, Z.cptr[v[y] + 1] - Z.cptr[v[y]]);
+          abase = static_cast<int64_t>(B.amap.size());
+          B.amap.resize(B.amap.size() + static_cast<size_t>(np) * 32, -1);
+          wbase = static_cast<int64_t>(B.cmapw.size());
+          B.cmapw.resize(B.cmapw.size() + static_cast<size_t>(maxnch) * nw * 32, 0xffffffffu);
+        }
+        batched[s] = 1;
+        RegInst I{};
+        I.loff = Z.sn_loff[s];
+        I.cboff = Z.cb_off[s];
+        I.s = s;
+        I.f = Z.sn_first[s];
+        I.nch = Z.cptr[s + 1] - Z.cptr[s];
+        I.shape = k;
+        const int64_t ast = R == 1 ? 32 : 1;  // A-map stride
+        if (R == 1) {
+          I.amap = abase + ix;
+          I.cmap = wbase + ix;
+        } else {
+          I.amap = static_cast<int64_t>(B.amap.size());
+          B.amap.resize(B.amap.size() + np, -1);
+          I.cmap = static_cast<int64_t>(B.cmap.size());
+        }
+        for (int64_t e = Z.a_ptr[s]; e < Z.a_ptr[s + 1]; ++e)
+          B.amap[I.amap + ast * (cb_col(Z.a_off[e] / nr, nr) + Z.a_off[e] % nr)] = Z.a_src[e];
+        I.ccb = static_cast<int64_t>(B.ccb.size());
+        for (int q = Z.cptr[s]; q < Z.cptr[s + 1]; ++q) {
+          const int c = Z.child[q], qi = q - Z.cptr[s];
+          const int m2c = nrof(c) - wof(c);
+          const int* rel = Z.relp.data() + Z.sn_rptr[c] + wof(c);
+          if (R == 1) {
+            for (int j = 0; j < m2c; ++j)
+              for (int ii = j; ii < m2c; ++ii) {
+                const int64_t pp = cb_col(rel[j], nr) + rel[ii];
+                uint32_t& wd = B.cmapw[I.cmap + (static_cast<int64_t>(qi) * nw + pp / 4) * 32];
+                wd = (wd & ~(0xffu << (8 * (pp % 4)))) | (static_cast<uint32_t>(cb_col(j, m2c) + ii) << (8 * (pp % 4)));
+              }
+          } else {
+            const size_t base = B.cmap.size();
+            B.cmap.resize(base + npad, 255);
+            for (int j = 0; j < m2c; ++j)
+              for (int ii = j; ii < m2c; ++ii)
+                B.cmap[base + cb_col(rel[j], nr) + rel[ii]] = static_cast<uint8_t>(cb_col(j, m2c) + ii);
+          }
+          B.ccb.push_back(Z.cb_off[c]);
+          B.cid.push_back(c);
+          if (qi < 4) I.cid[qi] = c, I.cb[qi] = Z.cb_off[c];
+        }
+        B.inst.push_back(I);
+        B.nodes++;
+      }
+    }
+    if (l == nlev / 2 - 1) B.nchunk1 = static_cast<int>(B.chunks.size());
+  }
+}
+
 // Task layout of a list (leaves-first height order, CTA part from `split`):
 // every warp-part supernode whose subtree has <= kGroup supernodes and whose
 // parent does not qualify roots a GROUP task (its subtree in postorder,
 // processed by one warp without scheduling between nodes); the remaining
 // warp-part supernodes and the CTA part are single-node tasks. Order: groups
 // (dependency-free), warp singles by height, CTA singles by height.
-TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int split) {
+//
+// With `batch`, warp-part supernodes of the register-front shapes
+// (kRegShapes) whose children in the list are such fronts too are factored
+// level by level, one thread per front (BatchSched), and leave the group /
+// single tasks.
+void build_batches(const Supernodal& Z, const std::vector<int>& list, int split, const std::vector<uint8_t>& inlist,
+                   std::vector<uint8_t>& batched, BatchSched& B);
+
+TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int split, bool batch = false) {
   const int nsn = Z.nsn;
   TaskLayout L;
-  std::vector<uint8_t> warp(nsn, 0);
+  std::vector<uint8_t> warp(nsn, 0), inlist(nsn, 0), batched(nsn, 0);
   for (int i = 0; i < split; ++i) warp[list[i]] = 1;
+  for (int s : list) inlist[s] = 1;
+  if (batch) build_batches(Z, list, split, inlist, batched, L.batch);
   // Groups are maximal warp-part subtrees whose whole multifrontal working
   // set fits one warp's shared memory: every front nr <= kGrpFront, the
   // program (records + relative maps + A entries) <= kGrpProg ints, the A
@@ -396,10 +531,17 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
   std::vector<int64_t> prog(nsn, 0), na(nsn, 0), stk(nsn, 0);
   for (int i = 0; i < split; ++i) {
     const int s = list[i];
-    bool ok = nrof(s) <= kGrpFront;
+    // batched (register-front) nodes are never grouped; a group reads their
+    // CBs as EXTERNAL children from the standard CB layout (they finished in
+    // an earlier launch)
+    bool ok = nrof(s) <= kGrpFront && !batched[s];
     int64_t pr = 14 + 2 * (Z.a_ptr[s + 1] - Z.a_ptr[s]), a = Z.a_ptr[s + 1] - Z.a_ptr[s], pk = 0, run = 0;
     for (int q = Z.cptr[s]; q < Z.cptr[s + 1]; ++q) {
       const int c = Z.child[q];
+      if (batched[c]) {
+        pr += 4 + (nrof(c) - wof(c));
+        continue;
+      }
       ok = ok && fits[c];
       pr += prog[c] + 2 + (nrof(c) - wof(c));
       a += na[c];
@@ -426,7 +568,7 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
       auto& top = st.back();
       if (top.second < Z.cptr[top.first + 1]) {
         const int c = Z.child[top.second++];
-        st.emplace_back(c, Z.cptr[c]);
+        if (!batched[c]) st.emplace_back(c, Z.cptr[c]);  // external children are not group members
       } else {
         post.push_back(top.first);
         st.pop_back();
@@ -436,7 +578,8 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
     L.tptr.push_back(static_cast<int>(L.nodes.size()));
     // program: [nnodes, nA, tab, len] [aoff x nA] [asrc x nA] then per node
     // [s, f, w, nr, nch, push_off(-1 = root), a_first, a_cnt, loff lo/hi, cboff lo/hi, rptr lo/hi] and per child
-    // [m2c, stack_off, rel x m2c], then the record offsets [tab .. tab + nnodes);
+    // [m2c, stack_off, rel x m2c] ([m2c, -1, cboff lo/hi, rel x m2c] for an external child),
+    // then the record offsets [tab .. tab + nnodes);
     // stack offsets from a postorder simulation
     const size_t base = L.prog.size();
     const int nA = static_cast<int>(na[r]);
@@ -454,7 +597,8 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
         L.prog[aoff0 + nA + afirst + e] = Z.a_src[Z.a_ptr[s] + e];
       }
       int pop = 0;
-      for (int q = Z.cptr[s]; q < Z.cptr[s + 1]; ++q) pop += static_cast<int>(cbof(Z.child[q]));
+      for (int q = Z.cptr[s]; q < Z.cptr[s + 1]; ++q)
+        if (!batched[Z.child[q]]) pop += static_cast<int>(cbof(Z.child[q]));
       const int push = s == r ? -1 : top - pop;
       const int64_t lo = Z.sn_loff[s], cbo = Z.cb_off[s], rp = Z.sn_rptr[s];
       rec_off.push_back(static_cast<int>(L.prog.size() - base));
@@ -466,7 +610,13 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
         const int c = Z.child[q];
         const int m2c = nrof(c) - wof(c);
         L.prog.push_back(m2c);
-        L.prog.push_back(cboff[c]);
+        if (batched[c]) {
+          L.prog.push_back(-1);
+          L.prog.push_back(static_cast<int>(Z.cb_off[c] & 0xffffffff));
+          L.prog.push_back(static_cast<int>(Z.cb_off[c] >> 32));
+        } else {
+          L.prog.push_back(cboff[c]);
+        }
         for (int k = 0; k < m2c; ++k) L.prog.push_back(Z.relp[Z.sn_rptr[c] + wof(c) + k]);
       }
       top -= pop;
@@ -485,7 +635,7 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
   std::vector<uint8_t> grouped(nsn, 0);
   for (int s : L.nodes) grouped[s] = 1;
   for (int i = 0; i < split; ++i)
-    if (!grouped[list[i]]) {
+    if (!grouped[list[i]] && !batched[list[i]]) {
       L.nodes.push_back(list[i]);
       L.tptr.push_back(static_cast<int>(L.nodes.size()));
     }
@@ -515,7 +665,7 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
         b.nr = nr;
         b.pw = 32;  // panel width: while a panel fits 220 KB of shared memory (a function of nr only)
         while (b.pw > 8 && static_cast<int64_t>(nr) * b.pw * 8 > 220 * 1024) b.pw /= 2;
-        b.npan = nr <= 160 ? 0 : (b.w + b.pw - 1) / b.pw;  // <= kCtaFront: one CTA (dev_big_cta)
+        b.npan = nr <= kCtaFront ? 0 : (b.w + b.pw - 1) / b.pw;  // one CTA (dev_big_cta)
         b.g0 = Z.gm_ptr[s];
         b.g1 = Z.gm_ptr[s + 1];
         // lanes per front entry in the assembly: ~4 sources per lane
@@ -573,6 +723,33 @@ void upload_top(TopSched& t, std::vector<DevBuf<BigDesc>>& store) {
     }
 }
 
+DevTasks upload_layout(TaskLayout& L, LayoutDev& D) {
+  upload_top(L.top, D.top);
+  D.nodes.upload(L.nodes);
+  D.tptr.upload(L.tptr);
+  D.prog.upload(L.prog);
+  D.gpo.upload(L.gpo);
+  const bool has_batch = !L.batch.inst.empty();
+  if (has_batch) {
+    D.binst.upload(L.batch.inst);
+    D.bamap.upload(L.batch.amap);
+    D.bcmap.upload(L.batch.cmap);
+    D.bcmapw.upload(L.batch.cmapw);
+    L.batch.dev_cmapw = D.bcmapw.p;
+    D.bccb.upload(L.batch.ccb);
+    D.bcid.upload(L.batch.cid);
+    D.bchunks.upload(L.batch.chunks);
+    L.batch.dev_cid = D.bcid.p;
+    L.batch.dev_chunks = D.bchunks.p;
+    L.batch.dev_inst = D.binst.p;
+    L.batch.dev_amap = D.bamap.p;
+    L.batch.dev_cmap = D.bcmap.p;
+    L.batch.dev_ccb = D.bccb.p;
+  }
+  return DevTasks{D.nodes.p, D.tptr.p, D.prog.p, D.gpo.p, static_cast<int>(L.tptr.size()) - 1, L.nleaf, L.split,
+                  &L.top, has_batch ? &L.batch : nullptr};
+}
+
 void upload_symb(ncl_symb* S) {
   if (S->dev_ready) return;
   ensure_init();
@@ -608,6 +785,15 @@ void upload_symb(ncl_symb* S) {
   S->asrc.upload(Z.a_src);
   S->aoff.upload(Z.a_off);
   {
+    std::vector<int> ap(Z.a_off.size());
+    for (int s = 0; s < nsn; ++s) {
+      const int nr = static_cast<int>(Z.sn_rptr[s + 1] - Z.sn_rptr[s]);
+      for (int64_t e = aptr[s]; e < aptr[s + 1]; ++e)
+        ap[e] = static_cast<int>(cb_col(Z.a_off[e] / nr, nr) + Z.a_off[e] % nr);
+    }
+    S->aoffp.upload(ap);
+  }
+  {
     std::vector<SnMeta> mv(nsn);
     for (int s = 0; s < nsn; ++s) {
       SnMeta& m = mv[s];
@@ -625,6 +811,14 @@ void upload_symb(ncl_symb* S) {
       m.pad = 0;
     }
     S->meta.upload(mv);
+    std::vector<ChildRec> cr(Z.child.size());
+    for (size_t q = 0; q < Z.child.size(); ++q) {
+      const int c = Z.child[q];
+      cr[q].cboff = Z.cb_off[c];
+      cr[q].rel = static_cast<int>(Z.sn_rptr[c] + (Z.sn_first[c + 1] - Z.sn_first[c]));
+      cr[q].m2c = static_cast<int>(Z.sn_rptr[c + 1] - Z.sn_rptr[c]) - (Z.sn_first[c + 1] - Z.sn_first[c]);
+    }
+    S->chrec.upload(cr);
   }
   S->flags.alloc(3 * std::max(1, nsn));
   ck(cudaMemsetAsync(S->flags.p, 0, 3 * std::max(1, nsn) * sizeof(int), g_stream), "memset");
@@ -656,16 +850,20 @@ void upload_symb(ncl_symb* S) {
   d.meta = S->meta.p;
   d.tasks = DevTasks{S->lay_nodes.p, S->lay_tptr.p, S->lay_prog.p, S->lay_gpo.p,
                      static_cast<int>(S->lay.tptr.size()) - 1, S->lay.nleaf, S->lay.split, &S->lay.top};
+  d.ftasks = upload_layout(S->flay, S->fdev);
   d.cptr = S->cptr.p;
   d.child = S->child.p;
+  d.chrec = S->chrec.p;
   d.order = S->order.p;
   d.aptr = S->aptr.p;
   d.asrc = S->asrc.p;
   d.aoff = S->aoff.p;
+  d.aoffp = S->aoffp.p;
   d.flags = S->flags.p;
   d.tickets = S->tickets.p;
   d.epoch = 0;
-  if (Z.l_storage >= (int64_t(1) << 31) || static_cast<int64_t>(Z.amap.size()) >= (int64_t(1) << 31))
+  if (Z.l_storage >= (int64_t(1) << 31) || static_cast<int64_t>(Z.amap.size()) >= (int64_t(1) << 31) ||
+      static_cast<int64_t>(Z.rows.size()) >= (int64_t(1) << 31))
     throw Error{NCL_E_INVALID, "analyze: factor exceeds int32 panel addressing"};
   S->dev_ready = true;
 }
@@ -688,6 +886,7 @@ ncl_symb* analyze_impl(ncl_sym_t M, const int* perm) {
   S->core = analyze_core(n, M->pat.col_ptr(), M->pat.row_ind(), std::move(p));
   S->Z = build_supernodes(S->core, M->pat.col_ptr(), M->pat.row_ind());
   S->lay = build_layout(S->Z, S->Z.order, S->Z.nsplit);
+  S->flay = build_layout(S->Z, S->Z.order, S->Z.nsplit, true);
   S->hash = M->hash;
   S->nnz = M->pat.nnz();
   return S.release();
@@ -775,9 +974,9 @@ void alloc_fact(ncl_fact* f) {
   f->F.L = f->L.p;
   f->F.CB = f->CB.p;
   f->F.CV = f->CV.p;
-  if (f->S->lay.top.any_big) {  // scratch of the batched large-front path
-    f->bigF.alloc(f->S->lay.top.scratch_f);
-    f->bigW.alloc(f->S->lay.top.scratch_w);
+  if (f->S->flay.top.any_big) {  // scratch of the batched large-front path
+    f->bigF.alloc(f->S->flay.top.scratch_f);
+    f->bigW.alloc(f->S->flay.top.scratch_w);
     f->F.bigF = f->bigF.p;
     f->F.bigW = f->bigW.p;
   }
@@ -792,7 +991,7 @@ void run_factor(ncl_fact* f, ncl_sym_t M, double tol) {
   static const char* trace_path = std::getenv("NCL_TASK_TRACE");
   static int traced = 0;
   static DevBuf<unsigned long long> tbuf, pbuf;
-  const int ntask = f->S->d.tasks.n;
+  const int ntask = f->S->d.ftasks.n;
   const int64_t nsn = static_cast<int64_t>(f->S->Z.sn_first.size()) - 1;
   if (trace_path && traced == 2) {
     tbuf.alloc(2 * static_cast<int64_t>(ntask));
@@ -808,11 +1007,11 @@ void run_factor(ncl_fact* f, ncl_sym_t M, double tol) {
     std::vector<unsigned long long> h;
     tbuf.download(h, 2 * static_cast<int64_t>(ntask));
     if (FILE* fp = std::fopen(trace_path, "wb")) {
-      const int hdr[4] = {ntask, f->S->d.tasks.nleaf, f->S->d.tasks.split, 0};
+      const int hdr[4] = {ntask, f->S->d.ftasks.nleaf, f->S->d.ftasks.split, 0};
       std::fwrite(hdr, sizeof(int), 4, fp);
       std::fwrite(h.data(), sizeof(unsigned long long), h.size(), fp);
-      std::fwrite(f->S->lay.tptr.data(), sizeof(int), f->S->lay.tptr.size(), fp);
-      std::fwrite(f->S->lay.nodes.data(), sizeof(int), f->S->lay.nodes.size(), fp);
+      std::fwrite(f->S->flay.tptr.data(), sizeof(int), f->S->flay.tptr.size(), fp);
+      std::fwrite(f->S->flay.nodes.data(), sizeof(int), f->S->flay.nodes.size(), fp);
       std::fclose(fp);
     }
     dev_phase_trace(nullptr);
@@ -1073,6 +1272,9 @@ struct ncl_shard {
   DevBuf<double> send, recv;
   DevBuf<int> unrep;  // original indices this rank does not report (zeroed before the x all-reduce)
   TaskLayout layA, layB;
+  TaskLayout flayA, flayB;  // factor variants (batched subtrees split off)
+  LayoutDev fdevA, fdevB;
+  DevTasks ftA{}, ftB{};
   std::vector<DevBuf<BigDesc>> topA_dev, topB_dev;
   DevBuf<int> tA, tB, pA, pB;  // task pointers, group programs
   DevBuf<int64_t> gA, gB;
@@ -1094,6 +1296,8 @@ void shard_upload(ncl_shard* sh) {
   sh->pB.upload(sh->layB.prog);
   sh->gA.upload(sh->layA.gpo);
   sh->gB.upload(sh->layB.gpo);
+  sh->ftA = upload_layout(sh->flayA, sh->fdevA);
+  sh->ftB = upload_layout(sh->flayB, sh->fdevB);
   sh->bids.upload(sh->P.boundary);
   sh->bowner.upload(sh->P.bowner);
   sh->cb_off.upload(sh->P.cb_pack_off);
@@ -1121,8 +1325,8 @@ DevTasks tasks_B(ncl_shard* sh) {
                   sh->layB.nleaf, sh->layB.split, &sh->layB.top};
 }
 void grow_scratch(ncl_fact* F, ncl_shard* sh) {
-  const int64_t nf = std::max(sh->layA.top.scratch_f, sh->layB.top.scratch_f);
-  const int64_t nw = std::max(sh->layA.top.scratch_w, sh->layB.top.scratch_w);
+  const int64_t nf = std::max(sh->flayA.top.scratch_f, sh->flayB.top.scratch_f);
+  const int64_t nw = std::max(sh->flayA.top.scratch_w, sh->flayB.top.scratch_w);
   if (nf > 0) {
     F->bigF.alloc(std::max<int64_t>(nf, F->bigF.n));
     F->bigW.alloc(std::max<int64_t>(nw, F->bigW.n));
@@ -1156,6 +1360,8 @@ API int ncl_shard_create(ncl_symb_t S, const int* var_group, int ngroups, int wo
     sh->P = build_shard_plan(S->Z, S->core, g, ngroups, world, rank);
     sh->layA = build_layout(S->Z, sh->P.listA, sh->P.splitA);
     sh->layB = build_layout(S->Z, sh->P.listB, sh->P.splitB);
+    sh->flayA = build_layout(S->Z, sh->P.listA, sh->P.splitA, true);
+    sh->flayB = build_layout(S->Z, sh->P.listB, sh->P.splitB, true);
     *out = sh.release();
   });
 }
@@ -1201,9 +1407,9 @@ API int ncl_shard_refactorize(ncl_fact_t F, ncl_sym_t M, ncl_shard_t sh, double 
     DevSymb& d = F->S->d;
     grow_scratch(F, sh);
     dev_factor_begin(d, M->dp, F->F, M->vals.p, tol, g_stream);
-    dev_factor_list(d, F->F, M->vals.p, tasks_A(sh), 0, g_stream);
+    dev_factor_list(d, F->F, M->vals.p, sh->ftA, 0, g_stream);
     if (sh->P.world > 1) allgather_blocks(sh, F->F.CB, 0, d.flags, d.epoch);
-    dev_factor_list(d, F->F, M->vals.p, tasks_B(sh), 1, g_stream);
+    dev_factor_list(d, F->F, M->vals.p, sh->ftB, 1, g_stream);
     if (sh->P.world > 1) {
       dev_inertia(d, F->F, g_stream, sh->report.p);
       // istat = [zero-pivot position (min), npos, nneg, nzero (sums)]
@@ -1232,8 +1438,8 @@ API int ncl_shard_refactorize_emulated(ncl_fact_t F, ncl_sym_t M, ncl_shard_t* p
     DevSymb& d = F->S->d;
     for (int r = 0; r < G; ++r) grow_scratch(F, plans[r]);
     dev_factor_begin(d, M->dp, F->F, M->vals.p, tol, g_stream);
-    for (int r = 0; r < G; ++r) dev_factor_list(d, F->F, M->vals.p, tasks_A(plans[r]), r, g_stream);
-    dev_factor_list(d, F->F, M->vals.p, tasks_B(plans[0]), G, g_stream);
+    for (int r = 0; r < G; ++r) dev_factor_list(d, F->F, M->vals.p, plans[r]->ftA, r, g_stream);
+    dev_factor_list(d, F->F, M->vals.p, plans[0]->ftB, G, g_stream);
     dev_inertia(d, F->F, g_stream);
     check_launch("emulated shard factorize");
   });

@@ -7,6 +7,8 @@
 #include <cstdint>
 #include <vector>
 
+#include "../limits.hpp"
+
 namespace nclb {
 
 // Contribution blocks are packed lower-triangular, column-major: column j of
@@ -40,6 +42,62 @@ struct TopSched {
   int max_nr = 0;
   int64_t scratch_f = 0, scratch_w = 0;   // largest per-segment scratch (doubles)
 };
+// Register-resident fronts of a task list (csrc/capi.cpp build_batches).
+// The wide bottom of the tree is a handful of tiny front shapes (500x256:
+// (nr, w) = (7,1) 185 k, (8,2) 86 k, (10,2) 73 k, (8,1) 55 k, ... of 560 k
+// supernodes). For the shapes in kRegShapes every index of the front is a
+// compile-time constant, so a team of R lanes (R = 1 for the smallest
+// shapes) factors one front held in registers: no shared memory, nothing but
+// the arithmetic, one predicated load per front entry per source and, for
+// R > 1, one shuffle per pivot entry. Supernodes of these shapes whose
+// children in the list are such fronts too form a dependency-closed forest
+// that runs as ONE persistent launch before the other tasks: warps claim
+// chunks (up to 32 / R fronts of one shape and level; chunks sorted by
+// level), lanes wait on their children's flags (acquire) and publish their
+// own (release). Per front entry the operations
+// are small_task's in the same order (A value, children ascending, pivot
+// columns in order): the factor is bitwise that of the warp path.
+struct alignas(16) RegInst {
+  int64_t loff, cboff;  // panel, contribution-block offsets
+  int64_t amap;         // offset (ints) of the A map: per packed front entry the K value slot, -1 = none
+  int64_t cmap;         // children's maps: per child, per packed front entry the source position in the
+                        // child's packed CB, 255 = none. R > 1: byte offset in `cmap` (rows padded to 4
+                        // bytes); R == 1: word offset in `cmapw`, words interleaved over the chunk's 32 lanes
+                        // (word w of child q at cmap + (q * words + w) * 32), and the A map interleaved the
+                        // same way (entry p at amap + 32 p): coalesced
+  int64_t ccb;          // offset of the children's CB offsets (int64 each) and supernode ids (int each)
+  int s, f, nch, shape;  // shape = kRegShapes index
+  int cid[4];            // the first four children inline (supernode ids, CB offsets): one round trip less
+  int64_t cb[4];
+};
+struct RegChunk {
+  int shape, n, first, pad;  // n fronts inst[first .. first + n) of one shape
+};
+struct BatchSched {
+  std::vector<RegInst> inst;
+  std::vector<int> amap;
+  std::vector<uint8_t> cmap;
+  std::vector<uint32_t> cmapw;
+  std::vector<int64_t> ccb;
+  std::vector<int> cid;      // children's supernode ids (same index as ccb)
+  std::vector<RegChunk> chunks;  // tier-1 chunks in level order, then tier-2 chunks in level order
+  int nchunk1 = 0;               // chunks of tier 1
+  int64_t nodes = 0;         // supernodes covered
+  const RegInst* dev_inst = nullptr;
+  const int* dev_amap = nullptr;
+  const uint8_t* dev_cmap = nullptr;
+  const uint32_t* dev_cmapw = nullptr;
+  const int64_t* dev_ccb = nullptr;
+  const int* dev_cid = nullptr;
+  const RegChunk* dev_chunks = nullptr;
+};
+// Per child slot q of the children CSR (child[q]): what a parent needs to
+// extend-add that child's contribution block (one 16-byte load)
+struct alignas(16) ChildRec {
+  int64_t cboff;  // the child's CB offset
+  int rel;        // index in relp of the child's first CB row (rptr + w)
+  int m2c;        // CB order nr - w
+};
 // Packed per-supernode metadata (one 64-byte record, four 16-byte loads):
 // everything a small-front task needs before touching the numbers.
 struct alignas(16) SnMeta {
@@ -65,6 +123,7 @@ struct DevTasks {
   const int64_t* gpo = nullptr;    // [ngroups+1]
   int n = 0, nleaf = 0, split = 0;  // counts / indices in TASKS
   const TopSched* top = nullptr;    // host pointer; nullptr or !any_big -> one persistent launch
+  const BatchSched* batch = nullptr;  // host pointer; batched subtrees run before the task list (factor)
 };
 
 // Symbolic schedule resident in HBM (built once from host Supernodal).
@@ -90,12 +149,15 @@ struct DevSymb {
   int64_t* cvsrc = nullptr;
   int* cptr = nullptr;  // children CSR
   int* child = nullptr;
+  const ChildRec* chrec = nullptr;  // [child slots]
   int* order = nullptr;  // ticket order, leaves first
   int64_t* aptr = nullptr;   // [nsn+1] A entries per supernode
   int* asrc = nullptr;       // source value slot
   int* aoff = nullptr;       // offset inside panel
+  int* aoffp = nullptr;      // offset inside the packed-lower front (cb_col(off / nr, nr) + off % nr)
   // scheduling state
-  DevTasks tasks;           // default (unsharded) task list
+  DevTasks tasks;           // default (unsharded) task list (solves)
+  DevTasks ftasks;          // the same list with its batched subtrees split off (factor)
   const SnMeta* meta = nullptr;  // [nsn]
   int* flags = nullptr;     // [3*nsn] epoch flags: factor, fwd, bwd
   int* tickets = nullptr;   // [4]
@@ -134,6 +196,7 @@ struct TaskLayout {
   std::vector<int> nodes, tptr;
   int nleaf = 0, split = 0;
   TopSched top;
+  BatchSched batch;  // empty unless built with batched subtrees
   // group programs (one per group task, see build_layout): int stream
   std::vector<int> prog;
   std::vector<int64_t> gpo;  // [ngroups+1]

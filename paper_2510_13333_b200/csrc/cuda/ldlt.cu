@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <utility>
 #include <vector>
 #include <cstdlib>
 
@@ -30,12 +31,15 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kWarpFront = 32;    // nr cap of the warp smem path
-constexpr int kCtaFront = 160;    // nr cap of the CTA smem path (packed lower: 100 KB, two CTAs per SM)
+// kCtaFront (nr cap of the CTA smem path) lives in csrc/limits.hpp
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+__device__ __forceinline__ void st_relaxed(int* p, int v) {
+  asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -977,8 +981,13 @@ __device__ __forceinline__ void group_task(const FactorArgs& a, int g, int lane,
     __syncwarp();
     for (int q = 0; q < nch; ++q) {
       const int m2c = PG[p], off = PG[p + 1];
+      const double* Cc = stack + off;
+      if (off < 0) {  // external child (register-front phase): its CB in the standard layout
+        Cc = a.CB + (static_cast<int64_t>(static_cast<uint32_t>(PG[p + 2])) | (static_cast<int64_t>(PG[p + 3]) << 32));
+        p += 2;
+      }
       const int reli = lane < m2c ? PG[p + 2 + lane] : 0;
-      extend_add_flat(F, nr, stack + off, m2c, reli, lane);
+      extend_add_flat(F, nr, Cc, m2c, reli, lane);
       p += 2 + m2c;
       __syncwarp();
     }
@@ -1017,6 +1026,181 @@ __device__ __forceinline__ void group_task(const FactorArgs& a, int g, int lane,
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Register-resident fronts (BatchSched, csrc/capi.cpp build_batches): one
+// thread per front of a compile-time shape (NR rows, W pivots), the packed
+// front in registers (entry (i, j) at PK(i, j), all indices constants).
+// Per front entry: the A value (or 0) from the A map, then every child's CB
+// entry through its byte map (255 = none), children in ascending order, then
+// the pivot columns in order (l = F / d, F(i, c2) -= l_i (d l_c2)) — the
+// operations of small_task in the same order, so the factor is bitwise that
+// of the warp path. All loads of one source are independent and issued
+// together. One persistent launch: warps claim 32 consecutive tasks (the
+// list is padded so a warp never spans two levels), threads wait on their
+// children's flags and publish their own.
+// ---------------------------------------------------------------------------
+// acquire every child's flag (the first four ids inline, compile-time indexed
+// so the record stays in registers)
+__device__ __forceinline__ void wait_children(const FactorArgs& a, const RegInst& I, const int* __restrict__ cid) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (q < I.nch) wait_flag(a.flags + I.cid[q], a.epoch);
+  for (int q = 4; q < I.nch; ++q) wait_flag(a.flags + __ldg(cid + I.ccb + q), a.epoch);
+}
+
+template <int NR, int W, int R>
+__device__ __forceinline__ void reg_front(const FactorArgs& a, const RegInst& I, int r, unsigned tm,
+                                          const int* __restrict__ amap, const uint8_t* __restrict__ cmap,
+                                          const uint32_t* __restrict__ cmapw, const int64_t* __restrict__ ccb,
+                                          const int* __restrict__ cid, double thresh) {
+  constexpr int NP = NR * (NR + 1) / 2, NPAD = (NP + 3) & ~3, M2 = NR - W, KR = (NR + R - 1) / R;
+  auto PK = [](int i, int j) { return j * NR - j * (j + 1) / 2 + i; };  // packed lower, i >= j
+  auto row = [r](int k) { return R == 1 ? k : r + R * k; };            // the lane's k-th row
+  // broadcast of a team member's register (R == 1: the value itself)
+  auto bcast = [tm](double v, int src) { return R == 1 ? v : __shfl_sync(tm, v, src, R); };
+  double F[KR][NR];
+  const int* am = amap + I.amap;
+  const uint8_t* cm = cmap + I.cmap;
+  if constexpr (R == 1) {
+    // small fronts: round trip 1 (independent) = A slots + the first PRE
+    // children's maps, round trip 2 = the children's flags, round trip 3 = A
+    // values + CB entries; larger fronts keep fewer values in flight
+    constexpr int PRE = 0;  // measured: preloading children's maps costs more in registers than it saves
+    const int npre = min(I.nch, PRE);
+    const uint32_t* cmw = cmapw + I.cmap;
+    int sl[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) sl[p] = __ldg(am + 32 * p);
+    uint32_t mw[PRE > 0 ? PRE : 1][NPAD / 4];
+#pragma unroll
+    for (int q = 0; q < PRE; ++q)
+#pragma unroll
+      for (int w4 = 0; w4 < NPAD / 4; ++w4) mw[q][w4] = q < npre ? __ldg(cmw + (q * (NPAD / 4) + w4) * 32) : 0xffffffffu;
+    wait_children(a, I, cid);
+#pragma unroll
+    for (int j = 0; j < NR; ++j)
+#pragma unroll
+      for (int i = j; i < NR; ++i) F[i][j] = sl[PK(i, j)] >= 0 ? __ldg(a.kvals + sl[PK(i, j)]) : 0.0;
+#pragma unroll
+    for (int q = 0; q < PRE; ++q) {
+      if (q >= npre) break;
+      const double* C = a.CB + I.cb[q];
+#pragma unroll
+      for (int j = 0; j < NR; ++j)
+#pragma unroll
+        for (int i = j; i < NR; ++i) {
+          const uint32_t src = (mw[q][PK(i, j) >> 2] >> (8 * (PK(i, j) & 3))) & 0xffu;
+          if (src != 0xffu) F[i][j] += __ldcg(C + src);
+        }
+    }
+    for (int q = npre; q < I.nch; ++q) {
+      const double* C = a.CB + __ldg(ccb + I.ccb + q);
+      uint32_t w[NPAD / 4];
+#pragma unroll
+      for (int w4 = 0; w4 < NPAD / 4; ++w4) w[w4] = __ldg(cmw + (q * (NPAD / 4) + w4) * 32);
+#pragma unroll
+      for (int j = 0; j < NR; ++j)
+#pragma unroll
+        for (int i = j; i < NR; ++i) {
+          const uint32_t src = (w[PK(i, j) >> 2] >> (8 * (PK(i, j) & 3))) & 0xffu;
+          if (src != 0xffu) F[i][j] += __ldcg(C + src);
+        }
+    }
+  } else {
+    wait_children(a, I, cid);
+#pragma unroll
+    for (int k = 0; k < KR; ++k)
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        const int i = row(k);
+        const int slv = (i < NR && j <= i) ? __ldg(am + PK(i, j)) : -1;
+        F[k][j] = slv >= 0 ? __ldg(a.kvals + slv) : 0.0;
+      }
+    for (int q = 0; q < I.nch; ++q) {
+      const double* C = a.CB + __ldg(ccb + I.ccb + q);
+      const uint8_t* cq = cm + q * NPAD;
+#pragma unroll
+      for (int k = 0; k < KR; ++k)
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {
+          const int i = row(k);
+          const uint32_t src = (i < NR && j <= i) ? __ldg(cq + PK(i, j)) : 0xffu;
+          if (src != 0xffu) F[k][j] += __ldcg(C + src);
+        }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < W; ++c) {
+    const double d = bcast(F[c / R][c], c % R);
+    if (r == 0) {
+      a.D[I.f + c] = d;
+      if (fabs(d) <= thresh) atomicMin(a.zp, I.f + c);
+    }
+#pragma unroll
+    for (int k = 0; k < KR; ++k)
+      if (row(k) > c && row(k) < NR) F[k][c] = divz(F[k][c], d);
+#pragma unroll
+    for (int c2 = c + 1; c2 < NR; ++c2) {
+      const double lc2 = d * bcast(F[c2 / R][c], c2 % R);
+#pragma unroll
+      for (int k = 0; k < KR; ++k)
+        if (row(k) >= c2 && row(k) < NR) F[k][c2] -= F[k][c] * lc2;
+    }
+  }
+  double* P = a.L + I.loff;
+#pragma unroll
+  for (int c = 0; c < W; ++c)
+#pragma unroll
+    for (int k = 0; k < KR; ++k)
+      if (row(k) < NR) P[c * NR + row(k)] = row(k) >= c ? F[k][c] : 0.0;
+  double* Cs = a.CB + I.cboff;
+#pragma unroll
+  for (int j = 0; j < M2; ++j)
+#pragma unroll
+    for (int k = 0; k < KR; ++k)
+      if (row(k) >= W + j && row(k) < NR) Cs[j * M2 - j * (j + 1) / 2 + row(k) - W] = F[k][W + j];
+}
+
+template <int K0, int... K>
+__device__ __forceinline__ void reg_dispatch(const FactorArgs& a, const RegChunk& ch, int lane,
+                                             const RegInst* __restrict__ inst, const int* amap, const uint8_t* cmap,
+                                             const uint32_t* cmapw, const int64_t* ccb, const int* cid,
+                                             double thresh, std::integer_sequence<int, K...>) {
+  (((ch.shape == K0 + K) ? [&] {
+    constexpr int NR = kRegShapes[K0 + K][0], W = kRegShapes[K0 + K][1], R = kRegShapes[K0 + K][2];
+    const int ix = lane / R;
+    if (ix < ch.n) {
+      const unsigned tm = R == 32 ? kFull : (((1u << R) - 1u) << (ix * R));
+      const RegInst I = inst[ch.first + ix];
+      reg_front<NR, W, R>(a, I, lane % R, tm, amap, cmap, cmapw, ccb, cid, thresh);
+      if constexpr (R > 1) __syncwarp(tm);
+      if (lane % R == 0) st_release(a.flags + I.s, a.epoch);  // release: orders this thread's writes
+    }
+  }()
+                    : void()),
+   ...);
+}
+
+template <int K0, int K1>
+__global__ void __launch_bounds__(128) reg_factor_kernel(FactorArgs a, const RegInst* __restrict__ inst,
+                                                         const RegChunk* __restrict__ chunks, int nchunk,
+                                                         const int* __restrict__ amap,
+                                                         const uint8_t* __restrict__ cmap,
+                                                         const uint32_t* __restrict__ cmapw,
+                                                         const int64_t* __restrict__ ccb, const int* __restrict__ cid) {
+  const int lane = threadIdx.x & 31;
+  const double thresh = __ldcg(a.thresh);
+  for (;;) {
+    int c = 0;
+    if (lane == 0) c = atomicAdd(a.ticket, 1);
+    c = __shfl_sync(kFull, c, 0);
+    if (c >= nchunk) break;
+    const RegChunk ch = chunks[c];
+    reg_dispatch<K0>(a, ch, lane, inst, amap, cmap, cmapw, ccb, cid, thresh,
+                     std::make_integer_sequence<int, K1 - K0>{});
+  }
+}
 
 template <int NT>
 __global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 6 : NT == 128 ? 6 : 2) factor_kernel(FactorArgs a) {
@@ -1851,15 +2035,73 @@ void dev_factor_begin(const DevSymb& S0, const DevPattern& P, DevFactor& F, cons
   cudaMemsetAsync(S.tickets, 0, kTickets * sizeof(int), st);
 }
 
+// NCL_FACTOR_PHASES=1: CUDA events around the phases of every factorization
+// (batched subtrees | warp tasks | CTA segments), averaged and printed to stderr at
+// exit (debug timeline; synchronises the stream once per factorization)
+namespace {
+struct PhaseTimer {
+  bool on = std::getenv("NCL_FACTOR_PHASES") != nullptr;
+  cudaEvent_t ev[4]{};
+  double acc[3]{};
+  int n = 0;
+  void mark(int k, cudaStream_t st) {
+    if (!on) return;
+    if (!ev[k]) cudaEventCreate(&ev[k]);
+    cudaEventRecord(ev[k], st);
+    if (k == 3) {
+      cudaEventSynchronize(ev[3]);
+      for (int i = 0; i < 3; ++i) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+        acc[i] += ms;
+      }
+      ++n;
+    }
+  }
+  ~PhaseTimer() {
+    if (on && n)
+      std::fprintf(stderr, "[ncl] factor phases over %d runs (ms): batch %.4f  warp %.4f  cta %.4f\n", n, acc[0] / n,
+                   acc[1] / n, acc[2] / n);
+  }
+} g_ptimer;
+}  // namespace
+
 void dev_factor_list(const DevSymb& S, DevFactor& F, const double* kvals, const DevTasks& T, int slot,
                      cudaStream_t st) {
   if (T.n == 0) return;
+  g_ptimer.mark(0, st);
   FactorArgs a{S, F.L, F.CB, F.D, kvals, F.scal, F.istat, S.flags, S.tickets + 2 * slot, S.epoch, 0, T.split,
                T.ids, T.tptr, T.prog, T.gpo, T.nleaf, 0, g_task_trace};
-  if (T.split > 0) {
+  if (T.batch) {
+    const BatchSched& bs = *T.batch;
+    static int grid1 = 0, grid2 = 0;
+    if (!grid1) {
+      grid1 = persistent_grid(reg_factor_kernel<0, kRegTier1>, 128, 1 << 30);
+      grid2 = persistent_grid(reg_factor_kernel<kRegTier1, kNumRegShapes>, 128, 1 << 30);
+    }
+    const int n1 = bs.nchunk1, n2 = static_cast<int>(bs.chunks.size()) - bs.nchunk1;
+    FactorArgs ra = a;
+    if (n1 > 0) {
+      ra.ticket = S.tickets + kTickets - 2;
+      cudaMemsetAsync(ra.ticket, 0, sizeof(int), st);
+      COUNT(1);
+      reg_factor_kernel<0, kRegTier1><<<std::min(grid1, (n1 + 3) / 4), 128, 0, st>>>(
+          ra, bs.dev_inst, bs.dev_chunks, n1, bs.dev_amap, bs.dev_cmap, bs.dev_cmapw, bs.dev_ccb, bs.dev_cid);
+    }
+    if (n2 > 0) {
+      ra.ticket = S.tickets + kTickets - 3;
+      cudaMemsetAsync(ra.ticket, 0, sizeof(int), st);
+      COUNT(1);
+      reg_factor_kernel<kRegTier1, kNumRegShapes><<<std::min(grid2, (n2 + 3) / 4), 128, 0, st>>>(
+          ra, bs.dev_inst, bs.dev_chunks + n1, n2, bs.dev_amap, bs.dev_cmap, bs.dev_cmapw, bs.dev_ccb, bs.dev_cid);
+    }
+  }
+  g_ptimer.mark(1, st);
+  if (T.split > 0 && T.tptr) {
     COUNT(1);
     factor_kernel<32><<<g_fg, 128, kFacSmem1, st>>>(a);
   }
+  g_ptimer.mark(2, st);
   if (T.top && (T.top->any_big || T.top->any_small)) {
     // segment by segment (merged levels): the segment's fronts in one
     // persistent launch (128-thread CTAs when they all fit kCtaFrontS rows),
@@ -1881,6 +2123,7 @@ void dev_factor_list(const DevSymb& S, DevFactor& F, const double* kvals, const 
       }
       if (!ts.big[L].empty()) dev_factor_big_batch(S, F, kvals, ts.big[L], ts.big_dev[L], st);
     }
+    g_ptimer.mark(3, st);
     return;
   }
   if (T.split < T.n) {
@@ -1890,6 +2133,7 @@ void dev_factor_list(const DevSymb& S, DevFactor& F, const double* kvals, const 
     COUNT(1);
     factor_kernel<256><<<std::min(g_fg2, T.n - T.split), 256, kFacSmem2, st>>>(a);
   }
+  g_ptimer.mark(3, st);
 }
 
 // NCL_TASK_TRACE: per-supernode phase stamps of the CTA smem path
@@ -1899,7 +2143,9 @@ void dev_phase_trace(unsigned long long* buf) { cudaMemcpyToSymbol(g_phase, &buf
 void dev_factor(const DevSymb& S, const DevPattern& P, DevFactor& F, const double* kvals, double pivot_tol,
                 cudaStream_t st, const TopSched* top) {
   dev_factor_begin(S, P, F, kvals, pivot_tol, st);
-  DevTasks T = S.tasks;
+  // NCL_NO_BATCH=1: the layout without batched subtrees (A/B timing only)
+  static const bool no_batch = std::getenv("NCL_NO_BATCH") != nullptr;
+  DevTasks T = no_batch ? S.tasks : S.ftasks;
   if (top) T.top = top;
   dev_factor_list(S, F, kvals, T, 0, st);
 }

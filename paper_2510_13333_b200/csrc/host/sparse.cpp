@@ -2,6 +2,8 @@
 // names the reference routine whose semantics it reproduces.
 #include "sparse.hpp"
 
+#include "../limits.hpp"
+
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -359,7 +361,7 @@ void true_L_structure(const SymbolicCore& S, std::vector<int64_t>& lp, std::vect
 
 Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
                             const std::vector<int>& ri, int relax) {
-  constexpr int64_t kSmemFront = 160;       // = kCtaFront (csrc/cuda/ldlt.cu)
+  constexpr int64_t kSmemFront = kCtaFront;  // csrc/limits.hpp
   // child entries one CTA assembles comfortably; beyond, the front is assembled
   // by a multi-CTA gather (NCL_HEAVY_GATHER overrides: tests drive that path)
   static const char* heavy_env = std::getenv("NCL_HEAVY_GATHER");
