@@ -48,6 +48,33 @@ int ncl_shard_boundary(ncl_shard_t P, int* ids, int* owner, int64_t* cb_off, int
 int ncl_shard_refactorize(ncl_fact_t F, ncl_sym_t M, ncl_shard_t P, double pivot_tol);
 /* sharded solve_in_place; the full x ends up on every rank */
 int ncl_shard_solve(ncl_fact_t F, ncl_shard_t P, double* x, int where);
+/* Split-phase form of the two calls above, for callers that bring their own
+ * transport (and for single-GPU tests of the exchange): the same kernels and
+ * the same pack / unpack, with the collectives done by the caller.
+ *   factor:  phase_a (own + base-only supernodes, then pack this rank's
+ *            boundary contribution blocks into `send`, cb_chunk doubles)
+ *            -> caller all-gathers send into recv (world * cb_chunk doubles,
+ *               rank-major, as ncclAllGather lays it out)
+ *            -> phase_b (unpack, separator, this rank's pivot report into
+ *               istat[4] = {zero-pivot position or n, npos, nneg, nzero})
+ *            -> caller reduces istat over ranks (min, sum, sum, sum) and
+ *               stores it with ncl_shard_set_status.
+ *   solve:   phase_a (forward over own subtrees, pack boundary contribution
+ *            vectors, cv_chunk doubles) -> all-gather -> phase_b (rest of
+ *            the solve; x holds only this rank's reported entries, zeros
+ *            elsewhere) -> caller sums x over ranks.
+ * `where` / `swhere` / `rwhere` say whether x / send / recv are host or
+ * device pointers; device buffers are read and written asynchronously on the
+ * library stream (ncl_stream), host buffers are complete on return. After a world > 1 factorization the whole-factor getters
+ * (ncl_fact_diagonal, ncl_fact_get_L, ncl_fact_solve, ncl_solve_refined)
+ * return NCL_E_LOGIC; ncl_shard_diagonal returns this rank's reported D
+ * entries (NaN elsewhere). */
+int ncl_shard_factor_phase_a(ncl_fact_t F, ncl_sym_t M, ncl_shard_t P, double pivot_tol, double* send, int where);
+int ncl_shard_factor_phase_b(ncl_fact_t F, ncl_sym_t M, ncl_shard_t P, const double* recv, int where, int* istat);
+int ncl_shard_set_status(ncl_fact_t F, const int* istat);
+int ncl_shard_solve_phase_a(ncl_fact_t F, ncl_shard_t P, double* x, int where, double* send, int swhere);
+int ncl_shard_solve_phase_b(ncl_fact_t F, ncl_shard_t P, double* x, int where, const double* recv, int rwhere);
+int ncl_shard_diagonal(ncl_fact_t F, ncl_shard_t P, double* d);
 /* single-GPU emulation of a world-G factorization (plans = ranks 0..G-1) */
 int ncl_shard_refactorize_emulated(ncl_fact_t F, ncl_sym_t M, ncl_shard_t* plans, int G, double pivot_tol);
 

@@ -4,8 +4,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstring>
+#include <limits>
 #include <map>
 #include <memory>
 #include <sstream>
@@ -880,13 +882,27 @@ API int ncl_symbolic_order(ncl_sym_t M, int* perm) {
 ncl_symb* analyze_impl(ncl_sym_t M, const int* perm) {
   if (!M->pat.finalized()) throw Error{NCL_E_LOGIC, "analyze: matrix not finalized"};
   const int n = M->pat.dim();
+  // NCL_ANALYZE_TIMING=1: per-phase host seconds on stderr
+  static const bool timing = std::getenv("NCL_ANALYZE_TIMING") != nullptr;
+  auto t = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!timing) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[analyze] %-16s %.3f s\n", what, std::chrono::duration<double>(now - t).count());
+    t = now;
+  };
   std::vector<int> p = perm ? std::vector<int>(perm, perm + n)
                             : symbolic_order(n, M->pat.col_ptr(), M->pat.row_ind());
+  lap("symbolic_order");
   auto S = std::make_unique<ncl_symb>();
   S->core = analyze_core(n, M->pat.col_ptr(), M->pat.row_ind(), std::move(p));
+  lap("analyze_core");
   S->Z = build_supernodes(S->core, M->pat.col_ptr(), M->pat.row_ind());
+  lap("build_supernodes");
   S->lay = build_layout(S->Z, S->Z.order, S->Z.nsplit);
+  lap("build_layout");
   S->flay = build_layout(S->Z, S->Z.order, S->Z.nsplit, true);
+  lap("build_layout(f)");
   S->hash = M->hash;
   S->nnz = M->pat.nnz();
   return S.release();
@@ -951,6 +967,10 @@ struct ncl_fact {
   DevFactor F;
   DevBuf<double> L, CB, CV, D, xp, scal, work1, work2, work3, bigF, bigW;
   DevBuf<int> istat;
+  // > 1 after a sharded refactorization of a world > 1 run: L / D hold only
+  // this rank's supernodes (plus the shared separator), so the whole-factor
+  // getters refuse it
+  int sharded_world = 1;
 };
 
 namespace {
@@ -1051,6 +1071,7 @@ API int ncl_refactorize(ncl_fact_t F, ncl_sym_t M, double pivot_tol) {
     check_match(M, F->S);
     ensure_dev(M, "factorize");
     run_factor(F, M, pivot_tol);
+    F->sharded_world = 1;
   });
 }
 API void ncl_fact_destroy(ncl_fact_t F) { delete F; }
@@ -1075,6 +1096,8 @@ API int ncl_fact_status(ncl_fact_t F, int* status, int* zpi, int* np, int* nn, i
 }
 API int ncl_fact_diagonal(ncl_fact_t F, double* d) {
   GUARD({
+    if (F->sharded_world > 1)
+      throw Error{NCL_E_LOGIC, "diagonal: factor of a sharded world > 1 run (use ncl_shard_diagonal)"};
     const int n = F->S->core.n;
     if (n > 0) ck(cudaMemcpyAsync(d, F->D.p, n * sizeof(double), cudaMemcpyDeviceToHost, g_stream), "D2H");
     ck(cudaStreamSynchronize(g_stream), "sync");
@@ -1090,6 +1113,7 @@ bool fact_ok_sync(ncl_fact_t F) {
 }  // namespace
 API int ncl_fact_solve(ncl_fact_t F, double* x, int where) {
   GUARD({
+    if (F->sharded_world > 1) throw Error{NCL_E_LOGIC, "solve: factor of a sharded world > 1 run (use ncl_shard_solve)"};
     const int n = F->S->core.n;
     if (where == NCL_DEVICE) {
       dev_solve(F->S->d, F->F, x, x, g_stream);
@@ -1143,6 +1167,7 @@ int solve_refined_dev(ncl_fact_t F, ncl_sym_t M, const double* db, double* dx, d
 API int ncl_solve_refined(ncl_fact_t F, ncl_sym_t M, const double* b, double target, int max_sweeps, double* x,
                           int where, double* residual, int* sweeps, int* converged) {
   GUARD({
+    if (F->sharded_world > 1) throw Error{NCL_E_LOGIC, "solve_refined: factor of a sharded world > 1 run"};
     if (!fact_ok_sync(F)) throw Error{NCL_E_LOGIC, "solve_refined: factorization not usable"};
     check_match(M, F->S);
     ensure_dev(M, "solve_refined");
@@ -1160,6 +1185,7 @@ API int ncl_solve_refined(ncl_fact_t F, ncl_sym_t M, const double* b, double tar
 
 API int ncl_fact_get_L(ncl_fact_t F, int* lp, int* li, double* lx) {
   GUARD({
+    if (F->sharded_world > 1) throw Error{NCL_E_LOGIC, "get_L: factor of a sharded world > 1 run"};
     const Supernodal& Z = F->S->Z;
     const int n = F->S->core.n;
     std::vector<double> Lh(Z.l_storage);
@@ -1339,16 +1365,80 @@ void need_comm(const ncl_shard* sh) {
   if (!g_nccl.comm || g_nccl.world != sh->P.world || g_nccl.rank != sh->P.rank)
     throw Error{NCL_E_LOGIC, "sharded call needs ncl_dist_init with the plan's world/rank"};
 }
-void allgather_blocks(ncl_shard* sh, double* base, int cv, int* flags, int epoch) {
+// The boundary exchange in three steps so that the transport is pluggable:
+// pack (device kernel) -> all-gather of `chunk` doubles per rank (NCCL here,
+// or the caller's own transport in the split-phase API) -> unpack (device
+// kernel, publishes the separator's completion flags).
+int64_t xchunk(const ncl_shard* sh, int cv) { return cv ? sh->P.cv_chunk : sh->P.cb_chunk; }
+void pack_blocks(ncl_shard* sh, const double* base, int cv) {
   const ShardPlan& P = sh->P;
   const int nb = static_cast<int>(P.boundary.size());
-  const int64_t chunk = cv ? P.cv_chunk : P.cb_chunk;
-  if (nb == 0 || chunk == 0) return;
-  const int64_t* off = cv ? sh->cv_off.p : sh->cb_off.p;
-  dev_shard_pack(sh->S->d, base, sh->bids.p, sh->bowner.p, off, nb, P.rank, cv, sh->send.p, g_stream);
+  if (nb == 0 || xchunk(sh, cv) == 0) return;
+  dev_shard_pack(sh->S->d, base, sh->bids.p, sh->bowner.p, cv ? sh->cv_off.p : sh->cb_off.p, nb, P.rank, cv,
+                 sh->send.p, g_stream);
+}
+void unpack_blocks(ncl_shard* sh, double* base, int cv, int* flags, int epoch, const double* recv) {
+  const ShardPlan& P = sh->P;
+  const int nb = static_cast<int>(P.boundary.size());
+  if (nb == 0 || xchunk(sh, cv) == 0) return;
+  dev_shard_unpack(sh->S->d, base, sh->bids.p, sh->bowner.p, cv ? sh->cv_off.p : sh->cb_off.p, nb, P.rank, cv, recv,
+                   xchunk(sh, cv), flags, epoch, g_stream);
+}
+void allgather_blocks(ncl_shard* sh, double* base, int cv, int* flags, int epoch) {
+  const int64_t chunk = xchunk(sh, cv);
+  if (sh->P.boundary.empty() || chunk == 0) return;
+  pack_blocks(sh, base, cv);
   nck(g_nccl.all_gather(sh->send.p, sh->recv.p, chunk, ncclFloat64, g_nccl.comm, g_stream), "ncclAllGather");
-  dev_shard_unpack(sh->S->d, base, sh->bids.p, sh->bowner.p, off, nb, P.rank, cv, sh->recv.p, chunk, flags, epoch,
-                   g_stream);
+  unpack_blocks(sh, base, cv, flags, epoch, sh->recv.p);
+}
+// caller-side buffers of the split-phase API (host or device)
+void copy_out(double* dst, const double* src, int64_t n, int where) {
+  if (n > 0)
+    ck(cudaMemcpyAsync(dst, src, n * sizeof(double),
+                       where == NCL_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, g_stream),
+       "copy out");
+}
+const double* stage_in(ncl_shard* sh, const double* src, int64_t n, int where) {
+  if (where != NCL_HOST) return src;
+  if (n > 0) ck(cudaMemcpyAsync(sh->recv.p, src, n * sizeof(double), cudaMemcpyHostToDevice, g_stream), "H2D");
+  return sh->recv.p;
+}
+void shard_factor_a(ncl_fact* F, ncl_sym_t M, ncl_shard* sh, double tol) {
+  if (sh->S != F->S) throw Error{NCL_E_INVALID, "shard plan built for another symbolic factor"};
+  check_match(M, F->S);
+  ensure_dev(M, "factorize");
+  shard_upload(sh);
+  grow_scratch(F, sh);
+  DevSymb& d = F->S->d;
+  dev_factor_begin(d, M->dp, F->F, M->vals.p, tol, g_stream);
+  dev_factor_list(d, F->F, M->vals.p, sh->ftA, 0, g_stream);
+  F->sharded_world = sh->P.world;
+}
+void shard_factor_b(ncl_fact* F, ncl_sym_t M, ncl_shard* sh) {
+  DevSymb& d = F->S->d;
+  dev_factor_list(d, F->F, M->vals.p, sh->ftB, 1, g_stream);
+  // istat = [zero-pivot position, npos, nneg, nzero] over the pivots this rank reports
+  dev_inertia(d, F->F, g_stream, sh->P.world > 1 ? sh->report.p : nullptr);
+}
+double* shard_x(ncl_fact* F, double* x, int where) { return where == NCL_HOST ? F->work1.p : x; }
+void shard_solve_a(ncl_fact* F, ncl_shard* sh, double* x, int where) {
+  if (sh->S != F->S) throw Error{NCL_E_INVALID, "shard plan built for another symbolic factor"};
+  shard_upload(sh);
+  const int n = F->S->core.n;
+  double* dx = shard_x(F, x, where);
+  if (where == NCL_HOST && n > 0)
+    ck(cudaMemcpyAsync(dx, x, n * sizeof(double), cudaMemcpyHostToDevice, g_stream), "H2D");
+  DevSymb& d = F->S->d;
+  dev_solve_begin(d, g_stream);
+  dev_solve_fwd_list(d, F->F, dx, tasks_A(sh), 0, g_stream);
+}
+void shard_solve_b(ncl_fact* F, ncl_shard* sh, double* dx) {
+  DevSymb& d = F->S->d;
+  dev_solve_fwd_list(d, F->F, dx, tasks_B(sh), 1, g_stream);
+  dev_solve_bwd_list(d, F->F, dx, tasks_B(sh), 2, g_stream);
+  dev_solve_bwd_list(d, F->F, dx, tasks_A(sh), 3, g_stream);
+  // every rank keeps only the entries it reports: the sum over ranks is x
+  if (sh->P.world > 1) dev_zero_indexed(dx, sh->unrep.p, sh->nunrep, g_stream);
 }
 }  // namespace
 
@@ -1399,27 +1489,86 @@ API int ncl_shard_boundary(ncl_shard_t sh, int* ids, int* owner, int64_t* cb_off
 
 API int ncl_shard_refactorize(ncl_fact_t F, ncl_sym_t M, ncl_shard_t sh, double tol) {
   GUARD({
-    if (sh->S != F->S) throw Error{NCL_E_INVALID, "shard plan built for another symbolic factor"};
     need_comm(sh);
-    check_match(M, F->S);
-    ensure_dev(M, "factorize");
-    shard_upload(sh);
+    shard_factor_a(F, M, sh, tol);
     DevSymb& d = F->S->d;
-    grow_scratch(F, sh);
-    dev_factor_begin(d, M->dp, F->F, M->vals.p, tol, g_stream);
-    dev_factor_list(d, F->F, M->vals.p, sh->ftA, 0, g_stream);
     if (sh->P.world > 1) allgather_blocks(sh, F->F.CB, 0, d.flags, d.epoch);
-    dev_factor_list(d, F->F, M->vals.p, sh->ftB, 1, g_stream);
+    shard_factor_b(F, M, sh);
     if (sh->P.world > 1) {
-      dev_inertia(d, F->F, g_stream, sh->report.p);
-      // istat = [zero-pivot position (min), npos, nneg, nzero (sums)]
       nck(g_nccl.all_reduce(F->F.istat, F->F.istat, 1, ncclInt32, ncclMin, g_nccl.comm, g_stream), "allreduce");
       nck(g_nccl.all_reduce(F->F.istat + 1, F->F.istat + 1, 3, ncclInt32, ncclSum, g_nccl.comm, g_stream),
           "allreduce");
-    } else {
-      dev_inertia(d, F->F, g_stream);
     }
     check_launch("shard factorize");
+  });
+}
+
+// Split-phase sharded factorization / solve: the same kernels and the same
+// pack / unpack as ncl_shard_refactorize / ncl_shard_solve, with the two
+// collectives (the all-gather of boundary blocks and the final reduction)
+// left to the caller's transport.
+API int ncl_shard_factor_phase_a(ncl_fact_t F, ncl_sym_t M, ncl_shard_t sh, double tol, double* send, int where) {
+  GUARD({
+    shard_factor_a(F, M, sh, tol);
+    pack_blocks(sh, F->F.CB, 0);
+    copy_out(send, sh->send.p, sh->P.cb_chunk, where);
+    if (where == NCL_HOST) ck(cudaStreamSynchronize(g_stream), "sync");
+    check_launch("shard factor phase A");
+  });
+}
+API int ncl_shard_factor_phase_b(ncl_fact_t F, ncl_sym_t M, ncl_shard_t sh, const double* recv, int where,
+                                 int* istat) {
+  GUARD({
+    check_match(M, F->S);
+    DevSymb& d = F->S->d;
+    const int64_t chunk = sh->P.cb_chunk;
+    if (sh->P.world > 1 && chunk > 0)
+      unpack_blocks(sh, F->F.CB, 0, d.flags, d.epoch, stage_in(sh, recv, chunk * sh->P.world, where));
+    shard_factor_b(F, M, sh);
+    ck(cudaMemcpyAsync(istat, F->istat.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, g_stream), "D2H");
+    ck(cudaStreamSynchronize(g_stream), "sync");
+    check_launch("shard factor phase B");
+  });
+}
+API int ncl_shard_set_status(ncl_fact_t F, const int* istat) {
+  GUARD(ck(cudaMemcpyAsync(F->istat.p, istat, 4 * sizeof(int), cudaMemcpyHostToDevice, g_stream), "H2D");
+        ck(cudaStreamSynchronize(g_stream), "sync"));
+}
+API int ncl_shard_solve_phase_a(ncl_fact_t F, ncl_shard_t sh, double* x, int where, double* send, int swhere) {
+  GUARD({
+    shard_solve_a(F, sh, x, where);
+    pack_blocks(sh, F->F.CV, 1);
+    copy_out(send, sh->send.p, sh->P.cv_chunk, swhere);
+    if (swhere == NCL_HOST) ck(cudaStreamSynchronize(g_stream), "sync");
+    check_launch("shard solve phase A");
+  });
+}
+API int ncl_shard_solve_phase_b(ncl_fact_t F, ncl_shard_t sh, double* x, int where, const double* recv, int rwhere) {
+  GUARD({
+    DevSymb& d = F->S->d;
+    const int64_t chunk = sh->P.cv_chunk;
+    double* dx = shard_x(F, x, where);
+    if (sh->P.world > 1 && chunk > 0)
+      unpack_blocks(sh, F->F.CV, 1, d.flags + d.nsn, d.epoch, stage_in(sh, recv, chunk * sh->P.world, rwhere));
+    shard_solve_b(F, sh, dx);
+    const int n = F->S->core.n;
+    if (where == NCL_HOST && n > 0) {
+      ck(cudaMemcpyAsync(x, dx, n * sizeof(double), cudaMemcpyDeviceToHost, g_stream), "D2H");
+      ck(cudaStreamSynchronize(g_stream), "sync");
+    }
+    check_launch("shard solve phase B");
+  });
+}
+API int ncl_shard_diagonal(ncl_fact_t F, ncl_shard_t sh, double* d) {
+  GUARD({
+    if (sh->S != F->S) throw Error{NCL_E_INVALID, "shard plan built for another symbolic factor"};
+    const int n = F->S->core.n;
+    if (n > 0) ck(cudaMemcpyAsync(d, F->D.p, n * sizeof(double), cudaMemcpyDeviceToHost, g_stream), "D2H");
+    ck(cudaStreamSynchronize(g_stream), "sync");
+    const double nan = std::numeric_limits<double>::quiet_NaN();
+    if (sh->P.world > 1)
+      for (int k = 0; k < n; ++k)
+        if (!sh->P.col_report[k]) d[k] = nan;
   });
 }
 
@@ -1441,6 +1590,7 @@ API int ncl_shard_refactorize_emulated(ncl_fact_t F, ncl_sym_t M, ncl_shard_t* p
     for (int r = 0; r < G; ++r) dev_factor_list(d, F->F, M->vals.p, plans[r]->ftA, r, g_stream);
     dev_factor_list(d, F->F, M->vals.p, plans[0]->ftB, G, g_stream);
     dev_inertia(d, F->F, g_stream);
+    F->sharded_world = 1;
     check_launch("emulated shard factorize");
   });
 }
@@ -1449,25 +1599,15 @@ API int ncl_shard_refactorize_emulated(ncl_fact_t F, ncl_sym_t M, ncl_shard_t* p
 API int ncl_shard_solve(ncl_fact_t F, ncl_shard_t sh, double* x, int where) {
   GUARD({
     need_comm(sh);
-    shard_upload(sh);
-    const int n = F->S->core.n;
-    double* dx = x;
-    if (where == NCL_HOST) {
-      ck(cudaMemcpyAsync(F->work1.p, x, n * sizeof(double), cudaMemcpyHostToDevice, g_stream), "H2D");
-      dx = F->work1.p;
-    }
+    shard_solve_a(F, sh, x, where);
     DevSymb& d = F->S->d;
-    dev_solve_begin(d, g_stream);
-    dev_solve_fwd_list(d, F->F, dx, tasks_A(sh), 0, g_stream);
+    double* dx = shard_x(F, x, where);
     if (sh->P.world > 1) allgather_blocks(sh, F->F.CV, 1, d.flags + d.nsn, d.epoch);
-    dev_solve_fwd_list(d, F->F, dx, tasks_B(sh), 1, g_stream);
-    dev_solve_bwd_list(d, F->F, dx, tasks_B(sh), 2, g_stream);
-    dev_solve_bwd_list(d, F->F, dx, tasks_A(sh), 3, g_stream);
-    if (sh->P.world > 1) {
-      dev_zero_indexed(dx, sh->unrep.p, sh->nunrep, g_stream);
-      nck(g_nccl.all_reduce(dx, dx, n, ncclFloat64, ncclSum, g_nccl.comm, g_stream), "allreduce x");
-    }
-    if (where == NCL_HOST) {
+    shard_solve_b(F, sh, dx);
+    if (sh->P.world > 1) nck(g_nccl.all_reduce(dx, dx, F->S->core.n, ncclFloat64, ncclSum, g_nccl.comm, g_stream),
+                             "allreduce x");
+    const int n = F->S->core.n;
+    if (where == NCL_HOST && n > 0) {
       ck(cudaMemcpyAsync(x, dx, n * sizeof(double), cudaMemcpyDeviceToHost, g_stream), "D2H");
       ck(cudaStreamSynchronize(g_stream), "sync");
     }

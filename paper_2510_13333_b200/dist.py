@@ -31,6 +31,12 @@ register({
     "ncl_shard_refactorize": (i32, [P, P, P, C.c_double]),
     "ncl_shard_solve": (i32, [P, P, P, i32]),
     "ncl_shard_refactorize_emulated": (i32, [P, P, P, i32, C.c_double]),
+    "ncl_shard_factor_phase_a": (i32, [P, P, P, C.c_double, P, i32]),
+    "ncl_shard_factor_phase_b": (i32, [P, P, P, P, i32, P]),
+    "ncl_shard_set_status": (i32, [P, P]),
+    "ncl_shard_solve_phase_a": (i32, [P, P, P, i32, P, i32]),
+    "ncl_shard_solve_phase_b": (i32, [P, P, P, i32, P, i32]),
+    "ncl_shard_diagonal": (i32, [P, P, P]),
     "ncl_scopf_var_groups": (i32, [P, P]),
 })
 
@@ -110,11 +116,52 @@ class ShardPlan:
     def solve_in_place(self, F, x, where: int = HOST) -> None:
         check(lib.ncl_shard_solve(F.handle, self._h, _ptr(x), where))
 
+    # split-phase form (include/nclopf_dist.h): the caller moves the bytes
+    @staticmethod
+    def _where(a) -> int:
+        return DEVICE if (hasattr(a, "is_cuda") and a.is_cuda) else HOST
+
+    def factor_phase_a(self, F, M, send, pivot_tol: float = 1e-12) -> None:
+        """own + base-only supernodes, boundary CBs packed into send (cb_chunk doubles)"""
+        check(lib.ncl_shard_factor_phase_a(F.handle, M.handle, self._h, float(pivot_tol), _ptr(send),
+                                           self._where(send)))
+
+    def factor_phase_b(self, F, M, recv) -> np.ndarray:
+        """unpack the all-gathered blocks (world * cb_chunk), separator; returns
+        this rank's [zero-pivot position, npos, nneg, nzero]"""
+        ist = np.zeros(4, np.int32)
+        check(lib.ncl_shard_factor_phase_b(F.handle, M.handle, self._h, _ptr(recv), self._where(recv), _ptr(ist)))
+        return ist
+
+    @staticmethod
+    def set_status(F, istat) -> None:
+        ist = np.ascontiguousarray(istat, np.int32)
+        check(lib.ncl_shard_set_status(F.handle, _ptr(ist)))
+
+    def solve_phase_a(self, F, x, send) -> None:
+        check(lib.ncl_shard_solve_phase_a(F.handle, self._h, _ptr(x), self._where(x), _ptr(send), self._where(send)))
+
+    def solve_phase_b(self, F, x, recv) -> None:
+        check(lib.ncl_shard_solve_phase_b(F.handle, self._h, _ptr(x), self._where(x), _ptr(recv), self._where(recv)))
+
+    def diagonal(self, F) -> np.ndarray:
+        """D by pivot position on the columns this rank reports, NaN elsewhere"""
+        d = np.empty(F._n, np.float64)
+        check(lib.ncl_shard_diagonal(F.handle, self._h, _ptr(d)))
+        return d
+
+
+def combine_status(istats) -> np.ndarray:
+    """the reduction ncl_shard_refactorize does with NCCL: min of the zero-pivot
+    position, sums of the inertia counts"""
+    a = np.asarray(istats, np.int64)
+    return np.array([a[:, 0].min(), a[:, 1].sum(), a[:, 2].sum(), a[:, 3].sum()], np.int32)
+
 
 def refactorize_emulated(F, M, plans, pivot_tol: float = 1e-12) -> None:
     arr = (C.c_void_p * len(plans))(*[p.handle.value for p in plans])
     check(lib.ncl_shard_refactorize_emulated(F.handle, M.handle, arr, len(plans), float(pivot_tol)))
 
 
-__all__ = ["ShardPlan", "ShardInfo", "var_groups", "init_nccl", "finalize_nccl", "refactorize_emulated",
+__all__ = ["ShardPlan", "ShardInfo", "combine_status", "var_groups", "init_nccl", "finalize_nccl", "refactorize_emulated",
            "DEVICE", "HOST"]

@@ -153,3 +153,175 @@ def test_world1_shard_path_bitwise(gpu):
     x2 = b.copy()
     plan.solve_in_place(F2, x2)
     assert np.array_equal(x1, x2)
+
+
+def _assembled(grid, K, seed):
+    s, M, kk, S = _problem(grid, K)
+    rng = np.random.default_rng(seed)
+    kk.assemble(rng.standard_normal(M.nnzh) * 0.1, rng.standard_normal(M.nnzj), 1.0 + rng.random(s.n), 0.0,
+                10.0 + rng.random(M.m))
+    return s, M, kk, S
+
+
+def _split_phase_world(s, A, S, G, rng):
+    """One process drives G ranks through the split-phase API: every rank has
+    its own symbolic copy (own completion flags), factor and plan; the
+    all-gathers are device copies of the ranks' send chunks, laid out as
+    ncclAllGather lays them out. Returns the per-rank D / x and combined istat."""
+    import torch
+    from paper_2510_13333_b200 import _lib
+    from paper_2510_13333_b200.dist import combine_status
+
+    def sync():  # torch's stream <-> the library's stream (ncl_stream)
+        torch.cuda.synchronize()
+        _lib.check(_lib.lib.ncl_synchronize())
+
+    perm = S.perm
+    Ss = [S] + [ps.analyze(A, perm) for _ in range(G - 1)]
+    groups = var_groups(s)
+    plans = [ShardPlan(Ss[r], groups, s.K + 1, G, r) for r in range(G)]
+    Fs = [ps.factorize(A, Ss[r]) for r in range(G)]  # allocation (and a throw-away unsharded factor)
+    info = plans[0].info()
+    dev = torch.device("cuda")
+    sends = [torch.full((max(1, info.cb_chunk),), float("nan"), dtype=torch.float64, device=dev) for _ in range(G)]
+    sync()
+    for r in range(G):
+        plans[r].factor_phase_a(Fs[r], A, sends[r])
+    sync()
+    recv = torch.cat([t[:info.cb_chunk] for t in sends]).contiguous()
+    sync()
+    ist = [plans[r].factor_phase_b(Fs[r], A, recv) for r in range(G)]
+    tot = combine_status(ist)
+    for r in range(G):
+        ShardPlan.set_status(Fs[r], tot)
+    b = rng.standard_normal(s.n)
+    xs = [torch.from_numpy(b.copy()).to(dev) for _ in range(G)]
+    cvs = [torch.full((max(1, info.cv_chunk),), float("nan"), dtype=torch.float64, device=dev) for _ in range(G)]
+    sync()
+    for r in range(G):
+        plans[r].solve_phase_a(Fs[r], xs[r], cvs[r])
+    sync()
+    recv_cv = torch.cat([t[:info.cv_chunk] for t in cvs]).contiguous()
+    sync()
+    for r in range(G):
+        plans[r].solve_phase_b(Fs[r], xs[r], recv_cv)
+    sync()
+    x = xs[0].clone()
+    for r in range(1, G):
+        x += xs[r]  # the all-reduce(sum) of ncl_shard_solve: every entry has one non-zero term
+    D = [plans[r].diagonal(Fs[r]) for r in range(G)]
+    return plans, Fs, D, b, x.cpu().numpy(), tot
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("grid,K,G", [("case118", 8, 2), ("activsg500", 16, 4), ("activsg500", 256, 8)])
+def test_split_phase_exchange_bitwise(gpu, grid, K, G):
+    """pack -> exchange -> unpack through the library (the NCCL all-gather
+    replaced by device copies): every rank's reported D, the combined inertia
+    and the summed x are bitwise the unsharded factor's / solve's."""
+    s, M, kk, S = _assembled(grid, K, 5)
+    A = kk.matrix
+    F1 = ps.factorize(A, S)
+    D1 = F1.diagonal()
+    rng = np.random.default_rng(6)
+    plans, Fs, D, b, x, tot = _split_phase_world(s, A, S, G, rng)
+    got = np.full(s.n, np.nan)
+    for r in range(G):
+        m = ~np.isnan(D[r])
+        assert not np.any(~np.isnan(got[m])), "a pivot reported by two ranks"
+        got[m] = D[r][m]
+    assert np.array_equal(got, D1)
+    assert all(F.status == "ok" for F in Fs)
+    assert Fs[0].inertia == F1.inertia
+    assert np.array_equal(x, F1.solve(b))
+    # the whole-factor getters refuse a sharded factor
+    from paper_2510_13333_b200._lib import NclError
+    with pytest.raises(NclError):
+        Fs[1].diagonal()
+    with pytest.raises(NclError):
+        Fs[1].solve(b)
+
+
+@pytest.mark.gpu
+def test_split_phase_exchange_500x1024_g8(gpu):
+    """BASELINE configs[4]: the 500-bus x 1024-contingency KKT split 8 ways
+    (128 contingencies per rank), bitwise against the unsharded factor."""
+    s, M, kk, S = _assembled("activsg500", 1024, 7)
+    A = kk.matrix
+    F1 = ps.factorize(A, S)
+    D1 = F1.diagonal()
+    plans, Fs, D, b, x, tot = _split_phase_world(s, A, S, 8, np.random.default_rng(8))
+    got = np.where(np.isnan(D[0]), 0.0, D[0])
+    for r in range(1, 8):
+        got = np.where(np.isnan(D[r]), got, D[r])
+    assert np.array_equal(got, D1)
+    assert Fs[0].inertia == F1.inertia
+    assert np.array_equal(x, F1.solve(b))
+
+
+def _two_process_worker(rank, world, port, q):
+    """one rank of a world-2 run on ONE GPU: the library's pack / unpack with a
+    host-staged gloo all-gather as the transport (NCCL refuses two ranks on one
+    device), then the gloo reductions of istat and x."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2510_13333_b200 import _lib
+        _lib.check(_lib.lib.ncl_init(0))
+        s, M, kk, S = _assembled("case118", 8, 9)
+        A = kk.matrix
+        F1 = ps.factorize(A, S)
+        F = ps.factorize(A, ps.analyze(A, S.perm))
+        plan = ShardPlan(F._symb, var_groups(s), s.K + 1, world, rank)
+        info = plan.info()
+        send = np.zeros(info.cb_chunk)
+        plan.factor_phase_a(F, A, send)
+        parts = [torch.zeros(info.cb_chunk, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(send))
+        ist = plan.factor_phase_b(F, A, torch.cat(parts).numpy())
+        t = torch.from_numpy(ist.astype(np.int64))
+        zp = t[:1].clone()
+        dist.all_reduce(zp, op=dist.ReduceOp.MIN)
+        cnt = t[1:].clone()
+        dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
+        ShardPlan.set_status(F, np.concatenate([zp.numpy(), cnt.numpy()]))
+        D = plan.diagonal(F)
+        m = ~np.isnan(D)
+        okD = bool(np.array_equal(D[m], F1.diagonal()[m]))
+        b = np.random.default_rng(10).standard_normal(s.n)
+        x = b.copy()
+        cv = np.zeros(info.cv_chunk)
+        plan.solve_phase_a(F, x, cv)
+        parts = [torch.zeros(info.cv_chunk, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(cv))
+        plan.solve_phase_b(F, x, torch.cat(parts).numpy())
+        xt = torch.from_numpy(x)
+        dist.all_reduce(xt, op=dist.ReduceOp.SUM)
+        okx = bool(np.array_equal(xt.numpy(), F1.solve(b)))
+        q.put((rank, okD, okx, F.inertia == F1.inertia, int(m.sum()), int(info.n_boundary)))
+    except Exception as e:  # report instead of hanging the parent
+        q.put((rank, repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_split_phase_two_processes_one_gpu(gpu):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 30500 + (os.getpid() % 1000)
+    procs = [ctx.Process(target=_two_process_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert all(len(r) == 6 for r in res), res
+    assert all(r[1] and r[2] and r[3] for r in res), res
+    s, M, kk, S = _problem("case118", 8)
+    assert res[0][4] + res[1][4] == s.n  # the ranks' reported pivots partition the columns
+    assert res[0][5] > 0
