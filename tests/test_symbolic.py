@@ -125,3 +125,20 @@ def test_high_degree_nodes_bit_exact(seed):
     v = rng.standard_normal(len(r))
     A, B = both(n, np.array(r), np.array(c), v)
     assert_symbolic_equal(A, B)
+
+
+@pytest.mark.parametrize("grid,K", [("case118", 16), ("activsg500", 16)])
+def test_scopf_kkt_symbolic_bit_exact(grid, K):
+    """The condensed SCOPF KKT pattern itself (the bench / solve matrix):
+    perm, etree, permuted pattern, entry map and column counts identical to
+    the reference's symbolic_order + analyze (a SCOPF pattern was
+    never under test; the 500x256 record is profiles/r02_symbolic_500x256.json)."""
+    from paper_2510_13333_b200.kkt import Kkt
+    from paper_2510_13333_b200.scopf import Scopf
+    s = Scopf(grid, K)
+    A = Kkt(s.build_model()).matrix
+    cp, ri = A.col_ptr(), A.row_ind()
+    n = A.dim()
+    cols = np.repeat(np.arange(n, dtype=np.int32), np.diff(cp))
+    B = RefSparseSym(n, ri, cols, np.ones(len(ri)))
+    assert_symbolic_equal(A, B)
