@@ -360,7 +360,7 @@ API int ncl_sym_write_matrix_market(ncl_sym_t M, char* buf, int64_t cap, int64_t
 struct LayoutDev {
   DevBuf<int> nodes, tptr, prog, bamap;
   DevBuf<uint8_t> bcmap;
-  DevBuf<uint32_t> bcmapw;
+  DevBuf<uint32_t> bcmapw, bsmapw;
   DevBuf<int64_t> bccb;
   DevBuf<int> bcid;
   DevBuf<RegChunk> bchunks;
@@ -433,9 +433,11 @@ void build_batches(const Supernodal& Z, const std::vector<int>& list, int split,
       const int nr = kRegShapes[k][0], per = 32 / kRegShapes[k][2];
       const int np = nr * (nr + 1) / 2, npad = (np + 3) & ~3;
       const int R = kRegShapes[k][2], nw = npad / 4;
+      const size_t chunk0 = B.chunks.size();
       for (size_t x = 0; x < v.size(); x += per)
         B.chunks.push_back(RegChunk{k, static_cast<int>(std::min<size_t>(per, v.size() - x)),
-                                    static_cast<int>(B.inst.size() + x), 0});
+                                    static_cast<int>(B.inst.size() + x), -1});
+      static_assert(kSmapWords * 4 >= 12, "solve row maps cover 12 rows");
       int64_t abase = 0, wbase = 0;  // R == 1: per-chunk blocks interleaved over the 32 lanes
       for (size_t x = 0; x < v.size(); ++x) {
         const int s = v[x];
@@ -447,6 +449,8 @@ void build_batches(const Supernodal& Z, const std::vector<int>& list, int split,
           B.amap.resize(B.amap.size() + static_cast<size_t>(np) * 32, -1);
           wbase = static_cast<int64_t>(B.cmapw.size());
           B.cmapw.resize(B.cmapw.size() + static_cast<size_t>(maxnch) * nw * 32, 0xffffffffu);
+          B.chunks[chunk0 + x / 32].smap = static_cast<int>(B.smapw.size());
+          B.smapw.resize(B.smapw.size() + static_cast<size_t>(maxnch) * kSmapWords * 32, 0xffffffffu);
         }
         batched[s] = 1;
         RegInst I{};
@@ -473,6 +477,12 @@ void build_batches(const Supernodal& Z, const std::vector<int>& list, int split,
           const int m2c = nrof(c) - wof(c);
           const int* rel = Z.relp.data() + Z.sn_rptr[c] + wof(c);
           if (R == 1) {
+            // forward solve: parent row rel[kk] <- the child's CV entry kk
+            const int64_t sb = B.chunks[chunk0 + x / 32].smap;
+            for (int kk = 0; kk < m2c; ++kk) {
+              uint32_t& wd = B.smapw[sb + (static_cast<int64_t>(qi) * kSmapWords + rel[kk] / 4) * 32 + ix];
+              wd = (wd & ~(0xffu << (8 * (rel[kk] % 4)))) | (static_cast<uint32_t>(kk) << (8 * (rel[kk] % 4)));
+            }
             for (int j = 0; j < m2c; ++j)
               for (int ii = j; ii < m2c; ++ii) {
                 const int64_t pp = cb_col(rel[j], nr) + rel[ii];
@@ -495,6 +505,12 @@ void build_batches(const Supernodal& Z, const std::vector<int>& list, int split,
       }
     }
     if (l == nlev / 2 - 1) B.nchunk1 = static_cast<int>(B.chunks.size());
+  }
+  // backward solve: a front whose parent is batched too waits on the parent's
+  // flag; any other parent finished in an earlier launch
+  for (RegInst& I : B.inst) {
+    const int p = Z.sn_parent[I.s];
+    if (p >= 0 && batched[p]) I.shape |= kRegParentBatched;
   }
 }
 
@@ -541,7 +557,7 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
     for (int q = Z.cptr[s]; q < Z.cptr[s + 1]; ++q) {
       const int c = Z.child[q];
       if (batched[c]) {
-        pr += 4 + (nrof(c) - wof(c));
+        pr += 6 + (nrof(c) - wof(c));
         continue;
       }
       ok = ok && fits[c];
@@ -580,7 +596,7 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
     L.tptr.push_back(static_cast<int>(L.nodes.size()));
     // program: [nnodes, nA, tab, len] [aoff x nA] [asrc x nA] then per node
     // [s, f, w, nr, nch, push_off(-1 = root), a_first, a_cnt, loff lo/hi, cboff lo/hi, rptr lo/hi] and per child
-    // [m2c, stack_off, rel x m2c] ([m2c, -1, cboff lo/hi, rel x m2c] for an external child),
+    // [m2c, stack_off, rel x m2c] ([m2c, -1, cboff lo/hi, cvoff lo/hi, rel x m2c] for an external child),
     // then the record offsets [tab .. tab + nnodes);
     // stack offsets from a postorder simulation
     const size_t base = L.prog.size();
@@ -613,9 +629,14 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
         const int m2c = nrof(c) - wof(c);
         L.prog.push_back(m2c);
         if (batched[c]) {
+          // external child: its CB (factor) and its CV (forward solve) in the
+          // standard layouts
+          const int64_t cv = Z.sn_rptr[c] + wof(c);
           L.prog.push_back(-1);
           L.prog.push_back(static_cast<int>(Z.cb_off[c] & 0xffffffff));
           L.prog.push_back(static_cast<int>(Z.cb_off[c] >> 32));
+          L.prog.push_back(static_cast<int>(cv & 0xffffffff));
+          L.prog.push_back(static_cast<int>(cv >> 32));
         } else {
           L.prog.push_back(cboff[c]);
         }
@@ -741,6 +762,8 @@ DevTasks upload_layout(TaskLayout& L, LayoutDev& D) {
     D.bccb.upload(L.batch.ccb);
     D.bcid.upload(L.batch.cid);
     D.bchunks.upload(L.batch.chunks);
+    D.bsmapw.upload(L.batch.smapw);
+    L.batch.dev_smapw = D.bsmapw.p;
     L.batch.dev_cid = D.bcid.p;
     L.batch.dev_chunks = D.bchunks.p;
     L.batch.dev_inst = D.binst.p;
@@ -1342,14 +1365,6 @@ void shard_upload(ncl_shard* sh) {
   sh->recv.alloc(std::max<int64_t>(1, chunk * sh->P.world));
   sh->dev_ready = true;
 }
-DevTasks tasks_A(ncl_shard* sh) {
-  return DevTasks{sh->listA.p, sh->tA.p, sh->pA.p, sh->gA.p, static_cast<int>(sh->layA.tptr.size()) - 1,
-                  sh->layA.nleaf, sh->layA.split, &sh->layA.top};
-}
-DevTasks tasks_B(ncl_shard* sh) {
-  return DevTasks{sh->listB.p, sh->tB.p, sh->pB.p, sh->gB.p, static_cast<int>(sh->layB.tptr.size()) - 1,
-                  sh->layB.nleaf, sh->layB.split, &sh->layB.top};
-}
 void grow_scratch(ncl_fact* F, ncl_shard* sh) {
   const int64_t nf = std::max(sh->flayA.top.scratch_f, sh->flayB.top.scratch_f);
   const int64_t nw = std::max(sh->flayA.top.scratch_w, sh->flayB.top.scratch_w);
@@ -1430,13 +1445,13 @@ void shard_solve_a(ncl_fact* F, ncl_shard* sh, double* x, int where) {
     ck(cudaMemcpyAsync(dx, x, n * sizeof(double), cudaMemcpyHostToDevice, g_stream), "H2D");
   DevSymb& d = F->S->d;
   dev_solve_begin(d, g_stream);
-  dev_solve_fwd_list(d, F->F, dx, tasks_A(sh), 0, g_stream);
+  dev_solve_fwd_list(d, F->F, dx, sh->ftA, 0, g_stream);
 }
 void shard_solve_b(ncl_fact* F, ncl_shard* sh, double* dx) {
   DevSymb& d = F->S->d;
-  dev_solve_fwd_list(d, F->F, dx, tasks_B(sh), 1, g_stream);
-  dev_solve_bwd_list(d, F->F, dx, tasks_B(sh), 2, g_stream);
-  dev_solve_bwd_list(d, F->F, dx, tasks_A(sh), 3, g_stream);
+  dev_solve_fwd_list(d, F->F, dx, sh->ftB, 1, g_stream);
+  dev_solve_bwd_list(d, F->F, dx, sh->ftB, 2, g_stream);
+  dev_solve_bwd_list(d, F->F, dx, sh->ftA, 3, g_stream);
   // every rank keeps only the entries it reports: the sum over ranks is x
   if (sh->P.world > 1) dev_zero_indexed(dx, sh->unrep.p, sh->nunrep, g_stream);
 }

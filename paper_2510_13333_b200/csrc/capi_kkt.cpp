@@ -1,6 +1,7 @@
 // C-ABI for the condensed Newton matrix (K2 assembly).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <memory>
 #include <vector>
 
@@ -25,6 +26,14 @@ struct ncl_kkt {
   DevBuf<int> slot_h, slot_diag, jterm;
   DevBuf<int64_t> jptr;
   DevBuf<double> h, j, s, d;  // host-path staging
+  // compact form (dev_kkt_assemble_compact): term starts (uint32), terms as
+  // J position + uint8 partner offset, J-entry rows, diagonal-slot bitmask +
+  // per-word rank; unused (compact = false) when a term's offset exceeds 255
+  bool compact = false;
+  DevBuf<uint32_t> tp;
+  DevBuf<int> ta, jrow, dgrank;
+  DevBuf<uint8_t> td;
+  DevBuf<uint64_t> dgmask;
 };
 
 namespace {
@@ -35,7 +44,50 @@ void kkt_upload(ncl_kkt* k) {
   k->slot_diag.upload(k->map.slot_diag);
   k->jptr.upload(k->map.jptr);
   k->jterm.upload(k->map.jterm);
+  // compact form (NCL_KKT_GATHER=1 keeps the per-slot gather kernel: A/B only)
+  static const bool gather = std::getenv("NCL_KKT_GATHER") != nullptr;
+  const KktMap& M = k->map;
+  const int64_t nnz = static_cast<int64_t>(M.slot_h.size()), nt = M.jptr.empty() ? 0 : M.jptr.back();
+  bool ok = !gather && nt < (int64_t(1) << 32) && M.nnzj < (int64_t(1) << 31);
+  std::vector<uint32_t> tp(nnz + 1);
+  std::vector<int> ta(nt), jrow(M.nnzj, 0), dgrank((nnz + 63) / 64 + 1, 0);
+  std::vector<uint8_t> td(nt);
+  std::vector<uint64_t> dgmask((nnz + 63) / 64 + 1, 0);
+  for (int64_t s = 0; ok && s <= nnz; ++s) tp[s] = static_cast<uint32_t>(M.jptr[s]);
+  for (int64_t t = 0; ok && t < nt; ++t) {
+    const int r = M.jterm[3 * t], a = M.jterm[3 * t + 1], b = M.jterm[3 * t + 2];
+    if (a - b < 0 || a - b > 255) ok = false;
+    ta[t] = a;
+    td[t] = static_cast<uint8_t>(a - b);
+    jrow[a] = r;
+    jrow[b] = r;
+  }
+  int next = 0;  // diagonal slots carry variables 0, 1, 2, ... in slot order
+  for (int64_t s = 0; ok && s < nnz; ++s)
+    if (M.slot_diag[s] >= 0) {
+      if (M.slot_diag[s] != next++) ok = false;
+      dgmask[s >> 6] |= 1ull << (s & 63);
+    }
+  for (size_t w = 1; ok && w < dgmask.size(); ++w) dgrank[w] = dgrank[w - 1] + __builtin_popcountll(dgmask[w - 1]);
+  k->compact = ok;
+  if (ok) {
+    k->tp.upload(tp);
+    k->ta.upload(ta);
+    k->td.upload(td);
+    k->jrow.upload(jrow);
+    k->dgmask.upload(dgmask);
+    k->dgrank.upload(dgrank);
+  }
   k->dev_ready = true;
+}
+void assemble(ncl_kkt* K, const double* hess, const double* jac, const double* sigx, double dw, const double* D,
+              double* out) {
+  const int64_t nnz = K->K->pat.nnz();
+  if (K->compact)
+    dev_kkt_assemble_compact(nnz, K->slot_h.p, K->dgmask.p, K->dgrank.p, K->tp.p, K->ta.p, K->td.p, K->jrow.p, hess,
+                             jac, sigx, dw, D, out, g_stream);
+  else
+    dev_kkt_assemble(nnz, K->slot_h.p, K->slot_diag.p, K->jptr.p, K->jterm.p, hess, jac, sigx, dw, D, out, g_stream);
 }
 }  // namespace
 
@@ -69,10 +121,8 @@ API int ncl_kkt_assemble(ncl_kkt_t K, const double* hess, const double* jac, con
   GUARD({
     kkt_upload(K);
     const KktMap& m = K->map;
-    const int64_t nnz = K->K->pat.nnz();
     if (where == NCL_DEVICE) {
-      dev_kkt_assemble(nnz, K->slot_h.p, K->slot_diag.p, K->jptr.p, K->jterm.p, hess, jac, sigx, dw, D,
-                       K->K->vals.p, g_stream);
+      assemble(K, hess, jac, sigx, dw, D, K->K->vals.p);
       check_launch("kkt_assemble");
       return NCL_OK;
     }
@@ -84,8 +134,7 @@ API int ncl_kkt_assemble(ncl_kkt_t K, const double* hess, const double* jac, con
     put(K->j, jac, m.nnzj);
     put(K->s, sigx, m.n);
     put(K->d, D, m.m);
-    dev_kkt_assemble(nnz, K->slot_h.p, K->slot_diag.p, K->jptr.p, K->jterm.p, K->h.p, K->j.p, K->s.p, dw, K->d.p,
-                     K->K->vals.p, g_stream);
+    assemble(K, K->h.p, K->j.p, K->s.p, dw, K->d.p, K->K->vals.p);
     check_launch("kkt_assemble");
     ck(cudaStreamSynchronize(g_stream), "sync");
   });

@@ -66,13 +66,18 @@ struct alignas(16) RegInst {
                         // (word w of child q at cmap + (q * words + w) * 32), and the A map interleaved the
                         // same way (entry p at amap + 32 p): coalesced
   int64_t ccb;          // offset of the children's CB offsets (int64 each) and supernode ids (int each)
-  int s, f, nch, shape;  // shape = kRegShapes index
+  int s, f, nch, shape;  // shape = kRegShapes index | kRegParentBatched
   int cid[4];            // the first four children inline (supernode ids, CB offsets): one round trip less
   int64_t cb[4];
 };
+constexpr int kRegParentBatched = 1 << 8;  // RegInst::shape flag: the parent is a register front too
 struct RegChunk {
-  int shape, n, first, pad;  // n fronts inst[first .. first + n) of one shape
+  int shape, n, first;  // n fronts inst[first .. first + n) of one shape
+  int smap;             // word offset of the chunk's forward-solve row maps in smapw: for front lane l and
+                        // child q, word w (rows 4w .. 4w + 3) at smap + (q * kSmapWords + w) * 32 + l holds the
+                        // child's CV entry index per parent row (255 = none)
 };
+constexpr int kSmapWords = 3;  // rows of a register front <= 12
 struct BatchSched {
   std::vector<RegInst> inst;
   std::vector<int> amap;
@@ -80,6 +85,7 @@ struct BatchSched {
   std::vector<uint32_t> cmapw;
   std::vector<int64_t> ccb;
   std::vector<int> cid;      // children's supernode ids (same index as ccb)
+  std::vector<uint32_t> smapw;   // forward-solve row maps (RegChunk::smap)
   std::vector<RegChunk> chunks;  // tier-1 chunks in level order, then tier-2 chunks in level order
   int nchunk1 = 0;               // chunks of tier 1
   int64_t nodes = 0;         // supernodes covered
@@ -90,6 +96,7 @@ struct BatchSched {
   const int64_t* dev_ccb = nullptr;
   const int* dev_cid = nullptr;
   const RegChunk* dev_chunks = nullptr;
+  const uint32_t* dev_smapw = nullptr;
 };
 // Per child slot q of the children CSR (child[q]): what a parent needs to
 // extend-add that child's contribution block (one 16-byte load)
@@ -254,6 +261,11 @@ void dev_frob_sq(const DevPattern& P, const int* colptr, const int* rowind, cons
 int dev_num_sms();
 void dev_gather_sum(int64_t nslots, const int* ptr, const int* idx, const double* src, double* dst,
                     cudaStream_t st);
+// compact K2 (csrc/cuda/assemble.cu): bitwise the same K as dev_kkt_assemble
+void dev_kkt_assemble_compact(int64_t nnz, const int* slot_h, const uint64_t* dgmask, const int* dgrank,
+                              const uint32_t* tp, const int* ta, const uint8_t* td, const int* jrow, const double* H,
+                              const double* J, const double* sigx, double dw, const double* D, double* K,
+                              cudaStream_t st);
 void dev_kkt_assemble(int64_t nnz, const int* slot_h, const int* slot_diag, const int64_t* jptr, const int* jterm,
                       const double* H, const double* J, const double* sigx, double dw, const double* D, double* K,
                       cudaStream_t st);

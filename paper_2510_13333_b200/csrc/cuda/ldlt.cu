@@ -984,7 +984,7 @@ __device__ __forceinline__ void group_task(const FactorArgs& a, int g, int lane,
       const double* Cc = stack + off;
       if (off < 0) {  // external child (register-front phase): its CB in the standard layout
         Cc = a.CB + (static_cast<int64_t>(static_cast<uint32_t>(PG[p + 2])) | (static_cast<int64_t>(PG[p + 3]) << 32));
-        p += 2;
+        p += 4;  // + CB offset, CV offset
       }
       const int reli = lane < m2c ? PG[p + 2 + lane] : 0;
       extend_add_flat(F, nr, Cc, m2c, reli, lane);
@@ -1351,8 +1351,14 @@ __device__ void fwd_group(const SolveArgs& a, int g, int lane, double* VS, doubl
     __syncwarp();
     for (int q = 0; q < nch; ++q) {
       const int m2c = PG[p], off = PG[p + 1];
-      if (lane < m2c) VS[PG[p + 2 + lane]] += ST[off + lane];
-      p += 2 + m2c;
+      if (off < 0) {  // external child (register-front phase): its CV in the standard layout
+        const int64_t cv = rec64(PG + p + 4);
+        if (lane < m2c) VS[PG[p + 6 + lane]] += __ldcg(a.CV + cv + lane);
+        p += 6 + m2c;
+      } else {
+        if (lane < m2c) VS[PG[p + 2 + lane]] += ST[off + lane];
+        p += 2 + m2c;
+      }
       __syncwarp();
     }
     const double* P = a.L + loff;
@@ -1881,6 +1887,144 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 8 : 4) bwd_ker
   }
 }
 
+// ---------------------------------------------------------------------------
+// Register-resident solves of the batched tiny-front forest (BatchSched, the
+// same forest reg_factor_kernel factors): one thread per front of a
+// compile-time shape (NR rows, W pivots). Forward, in the factor's chunk
+// order (children first): b through the permutation, the children's
+// contribution vectors extend-added in ascending child order (relative rows
+// from relp, every load of a child issued together), the unit-lower solve of
+// the W columns, x1 to xp and -L21 x1 to the front's CV. Backward, chunks in
+// reverse order (parents first): the ancestor values gathered through the
+// row list, T = L21^T x2, then the unit-upper block with D^{-1} fused and the
+// result scattered through the permutation. Same operations, in the same
+// order, as fwd_group / bwd_warp_reg do for a node.
+// ---------------------------------------------------------------------------
+template <int NR, int W>
+__device__ __forceinline__ void reg_fwd_front(const SolveArgs& a, const RegInst& I, const int* __restrict__ cid,
+                                              const uint32_t* __restrict__ smap) {
+  const DevSymb& S = a.S;
+  const int64_t rb = __ldg(S.sn_rptr + I.s);
+  const int q0 = __ldg(S.cptr + I.s);
+  double P[W][NR];
+  const double* Pg = a.L + I.loff;
+#pragma unroll
+  for (int c = 0; c < W; ++c)
+#pragma unroll
+    for (int i = c + 1; i < NR; ++i) P[c][i] = __ldg(Pg + c * NR + i);
+  double v[NR];
+#pragma unroll
+  for (int i = 0; i < NR; ++i) v[i] = i < W ? __ldcg(a.b + __ldg(S.perm + I.f + i)) : 0.0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (q < I.nch) wait_flag(a.flags + I.cid[q], a.epoch);
+  for (int q = 4; q < I.nch; ++q) wait_flag(a.flags + __ldg(cid + I.ccb + q), a.epoch);
+  static_assert(NR <= 4 * kSmapWords, "solve row map words");
+  constexpr int NW = (NR + 3) / 4;
+  for (int q = 0; q < I.nch; ++q) {
+    const int rel = S.chrec[q0 + q].rel;
+    uint32_t mw[NW];
+#pragma unroll
+    for (int w4 = 0; w4 < NW; ++w4) mw[w4] = __ldg(smap + (q * kSmapWords + w4) * 32);
+    // per parent row (constant index) the child's CV entry or none: v stays
+    // in registers, every load of the child in flight together
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      const uint32_t k = (mw[i >> 2] >> (8 * (i & 3))) & 0xffu;
+      if (k != 0xffu) v[i] += __ldcg(a.CV + rel + k);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < W; ++c) {
+    const double xc = v[c];
+#pragma unroll
+    for (int i = c + 1; i < NR; ++i) v[i] -= P[c][i] * xc;
+  }
+#pragma unroll
+  for (int i = 0; i < NR; ++i) {
+    if (i < W) a.xp[I.f + i] = v[i];
+    else a.CV[rb + i] = v[i];
+  }
+  st_release(a.flags + I.s, a.epoch);  // release: orders this thread's writes
+}
+
+template <int NR, int W>
+__device__ __forceinline__ void reg_bwd_front(const SolveArgs& a, const RegInst& I) {
+  const DevSymb& S = a.S;
+  const int ps = __ldg(S.sn_parent + I.s);
+  const int64_t rb = __ldg(S.sn_rptr + I.s);
+  int ri[NR];
+  double P[W][NR], d[W], xs[W];
+  int pl[W];
+  const double* Pg = a.L + I.loff;
+#pragma unroll
+  for (int i = W; i < NR; ++i) ri[i] = __ldg(S.rows + rb + i);
+#pragma unroll
+  for (int c = 0; c < W; ++c) {
+#pragma unroll
+    for (int i = 0; i < NR; ++i) P[c][i] = (i > c) ? __ldg(Pg + c * NR + i) : 0.0;
+    d[c] = __ldg(a.D + I.f + c);
+    pl[c] = __ldg(S.perm + I.f + c);
+    xs[c] = __ldcg(a.xp + I.f + c);
+  }
+  // only a batched parent can still be running (every other parent finished
+  // in an earlier launch, and group members publish no backward flags)
+  if (I.shape & kRegParentBatched) wait_flag(a.flags + ps, a.epoch);
+  double xi[NR];
+#pragma unroll
+  for (int i = W; i < NR; ++i) xi[i] = __ldcg(a.xp + ri[i]);
+  double T[W];
+#pragma unroll
+  for (int c = 0; c < W; ++c) {
+    double acc = 0.0;
+#pragma unroll
+    for (int i = W; i < NR; ++i) acc += P[c][i] * xi[i];
+    T[c] = acc;
+  }
+#pragma unroll
+  for (int c = W - 1; c >= 0; --c) {
+    const double vv = divz(xs[c], d[c]) - T[c];
+    a.xp[I.f + c] = vv;
+    a.x[pl[c]] = vv;
+#pragma unroll
+    for (int c2 = 0; c2 < c; ++c2) T[c2] += P[c2][c] * vv;
+  }
+  st_release(a.flags + I.s, a.epoch);
+}
+
+template <bool FWD, int... K>
+__device__ __forceinline__ void reg_solve_dispatch(const SolveArgs& a, const RegChunk& ch, int lane,
+                                                   const RegInst* __restrict__ inst, const int* cid,
+                                                   const uint32_t* smapw, std::integer_sequence<int, K...>) {
+  (((ch.shape == K) ? [&] {
+    constexpr int NR = kRegShapes[K][0], W = kRegShapes[K][1];
+    static_assert(kRegShapes[K][2] == 1, "register-front solves assume one thread per front");
+    if (lane < ch.n) {
+      const RegInst I = inst[ch.first + lane];
+      if constexpr (FWD) reg_fwd_front<NR, W>(a, I, cid, smapw + ch.smap + lane);
+      else reg_bwd_front<NR, W>(a, I);
+    }
+  }()
+                    : void()),
+   ...);
+}
+
+template <bool FWD>
+__global__ void __launch_bounds__(128) reg_solve_kernel(SolveArgs a, const RegInst* __restrict__ inst,
+                                                        const RegChunk* __restrict__ chunks, int nchunk,
+                                                        const int* __restrict__ cid,
+                                                        const uint32_t* __restrict__ smapw) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    int c = 0;
+    if (lane == 0) c = atomicAdd(a.ticket, 1);
+    c = __shfl_sync(kFull, c, 0);
+    if (c >= nchunk) break;
+    const RegChunk ch = chunks[FWD ? c : nchunk - 1 - c];
+    reg_solve_dispatch<FWD>(a, ch, lane, inst, cid, smapw, std::make_integer_sequence<int, kNumRegShapes>{});
+  }
+}
+
 // SpMV in the reference accumulation order (sparse_sym.cpp:105-115), no FMA.
 __global__ void spmv_kernel(int n, const int64_t* __restrict__ ptr, const int* __restrict__ vi,
                             const int* __restrict__ ci, const double* __restrict__ v, const double* __restrict__ x,
@@ -2162,11 +2306,29 @@ void dev_solve_begin(const DevSymb& S0, cudaStream_t st) {
   cudaMemsetAsync(S.tickets, 0, kTickets * sizeof(int), st);
 }
 
+// the batched forest of a task list (one launch; its chunks, children first)
+static void reg_solve(const DevSymb& S, const BatchSched& bs, SolveArgs a, bool fwd, cudaStream_t st) {
+  static int grid = 0;
+  if (!grid) grid = persistent_grid(reg_solve_kernel<true>, 128, 1 << 30);
+  const int n = static_cast<int>(bs.chunks.size());
+  if (n == 0) return;
+  a.ticket = S.tickets + kTickets - (fwd ? 4 : 5);
+  cudaMemsetAsync(a.ticket, 0, sizeof(int), st);
+  COUNT(1);
+  if (fwd)
+    reg_solve_kernel<true><<<std::min(grid, (n + 3) / 4), 128, 0, st>>>(a, bs.dev_inst, bs.dev_chunks, n, bs.dev_cid,
+                                                                       bs.dev_smapw);
+  else
+    reg_solve_kernel<false><<<std::min(grid, (n + 3) / 4), 128, 0, st>>>(a, bs.dev_inst, bs.dev_chunks, n,
+                                                                        bs.dev_cid, bs.dev_smapw);
+}
+
 void dev_solve_fwd_list(const DevSymb& S, DevFactor& F, const double* b, const DevTasks& T, int slot,
                         cudaStream_t st) {
-  if (T.n == 0) return;
+  if (T.n == 0 && !T.batch) return;
   SolveArgs fa{S, F.L, F.D, F.CV, F.xp, b, nullptr, S.flags + S.nsn, S.tickets + 2 * slot, S.epoch, 0, T.split,
                T.ids, T.tptr, T.prog, T.gpo, T.nleaf, g_solve_trace};
+  if (T.batch) reg_solve(S, *T.batch, fa, true, st);
   if (T.split > 0) COUNT(1), fwd_kernel<32><<<g_sf, 128, kSolSmem, st>>>(fa);
   if (T.split < T.n) {
     fa.ticket = S.tickets + 2 * slot + 1;
@@ -2179,9 +2341,10 @@ void dev_solve_fwd_list(const DevSymb& S, DevFactor& F, const double* b, const D
 
 // backward over one list, roots first (the CTA part first, then the warp part)
 void dev_solve_bwd_list(const DevSymb& S, DevFactor& F, double* x, const DevTasks& T, int slot, cudaStream_t st) {
-  if (T.n == 0) return;
+  if (T.n == 0 && !T.batch) return;
   SolveArgs ba{S, F.L, F.D, F.CV, F.xp, nullptr, x, S.flags + 2 * S.nsn, S.tickets + 2 * slot, S.epoch, T.split,
                T.n, T.ids, T.tptr, T.prog, T.gpo, T.nleaf, g_solve_trace ? g_solve_trace + 2 * T.n : nullptr};
+
   if (T.split < T.n) COUNT(1), bwd_kernel<256><<<std::min(g_sb2, T.n - T.split), 256, 0, st>>>(ba);
   if (T.split > 0) {
     ba.ticket = S.tickets + 2 * slot + 1;
@@ -2190,6 +2353,8 @@ void dev_solve_bwd_list(const DevSymb& S, DevFactor& F, double* x, const DevTask
     COUNT(1);
     bwd_kernel<32><<<g_sb, 128, kSolSmem, st>>>(ba);
   }
+  // the batched forest last: every parent is in this list or earlier
+  if (T.batch) reg_solve(S, *T.batch, ba, false, st);
 }
 
 void dev_solve(const DevSymb& S, DevFactor& F, const double* b, double* x, cudaStream_t st) {
@@ -2197,23 +2362,26 @@ void dev_solve(const DevSymb& S, DevFactor& F, const double* b, double* x, cudaS
   // NCL_SOLVE_TRACE=<file>: per-task globaltimer start/end of the 3rd solve
   // (forward then backward, 4 x tasks uint64; debug timeline)
   static const char* trace_path = std::getenv("NCL_SOLVE_TRACE");
+  // NCL_SOLVE_NO_BATCH=1: the layout without the register-front forest (A/B timing only)
+  static const bool no_batch = std::getenv("NCL_SOLVE_NO_BATCH") != nullptr;
+  const DevTasks& T = no_batch ? S.tasks : S.ftasks;
   static int traced = 0;
   const bool tr = trace_path && traced++ == 2;
   if (tr) {
-    cudaMalloc(&g_solve_trace, 4 * sizeof(unsigned long long) * S.tasks.n);
-    cudaMemsetAsync(g_solve_trace, 0, 4 * sizeof(unsigned long long) * S.tasks.n, st);
+    cudaMalloc(&g_solve_trace, 4 * sizeof(unsigned long long) * T.n);
+    cudaMemsetAsync(g_solve_trace, 0, 4 * sizeof(unsigned long long) * T.n, st);
   }
   dev_solve_begin(S, st);
-  dev_solve_fwd_list(S, F, b, S.tasks, 0, st);
-  dev_solve_bwd_list(S, F, x, S.tasks, 2, st);
+  dev_solve_fwd_list(S, F, b, T, 0, st);
+  dev_solve_bwd_list(S, F, x, T, 2, st);
   if (tr) {
-    std::vector<unsigned long long> h(4 * static_cast<size_t>(S.tasks.n));
+    std::vector<unsigned long long> h(4 * static_cast<size_t>(T.n));
     cudaMemcpyAsync(h.data(), g_solve_trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     cudaFree(g_solve_trace);
     g_solve_trace = nullptr;
     if (FILE* fp = std::fopen(trace_path, "wb")) {
-      const int hdr[4] = {S.tasks.n, S.tasks.nleaf, S.tasks.split, 0};
+      const int hdr[4] = {T.n, T.nleaf, T.split, 0};
       std::fwrite(hdr, sizeof(int), 4, fp);
       std::fwrite(h.data(), sizeof(unsigned long long), h.size(), fp);
       std::fclose(fp);

@@ -150,12 +150,57 @@ std::vector<int> symbolic_order(int n, const std::vector<int>& cp, const std::ve
   // node of the smallest non-empty degree yields exactly the (degree, node)
   // lexicographic sequence of one global heap (stale entries included), i.e.
   // the reference std::set's begin() sequence.
+  //
+  // Degrees below kSmallDeg (where nearly all eliminations happen) use exact
+  // buckets instead: a three-level bitmap per degree over the node ids, a
+  // node sits in the bucket of its current degree only (moved on every
+  // degree change, so these buckets hold no stale entries), and the
+  // smallest id is three find-first-set steps away.
   std::vector<std::vector<int>> bucket(n + 1);
   int dmin = n + 1;
+  constexpr int kSmallDeg = 64;
+  const int64_t w0 = (static_cast<int64_t>(n) + 63) / 64, w1 = (w0 + 63) / 64, w2 = (w1 + 63) / 64;
+  std::vector<uint64_t> b0(kSmallDeg * w0, 0), b1(kSmallDeg * w1, 0), b2(kSmallDeg * w2, 0);
+  std::vector<int> bcount(kSmallDeg, 0), inbm(n, -1);  // bitmap bucket of a node (its degree) or -1
+  auto bm_insert = [&](int d, int v) {
+    uint64_t* l0 = b0.data() + d * w0;
+    uint64_t* l1 = b1.data() + d * w1;
+    uint64_t* l2 = b2.data() + d * w2;
+    l0[v >> 6] |= 1ull << (v & 63);
+    l1[v >> 12] |= 1ull << ((v >> 6) & 63);
+    l2[v >> 18] |= 1ull << ((v >> 12) & 63);
+    bcount[d]++;
+    inbm[v] = d;
+  };
+  auto bm_erase = [&](int d, int v) {
+    uint64_t* l0 = b0.data() + d * w0;
+    uint64_t* l1 = b1.data() + d * w1;
+    uint64_t* l2 = b2.data() + d * w2;
+    if ((l0[v >> 6] &= ~(1ull << (v & 63))) == 0)
+      if ((l1[v >> 12] &= ~(1ull << ((v >> 6) & 63))) == 0) l2[v >> 18] &= ~(1ull << ((v >> 12) & 63));
+    bcount[d]--;
+    inbm[v] = -1;
+  };
+  auto bm_min = [&](int d) {
+    const uint64_t* l0 = b0.data() + d * w0;
+    const uint64_t* l1 = b1.data() + d * w1;
+    const uint64_t* l2 = b2.data() + d * w2;
+    int64_t i2 = 0;
+    while (l2[i2] == 0) ++i2;
+    const int64_t i1 = i2 * 64 + __builtin_ctzll(l2[i2]);
+    const int64_t i0 = i1 * 64 + __builtin_ctzll(l1[i1]);
+    return static_cast<int>(i0 * 64 + __builtin_ctzll(l0[i0]));
+  };
+  // (re)file node v under degree d (its old small-degree bucket, if any, is left)
   auto push = [&](int d, int v) {
-    auto& b = bucket[d];
-    b.push_back(v);
-    std::push_heap(b.begin(), b.end(), std::greater<int>());
+    if (inbm[v] >= 0) bm_erase(inbm[v], v);
+    if (d < kSmallDeg) {
+      bm_insert(d, v);
+    } else {
+      auto& b = bucket[d];
+      b.push_back(v);
+      std::push_heap(b.begin(), b.end(), std::greater<int>());
+    }
     if (d < dmin) dmin = d;
   };
   for (int i = 0; i < n; ++i) push(static_cast<int>(adj[i].size()), i);
@@ -189,16 +234,25 @@ std::vector<int> symbolic_order(int n, const std::vector<int>& cp, const std::ve
     bmap[u] = slot;
     std::vector<int>().swap(adj[u]);
   };
-  std::vector<int> clique, merged;
+  std::vector<int> clique;
+  std::vector<int> mark(n, 0);
+  int stamp_id = 0;
   for (;;) {
-    while (dmin <= n && bucket[dmin].empty()) ++dmin;
+    while (dmin < kSmallDeg && bcount[dmin] == 0) ++dmin;
+    if (dmin >= kSmallDeg)
+      while (dmin <= n && bucket[dmin].empty()) ++dmin;
     if (dmin > n) break;
-    auto& bk = bucket[dmin];
-    std::pop_heap(bk.begin(), bk.end(), std::greater<int>());
-    const int v = bk.back();
-    bk.pop_back();
-    const int deg = dmin;
-    if (dead[v] || deg != degree(v)) continue;
+    int v;
+    if (dmin < kSmallDeg) {
+      v = bm_min(dmin);
+      bm_erase(dmin, v);
+    } else {
+      auto& bk = bucket[dmin];
+      std::pop_heap(bk.begin(), bk.end(), std::greater<int>());
+      v = bk.back();
+      bk.pop_back();
+      if (dead[v] || dmin != degree(v) || inbm[v] >= 0) continue;  // stale heap entry
+    }
     perm.push_back(v);
     dead[v] = 1;
     if (bmap[v] >= 0) {  // enumerate the bitmap ascending, release it
@@ -235,24 +289,26 @@ std::vector<int> symbolic_order(int n, const std::vector<int>& cp, const std::ve
         if (wv & bv) wv &= ~bv, --d;
         bdeg[u] = d;
       } else {
+        // (adj[u] \ {v}) ∪ (clique \ {u}) with a stamp array instead of a
+        // sorted merge: adjacency lists are unordered sets (only the set is
+        // observable — degrees and clique membership — so the elimination
+        // order is unchanged)
         std::vector<int>& au = adj[u];
-        merged.clear();
-        if (merged.capacity() < au.size() + clique.size()) merged.reserve(2 * (au.size() + clique.size()));
-        size_t i = 0, j = 0;
-        const size_t na = au.size(), nc = clique.size();
-        while (i < na || j < nc) {
-          int x;
-          if (j >= nc || (i < na && au[i] < clique[j])) {
-            x = au[i++];
-          } else if (i >= na || clique[j] < au[i]) {
-            x = clique[j++];
-          } else {
-            x = au[i++];
-            ++j;
-          }
-          if (x != v && x != u) merged.push_back(x);
+        ++stamp_id;
+        size_t pv = au.size();
+        for (size_t i = 0; i < au.size(); ++i) {
+          const int x = au[i];
+          mark[x] = stamp_id;
+          if (x == v) pv = i;
         }
-        au.assign(merged.begin(), merged.end());  // au keeps (and only grows) its own buffer
+        if (pv < au.size()) {
+          au[pv] = au.back();
+          au.pop_back();
+        }
+        mark[u] = stamp_id;
+        mark[v] = stamp_id;
+        for (int x : clique)
+          if (mark[x] != stamp_id) au.push_back(x);
         if (static_cast<int>(au.size()) > kBig) to_bitmap(u);
       }
       if (degree(u) != old) push(degree(u), u);
@@ -599,31 +655,40 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
           adst_of[sn].push_back(Z.a_off[q]);
           asrc_of[sn].push_back(Z.a_src[q]);
         }
-    std::vector<int> cnt;
+    // counting sort by destination over the packed lower front (the only
+    // entries that receive anything), buffers reused across fronts
+    std::vector<int64_t> cnt, fill;
     for (int sn = 0; sn < nsn; ++sn) {
       if (!want[sn]) {
         Z.gm_ptr[sn + 1] = Z.gm_ptr[sn];
         continue;
       }
       const int nr = static_cast<int>(Z.sn_rptr[sn + 1] - Z.sn_rptr[sn]);
-      cnt.assign(static_cast<size_t>(nr) * nr + 1, 0);
-      for (int d : adst_of[sn]) cnt[d + 1]++;
+      const size_t np = static_cast<size_t>(nr) * (nr + 1) / 2;
+      auto pk = [nr](int rj, int ri) { return static_cast<size_t>(rj) * nr - static_cast<size_t>(rj) * (rj + 1) / 2 + ri; };
+      cnt.assign(np + 1, 0);
+      for (int d : adst_of[sn]) cnt[pk(d / nr, d % nr) + 1]++;
       for (int q = Z.cptr[sn]; q < Z.cptr[sn + 1]; ++q) {
         const int c = Z.child[q];
         const int wc = Z.sn_first[c + 1] - Z.sn_first[c];
         const int m2c = static_cast<int>(Z.sn_rptr[c + 1] - Z.sn_rptr[c]) - wc;
         const int* rel = Z.relp.data() + Z.sn_rptr[c] + wc;
         for (int j = 0; j < m2c; ++j)
-          for (int i = j; i < m2c; ++i) cnt[static_cast<size_t>(rel[j]) * nr + rel[i] + 1]++;
+          for (int i = j; i < m2c; ++i) cnt[pk(rel[j], rel[i]) + 1]++;
       }
-      // CSR over the entries that receive something, in front order
-      std::vector<int64_t> start(static_cast<size_t>(nr) * nr + 1, 0);
-      for (size_t d = 0; d < static_cast<size_t>(nr) * nr; ++d) start[d + 1] = start[d] + cnt[d + 1];
-      const int64_t nsrc = start.back();
+      // CSR over the entries that receive something, in front (column-major) order
       const int64_t base = static_cast<int64_t>(Z.gsrc.size());
-      Z.gsrc.resize(base + nsrc);
-      std::vector<int64_t> fill(start.begin(), start.end() - 1);
-      for (size_t k = 0; k < adst_of[sn].size(); ++k) Z.gsrc[base + fill[adst_of[sn][k]]++] = ~asrc_of[sn][k];
+      fill.resize(np);
+      int64_t run = 0;
+      for (size_t d = 0; d < np; ++d) {
+        fill[d] = run;
+        run += cnt[d + 1];
+      }
+      Z.gsrc.resize(base + run);
+      for (size_t k = 0; k < adst_of[sn].size(); ++k) {
+        const int d = adst_of[sn][k];
+        Z.gsrc[base + fill[pk(d / nr, d % nr)]++] = ~asrc_of[sn][k];
+      }
       for (int q = Z.cptr[sn]; q < Z.cptr[sn + 1]; ++q) {
         const int c = Z.child[q];
         const int wc = Z.sn_first[c + 1] - Z.sn_first[c];
@@ -631,18 +696,21 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
         const int* rel = Z.relp.data() + Z.sn_rptr[c] + wc;
         for (int j = 0; j < m2c; ++j) {
           const int64_t colb = Z.cb_off[c] + static_cast<int64_t>(j) * m2c - static_cast<int64_t>(j) * (j + 1) / 2;
-          for (int i = j; i < m2c; ++i) Z.gsrc[base + fill[static_cast<size_t>(rel[j]) * nr + rel[i]]++] = colb + i;
+          for (int i = j; i < m2c; ++i) Z.gsrc[base + fill[pk(rel[j], rel[i])]++] = colb + i;
         }
       }
       // destination: packed lower offset for fronts that fit the CTA path
       // (shared-memory and one-CTA large fronts), full column-major
       // rj * nr + ri for the wider ones (blocked DMMA path)
-      for (size_t d = 0; d < static_cast<size_t>(nr) * nr; ++d)
-        if (cnt[d + 1]) {
-          const int rj = static_cast<int>(d / nr), ri = static_cast<int>(d % nr);
-          const int packed = rj * nr - rj * (rj + 1) / 2 + ri;  // cb_col(rj, nr) + ri
-          Z.gdst.push_back(nr <= kSmemFront ? packed : static_cast<int>(d));
-          Z.gsp.push_back(base + start[d]);
+      int64_t at = base;
+      for (int rj = 0; rj < nr; ++rj)
+        for (int ri = rj; ri < nr; ++ri) {
+          const size_t d = pk(rj, ri);
+          if (cnt[d + 1]) {
+            Z.gdst.push_back(nr <= kSmemFront ? static_cast<int>(d) : rj * nr + ri);
+            Z.gsp.push_back(at);
+            at += cnt[d + 1];
+          }
         }
       Z.gm_ptr[sn + 1] = static_cast<int64_t>(Z.gdst.size());
     }
