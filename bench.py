@@ -372,7 +372,9 @@ def main():
     B_fact = 8 * nnzk + 12 * info.l_nnz + 8 * n
     achieved = B_fact / fact_avg_s / 1e9
     prof_traffic = None
-    tp = os.path.join(ROOT, "profiles", "factor_traffic.json")
+    # ncu DRAM bytes of one refactorization of THIS configuration
+    # (tools/factor_traffic.py); null when that configuration was not captured
+    tp = os.path.join(ROOT, "profiles", f"factor_traffic_{a.grid}x{a.K}.json")
     if os.path.exists(tp):
         with open(tp) as f:
             prof_traffic = json.load(f).get("bytes_per_launch")

@@ -1,8 +1,9 @@
 """Sum ncu per-launch DRAM bytes and durations of the kernels of ONE
 refactorization (the bench's dominant step) from a --metrics csv, and write
-profiles/factor_traffic.json (read by bench.py for roofline.traffic).
+profiles/factor_traffic_<grid>x<K>.json (read by bench.py for roofline.traffic
+of that configuration only).
 
-usage: python tools/factor_traffic.py gpurun_out/traffic.csv
+usage: python tools/factor_traffic.py gpurun_out/traffic.csv activsg500x256
 """
 import collections
 import csv
@@ -45,5 +46,7 @@ out = {"bytes_per_launch": tot_b, "seconds_serialised": tot_t, "launches": len(s
        "what": "dram__bytes_read.sum + dram__bytes_write.sum over every kernel of one refactorization "
                "(maxdiag .. inertia, solve excluded), ncu --metrics, serialised / cold-cache",
        "by_kernel": {k: {"bytes": v[0], "seconds": v[1], "launches": v[2]} for k, v in by.items()}}
-json.dump(out, open("profiles/factor_traffic.json", "w"), indent=1)
+cfg = sys.argv[2] if len(sys.argv) > 2 else "activsg500x256"
+out["config"] = cfg
+json.dump(out, open(f"profiles/factor_traffic_{cfg}.json", "w"), indent=1)
 print(json.dumps({k: out[k] for k in ("bytes_per_launch", "seconds_serialised", "launches")}))
