@@ -120,6 +120,10 @@ int ncl_solver_solution(ncl_solver_t S, double* x, double* y, double* r);
 int ncl_solver_newton_step(ncl_solver_t S, const ncl_ipm_state* st, const ncl_options* opt, ncl_newton_step* out);
 /* JSON-lines trace; *len = full size */
 int ncl_solver_trace(ncl_solver_t S, char* buf, int64_t cap, int64_t* len);
+/* variable-bound multipliers (zl, zu: n) at the last solution and the
+ * objective scale sf of the scaled Lagrangian sf f + y'(c - r - s) - zl'(x - xl)
+ * - zu'(xu - x) - ... (csrc/host/ipm_elem.hpp); the inputs of mpcc_check */
+int ncl_solver_bound_duals(ncl_solver_t S, double* zl, double* zu, double* sf);
 
 #ifdef __cplusplus
 }

@@ -232,6 +232,10 @@ class RefBackend final : public ipm::Backend {
     dn(o.dx, dx_), dn(o.dzl, dzl_), dn(o.dzu, dzu_), dn(o.dr, dr_), dn(o.ds, ds_), dn(o.dy, dy_);
     dn(o.dvl, dvl_), dn(o.dvu, dvu_);
   }
+  void get_bound_duals(double* zl, double* zu) override {
+    if (zl) std::copy(zl_.begin(), zl_.end(), zl);
+    if (zu) std::copy(zu_.begin(), zu_.end(), zu);
+  }
   void get_solution(double* x, double* y, double* r) override {
     if (x) std::copy(x_.begin(), x_.end(), x);
     if (y) std::copy(y_.begin(), y_.end(), y);

@@ -372,8 +372,8 @@ struct LayoutDev {
 struct ncl_symb {
   SymbolicCore core;
   Supernodal Z;
-  TaskLayout lay;   // default task layout (subtree groups + singles) and its level schedule (solves)
-  TaskLayout flay;  // the same list with its batched subtrees split off (factor)
+  TaskLayout flay;  // task layout of factor and solves: register-front forest + subtree groups + singles
+  TaskLayout lay;   // the same list unbatched (built only for the NCL_*NO_BATCH A/B switches)
   uint64_t hash = 0;
   int nnz = 0;
   DevSymb d;
@@ -450,7 +450,7 @@ void build_batches(const Supernodal& Z, const std::vector<int>& list, int split,
           wbase = static_cast<int64_t>(B.cmapw.size());
           B.cmapw.resize(B.cmapw.size() + static_cast<size_t>(maxnch) * nw * 32, 0xffffffffu);
           B.chunks[chunk0 + x / 32].smap = static_cast<int>(B.smapw.size());
-          B.smapw.resize(B.smapw.size() + static_cast<size_t>(maxnch) * kSmapWords * 32, 0xffffffffu);
+          B.smapw.resize(B.smapw.size() + static_cast<size_t>(maxnch) * kSmapStride * 32, 0xffffffffu);
         }
         batched[s] = 1;
         RegInst I{};
@@ -480,9 +480,12 @@ void build_batches(const Supernodal& Z, const std::vector<int>& list, int split,
             // forward solve: parent row rel[kk] <- the child's CV entry kk
             const int64_t sb = B.chunks[chunk0 + x / 32].smap;
             for (int kk = 0; kk < m2c; ++kk) {
-              uint32_t& wd = B.smapw[sb + (static_cast<int64_t>(qi) * kSmapWords + rel[kk] / 4) * 32 + ix];
+              uint32_t& wd = B.smapw[sb + (static_cast<int64_t>(qi) * kSmapStride + rel[kk] / 4) * 32 + ix];
               wd = (wd & ~(0xffu << (8 * (rel[kk] % 4)))) | (static_cast<uint32_t>(kk) << (8 * (rel[kk] % 4)));
             }
+            const int64_t cvo = Z.sn_rptr[c] + wof(c);
+            if (cvo >= (int64_t(1) << 31)) throw Error{NCL_E_INVALID, "analyze: row list exceeds int32 addressing"};
+            B.smapw[sb + (static_cast<int64_t>(qi) * kSmapStride + kSmapWords) * 32 + ix] = static_cast<uint32_t>(cvo);
             for (int j = 0; j < m2c; ++j)
               for (int ii = j; ii < m2c; ++ii) {
                 const int64_t pp = cb_col(rel[j], nr) + rel[ii];
@@ -798,11 +801,13 @@ void upload_symb(ncl_symb* S) {
   S->cv_ptr.upload(Z.cv_ptr);
   S->cvsp.upload(Z.cvsp);
   S->cvsrc.upload(Z.cvsrc);
-  upload_top(S->lay.top, S->top_dev);
-  S->lay_nodes.upload(S->lay.nodes);
-  S->lay_prog.upload(S->lay.prog);
-  S->lay_gpo.upload(S->lay.gpo);
-  S->lay_tptr.upload(S->lay.tptr);
+  if (!S->lay.tptr.empty()) {  // the unbatched layout exists only for NCL_*NO_BATCH A/B runs
+    upload_top(S->lay.top, S->top_dev);
+    S->lay_nodes.upload(S->lay.nodes);
+    S->lay_prog.upload(S->lay.prog);
+    S->lay_gpo.upload(S->lay.gpo);
+    S->lay_tptr.upload(S->lay.tptr);
+  }
   // A entries grouped by target supernode (Supernodal::a_ptr/a_src/a_off)
   const int nsn = Z.nsn;
   const std::vector<int64_t>& aptr = Z.a_ptr;
@@ -873,9 +878,11 @@ void upload_symb(ncl_symb* S) {
   d.cvsp = S->cvsp.p;
   d.cvsrc = S->cvsrc.p;
   d.meta = S->meta.p;
-  d.tasks = DevTasks{S->lay_nodes.p, S->lay_tptr.p, S->lay_prog.p, S->lay_gpo.p,
-                     static_cast<int>(S->lay.tptr.size()) - 1, S->lay.nleaf, S->lay.split, &S->lay.top};
   d.ftasks = upload_layout(S->flay, S->fdev);
+  d.tasks = S->lay.tptr.empty()
+                ? d.ftasks
+                : DevTasks{S->lay_nodes.p, S->lay_tptr.p, S->lay_prog.p, S->lay_gpo.p,
+                           static_cast<int>(S->lay.tptr.size()) - 1, S->lay.nleaf, S->lay.split, &S->lay.top};
   d.cptr = S->cptr.p;
   d.child = S->child.p;
   d.chrec = S->chrec.p;
@@ -922,10 +929,13 @@ ncl_symb* analyze_impl(ncl_sym_t M, const int* perm) {
   lap("analyze_core");
   S->Z = build_supernodes(S->core, M->pat.col_ptr(), M->pat.row_ind());
   lap("build_supernodes");
-  S->lay = build_layout(S->Z, S->Z.order, S->Z.nsplit);
-  lap("build_layout");
+  // factor and solves run on the batched layout (register fronts split off);
+  // the unbatched one is built only for the NCL_NO_BATCH / NCL_SOLVE_NO_BATCH
+  // A/B switches
+  static const bool unbatched = std::getenv("NCL_NO_BATCH") || std::getenv("NCL_SOLVE_NO_BATCH");
+  if (unbatched) S->lay = build_layout(S->Z, S->Z.order, S->Z.nsplit);
   S->flay = build_layout(S->Z, S->Z.order, S->Z.nsplit, true);
-  lap("build_layout(f)");
+  lap("build_layout");
   S->hash = M->hash;
   S->nnz = M->pat.nnz();
   return S.release();
@@ -946,9 +956,9 @@ API int ncl_symb_info_get(ncl_symb_t S, ncl_symb_info* info) {
     info->cb_storage = S->Z.cb_storage;
     info->nsplit = S->Z.nsplit;
     int nb = 0;
-    for (const auto& lv : S->lay.top.big) nb += static_cast<int>(lv.size());
+    for (const auto& lv : S->flay.top.big) nb += static_cast<int>(lv.size());
     info->n_big = nb;
-    info->n_tasks = static_cast<int>(S->lay.tptr.size()) - 1;
+    info->n_tasks = static_cast<int>(S->flay.tptr.size()) - 1 + static_cast<int>(S->flay.batch.inst.size());
   });
 }
 API int ncl_symb_supernodes(ncl_symb_t S, int* sn_first, int64_t* sn_rptr, int* sn_parent, int* height,
@@ -1315,18 +1325,14 @@ struct ncl_shard {
   ShardPlan P;
   ncl_symb* S = nullptr;
   bool dev_ready = false;
-  DevBuf<int> listA, listB, bids, bowner;
+  DevBuf<int> bids, bowner;
   DevBuf<int64_t> cb_off, cv_off;
   DevBuf<uint8_t> report;
   DevBuf<double> send, recv;
   DevBuf<int> unrep;  // original indices this rank does not report (zeroed before the x all-reduce)
-  TaskLayout layA, layB;
-  TaskLayout flayA, flayB;  // factor variants (batched subtrees split off)
+  TaskLayout flayA, flayB;  // phase A / B task layouts (register fronts split off)
   LayoutDev fdevA, fdevB;
   DevTasks ftA{}, ftB{};
-  std::vector<DevBuf<BigDesc>> topA_dev, topB_dev;
-  DevBuf<int> tA, tB, pA, pB;  // task pointers, group programs
-  DevBuf<int64_t> gA, gB;
   int64_t nunrep = 0;
 };
 
@@ -1335,16 +1341,6 @@ void shard_upload(ncl_shard* sh) {
   if (sh->dev_ready) return;
   ensure_init();
   upload_symb(sh->S);
-  upload_top(sh->layA.top, sh->topA_dev);
-  upload_top(sh->layB.top, sh->topB_dev);
-  sh->listA.upload(sh->layA.nodes);
-  sh->listB.upload(sh->layB.nodes);
-  sh->tA.upload(sh->layA.tptr);
-  sh->tB.upload(sh->layB.tptr);
-  sh->pA.upload(sh->layA.prog);
-  sh->pB.upload(sh->layB.prog);
-  sh->gA.upload(sh->layA.gpo);
-  sh->gB.upload(sh->layB.gpo);
   sh->ftA = upload_layout(sh->flayA, sh->fdevA);
   sh->ftB = upload_layout(sh->flayB, sh->fdevB);
   sh->bids.upload(sh->P.boundary);
@@ -1463,8 +1459,6 @@ API int ncl_shard_create(ncl_symb_t S, const int* var_group, int ngroups, int wo
     sh->S = S;
     std::vector<int> g(var_group, var_group + S->core.n);
     sh->P = build_shard_plan(S->Z, S->core, g, ngroups, world, rank);
-    sh->layA = build_layout(S->Z, sh->P.listA, sh->P.splitA);
-    sh->layB = build_layout(S->Z, sh->P.listB, sh->P.splitB);
     sh->flayA = build_layout(S->Z, sh->P.listA, sh->P.splitA, true);
     sh->flayB = build_layout(S->Z, sh->P.listB, sh->P.splitB, true);
     *out = sh.release();

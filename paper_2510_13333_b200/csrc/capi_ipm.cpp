@@ -233,6 +233,11 @@ class GpuBackend final : public ipm::Backend {
     dn(o.dr, V_.dr, m_), dn(o.ds, V_.ds, m_), dn(o.dy, V_.dy, m_), dn(o.dvl, V_.dvl, m_), dn(o.dvu, V_.dvu, m_);
     ck(cudaStreamSynchronize(g_stream), "sync");
   }
+  void get_bound_duals(double* zl, double* zu) override {
+    if (zl && n_) ck(cudaMemcpyAsync(zl, V_.zl, n_ * sizeof(double), cudaMemcpyDeviceToHost, g_stream), "D2H");
+    if (zu && n_) ck(cudaMemcpyAsync(zu, V_.zu, n_ * sizeof(double), cudaMemcpyDeviceToHost, g_stream), "D2H");
+    ck(cudaStreamSynchronize(g_stream), "sync");
+  }
   void get_solution(double* x, double* y, double* r) override {
     auto dn = [&](double* h, const double* d, int64_t cnt) {
       if (h && cnt) ck(cudaMemcpyAsync(h, d, cnt * sizeof(double), cudaMemcpyDeviceToHost, g_stream), "D2H");
@@ -279,6 +284,7 @@ struct ncl_solver {
   std::unique_ptr<GpuBackend> be;
   std::string trace;
   ncl_result last{};
+  double sf = 1.0;  // objective scale of the last solve
 };
 
 API int ncl_options_default(ncl_options* o) { GUARD(*o = ipm::default_options()); }
@@ -298,6 +304,7 @@ API int ncl_solver_solve(ncl_solver_t S, const ncl_options* opt, ncl_result* res
     ipm::Solver sol(*S->be, o);
     S->last = sol.solve();
     S->trace = sol.trace();
+    S->sf = sol.objective_scale();
     *res = S->last;
   });
 }
@@ -309,6 +316,12 @@ API int ncl_solver_newton_step(ncl_solver_t S, const ncl_ipm_state* st, const nc
   });
 }
 API int ncl_solver_solution(ncl_solver_t S, double* x, double* y, double* r) { GUARD(S->be->get_solution(x, y, r)); }
+API int ncl_solver_bound_duals(ncl_solver_t S, double* zl, double* zu, double* sf) {
+  GUARD({
+    S->be->get_bound_duals(zl, zu);
+    if (sf) *sf = S->sf;
+  });
+}
 API int ncl_solver_trace(ncl_solver_t S, char* buf, int64_t cap, int64_t* len) {
   GUARD({
     *len = static_cast<int64_t>(S->trace.size());

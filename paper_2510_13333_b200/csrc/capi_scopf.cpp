@@ -178,3 +178,17 @@ API int ncl_scopf_build_model(ncl_scopf_t S, ncl_model_t* out) {
     if ((rc = ncl_builder_build(B, out)) != NCL_OK) return rc;
   });
 }
+
+API int ncl_scopf_comp_pairs(ncl_scopf_t S, int* rows, int* w1var, int* xvar, int* side, double* bound) {
+  GUARD({
+    const ModelSpec& p = S->spec;
+    auto cp = [](auto* dst, const auto& v) {
+      if (dst) std::copy(v.begin(), v.end(), dst);
+    };
+    cp(rows, p.comp_rows);
+    cp(w1var, p.comp_w1);
+    cp(xvar, p.comp_x);
+    cp(side, p.comp_side);
+    cp(bound, p.comp_bound);
+  });
+}

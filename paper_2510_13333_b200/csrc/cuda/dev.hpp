@@ -73,11 +73,13 @@ struct alignas(16) RegInst {
 constexpr int kRegParentBatched = 1 << 8;  // RegInst::shape flag: the parent is a register front too
 struct RegChunk {
   int shape, n, first;  // n fronts inst[first .. first + n) of one shape
-  int smap;             // word offset of the chunk's forward-solve row maps in smapw: for front lane l and
-                        // child q, word w (rows 4w .. 4w + 3) at smap + (q * kSmapWords + w) * 32 + l holds the
-                        // child's CV entry index per parent row (255 = none)
+  int smap;             // word offset of the chunk's forward-solve child records in smapw: for front lane
+                        // l and child q, word w < kSmapWords (rows 4w .. 4w + 3) at
+                        // smap + (q * kSmapStride + w) * 32 + l holds the child's CV entry index per parent
+                        // row (255 = none), word kSmapWords the child's CV offset (int32)
 };
-constexpr int kSmapWords = 3;  // rows of a register front <= 12
+constexpr int kSmapWords = 3;                // rows of a register front <= 12
+constexpr int kSmapStride = kSmapWords + 1;  // + the child's CV offset
 struct BatchSched {
   std::vector<RegInst> inst;
   std::vector<int> amap;

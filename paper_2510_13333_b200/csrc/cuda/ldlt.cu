@@ -1257,14 +1257,22 @@ __global__ void __launch_bounds__(256) big_cta_kernel(DevSymb S, const BigDesc* 
                  tid);
 }
 
-__global__ void maxdiag_kernel(const int* __restrict__ pos, int nd, const double* __restrict__ v, double* out) {
+// one atomic per block (warp shuffles, then the block's warps through shared
+// memory): the per-warp atomics on one address serialised in L2
+__global__ void __launch_bounds__(256) maxdiag_kernel(const int* __restrict__ pos, int nd, const double* __restrict__ v,
+                                                      double* out) {
+  __shared__ double wm[8];
   double m = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nd; i += gridDim.x * blockDim.x)
-    m = fmax(m, fabs(v[pos[i]]));
+    m = fmax(m, fabs(__ldg(v + __ldg(pos + i))));
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(kFull, m, o));
-  if ((threadIdx.x & 31) == 0) atomic_max_nonneg(out, m);
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) m = fmax(m, wm[w]);
+    atomic_max_nonneg(out, m);
+  }
 }
-
 __global__ void thresh_kernel(double* scal, double tol, int* istat, int n) {
   // scal[1] = max|diag M| ; scal[0] = pivot_tol * max(1, maxdiag)  (sparse_sym.cpp:286)
   scal[0] = tol * fmax(1.0, scal[1]);
@@ -1272,13 +1280,14 @@ __global__ void thresh_kernel(double* scal, double tol, int* istat, int n) {
   istat[1] = istat[2] = istat[3] = 0;
 }
 
-__global__ void inertia_kernel(const double* __restrict__ D, int n, const double* scal, int* istat,
-                               const uint8_t* __restrict__ report) {
+__global__ void __launch_bounds__(256) inertia_kernel(const double* __restrict__ D, int n, const double* scal,
+                                                      int* istat, const uint8_t* __restrict__ report) {
+  __shared__ int wc[3][8];
   const double th = scal[0];
   int np = 0, nn = 0, nz = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     if (report && !report[i]) continue;  // sharded: every column counted by exactly one rank
-    const double d = D[i];
+    const double d = __ldg(D + i);
     if (fabs(d) <= th) nz++;
     else if (d > 0.0) np++;
     else nn++;
@@ -1288,10 +1297,13 @@ __global__ void inertia_kernel(const double* __restrict__ D, int n, const double
     nn += __shfl_xor_sync(kFull, nn, o);
     nz += __shfl_xor_sync(kFull, nz, o);
   }
-  if ((threadIdx.x & 31) == 0) {
-    atomicAdd(istat + 1, np);
-    atomicAdd(istat + 2, nn);
-    atomicAdd(istat + 3, nz);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) wc[0][w] = np, wc[1][w] = nn, wc[2][w] = nz;
+  __syncthreads();
+  if (threadIdx.x < 3) {  // one atomic per counter per block
+    int t = 0;
+    for (int k = 0; k < 8; ++k) t += wc[threadIdx.x][k];
+    if (t) atomicAdd(istat + 1 + threadIdx.x, t);
   }
 }
 
@@ -1904,8 +1916,12 @@ template <int NR, int W>
 __device__ __forceinline__ void reg_fwd_front(const SolveArgs& a, const RegInst& I, const int* __restrict__ cid,
                                               const uint32_t* __restrict__ smap) {
   const DevSymb& S = a.S;
+  static_assert(NR <= 4 * kSmapWords, "solve row map words");
+  constexpr int NW = (NR + 3) / 4;
+  // everything that does not depend on the children's results first: the
+  // panel, b through the permutation, the first four children's CV offsets
+  // and row maps — after the flags only the CV loads remain
   const int64_t rb = __ldg(S.sn_rptr + I.s);
-  const int q0 = __ldg(S.cptr + I.s);
   double P[W][NR];
   const double* Pg = a.L + I.loff;
 #pragma unroll
@@ -1915,23 +1931,37 @@ __device__ __forceinline__ void reg_fwd_front(const SolveArgs& a, const RegInst&
   double v[NR];
 #pragma unroll
   for (int i = 0; i < NR; ++i) v[i] = i < W ? __ldcg(a.b + __ldg(S.perm + I.f + i)) : 0.0;
+  int rel[4];
+  uint32_t mw[4][NW];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    rel[q] = q < I.nch ? static_cast<int>(__ldg(smap + (q * kSmapStride + kSmapWords) * 32)) : 0;
+#pragma unroll
+    for (int w4 = 0; w4 < NW; ++w4) mw[q][w4] = q < I.nch ? __ldg(smap + (q * kSmapStride + w4) * 32) : 0xffffffffu;
+  }
 #pragma unroll
   for (int q = 0; q < 4; ++q)
     if (q < I.nch) wait_flag(a.flags + I.cid[q], a.epoch);
   for (int q = 4; q < I.nch; ++q) wait_flag(a.flags + __ldg(cid + I.ccb + q), a.epoch);
-  static_assert(NR <= 4 * kSmapWords, "solve row map words");
-  constexpr int NW = (NR + 3) / 4;
-  for (int q = 0; q < I.nch; ++q) {
-    const int rel = S.chrec[q0 + q].rel;
-    uint32_t mw[NW];
+  // per parent row (constant index) the child's CV entry or none: v stays in
+  // registers; children in ascending order (the extend-add order)
 #pragma unroll
-    for (int w4 = 0; w4 < NW; ++w4) mw[w4] = __ldg(smap + (q * kSmapWords + w4) * 32);
-    // per parent row (constant index) the child's CV entry or none: v stays
-    // in registers, every load of the child in flight together
+  for (int q = 0; q < 4; ++q) {
 #pragma unroll
     for (int i = 0; i < NR; ++i) {
-      const uint32_t k = (mw[i >> 2] >> (8 * (i & 3))) & 0xffu;
-      if (k != 0xffu) v[i] += __ldcg(a.CV + rel + k);
+      const uint32_t k = (mw[q][i >> 2] >> (8 * (i & 3))) & 0xffu;
+      if (k != 0xffu) v[i] += __ldcg(a.CV + rel[q] + k);
+    }
+  }
+  for (int q = 4; q < I.nch; ++q) {
+    const int rq = static_cast<int>(__ldg(smap + (q * kSmapStride + kSmapWords) * 32));
+    uint32_t m[NW];
+#pragma unroll
+    for (int w4 = 0; w4 < NW; ++w4) m[w4] = __ldg(smap + (q * kSmapStride + w4) * 32);
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      const uint32_t k = (m[i >> 2] >> (8 * (i & 3))) & 0xffu;
+      if (k != 0xffu) v[i] += __ldcg(a.CV + rq + k);
     }
   }
 #pragma unroll
@@ -2123,7 +2153,8 @@ int64_t g_kernel_launches = 0;
 
 void dev_max_abs_diag(const DevPattern& P, const double* kvals, double* out, cudaStream_t st) {
   cudaMemsetAsync(out, 0, sizeof(double), st);
-  if (P.ndiag > 0) COUNT(1), maxdiag_kernel<<<grid_for(P.ndiag, 256), 256, 0, st>>>(P.diag_pos, P.ndiag, kvals, out);
+  if (P.ndiag > 0)
+    COUNT(1), maxdiag_kernel<<<std::min(grid_for(P.ndiag, 256), 2 * num_sms()), 256, 0, st>>>(P.diag_pos, P.ndiag, kvals, out);
 }
 
 template <class K>
@@ -2296,7 +2327,7 @@ void dev_factor(const DevSymb& S, const DevPattern& P, DevFactor& F, const doubl
 
 void dev_inertia(const DevSymb& S, DevFactor& F, cudaStream_t st, const uint8_t* report) {
   COUNT(1);
-  inertia_kernel<<<grid_for(S.n, 256), 256, 0, st>>>(F.D, S.n, F.scal, F.istat, report);
+  inertia_kernel<<<std::min(grid_for(S.n, 256), 2 * num_sms()), 256, 0, st>>>(F.D, S.n, F.scal, F.istat, report);
 }
 
 void dev_solve_begin(const DevSymb& S0, cudaStream_t st) {

@@ -62,6 +62,7 @@ class Backend {
   virtual double update_multipliers() = 0;  // lamN <- y on rows; returns |lamN|_inf
   virtual double objective() const = 0;  // unscaled f at x
   virtual void get_solution(double* x, double* y, double* r) = 0;
+  virtual void get_bound_duals(double* zl, double* zu) = 0;  // variable-bound multipliers at x
   // newton_step() only: overwrite the primal-dual state (then f, c at x are
   // re-evaluated) and read the last step back
   virtual void set_state(const ncl_ipm_state& st) = 0;
@@ -79,6 +80,7 @@ class Solver {
   Solver(Backend& be, const ncl_options& o) : be_(be), o_(o) {}
   ncl_result solve();
   const std::string& trace() const { return trace_; }
+  double objective_scale() const { return S_.sf; }  // sf of the scaled Lagrangian (ipm_elem.hpp)
 
  private:
   using clk = std::chrono::steady_clock;

@@ -571,20 +571,20 @@ ModelSpec build_scopf(const Grid& g, const std::vector<int>& cont) {
       const int vb = g.gbus[k];
       term(T_PVPQ, newrow(0.0, 0.0), {onp + k, onm + k, ov + vb, S.off_v[0] + vb}, {});
     }
+    auto pair = [&](int tmpl, int w1, int x, double bound) {
+      const int r = newrow(-kInf, 0.0);
+      term(tmpl, r, {w1, x}, {bound});
+      S.comp_rows.push_back(r);
+      S.comp_w1.push_back(w1);
+      S.comp_x.push_back(x);
+      S.comp_side.push_back(tmpl == T_COMPU ? -1 : 1);
+      S.comp_bound.push_back(bound);
+    };
     for (int k = 0; k < ng; ++k) {
-      int r;
-      r = newrow(-kInf, 0.0);
-      term(T_COMPU, r, {opm + k, opg + k}, {g.pmax[k]});
-      S.comp_rows.push_back(r);
-      r = newrow(-kInf, 0.0);
-      term(T_COMPL, r, {opp + k, opg + k}, {g.pmin[k]});
-      S.comp_rows.push_back(r);
-      r = newrow(-kInf, 0.0);
-      term(T_COMPU, r, {onm + k, oqg + k}, {g.qmax[k]});
-      S.comp_rows.push_back(r);
-      r = newrow(-kInf, 0.0);
-      term(T_COMPL, r, {onp + k, oqg + k}, {g.qmin[k]});
-      S.comp_rows.push_back(r);
+      pair(T_COMPU, opm + k, opg + k, g.pmax[k]);
+      pair(T_COMPL, opp + k, opg + k, g.pmin[k]);
+      pair(T_COMPU, onm + k, oqg + k, g.qmax[k]);
+      pair(T_COMPL, onp + k, oqg + k, g.qmin[k]);
     }
   }
   // objective: base-case generation cost

@@ -76,6 +76,10 @@ struct ModelSpec {
   int nvar_scen = 0, ncon_scen = 0;
   std::vector<int> contingencies;
   std::vector<int> comp_rows;  // rows of complementarity products
+  // pair i of row comp_rows[i]: w1 = x[comp_w1[i]] (>= 0), w2 = side * (x[comp_x[i]] - comp_bound[i])
+  // (side -1: the upper limit ub - x, +1: the lower limit x - lb), row = w1 * w2 <= 0
+  std::vector<int> comp_w1, comp_x, comp_side;
+  std::vector<double> comp_bound;
   // per-scenario variable offsets: v, theta, pg, qg, flows; contingency extras
   std::vector<int> off_v, off_th, off_pg, off_qg, off_fl, off_extra;
   std::vector<int> row_start;  // first row of each scenario

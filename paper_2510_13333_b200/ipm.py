@@ -95,6 +95,7 @@ register({
     "ncl_solver_destroy": (None, [P]),
     "ncl_solver_solve": (i32, [P, C.POINTER(NclOptions), C.POINTER(NclResult)]),
     "ncl_solver_solution": (i32, [P, P, P, P]),
+    "ncl_solver_bound_duals": (i32, [P, P, P, C.POINTER(f64)]),
     "ncl_solver_trace": (i32, [P, C.c_char_p, i64, C.POINTER(i64)]),
     "ncl_solver_newton_step": (i32, [P, C.POINTER(IpmState), C.POINTER(NclOptions), C.POINTER(NewtonStep)]),
 })
@@ -144,6 +145,14 @@ class NclSolver:
         if h:
             lib.ncl_solver_destroy(h)
             self._h = None
+
+    def bound_duals(self):
+        """(zl, zu, sf) of the last solve: variable-bound multipliers and the
+        objective scale of the scaled Lagrangian (csrc/host/ipm_elem.hpp)"""
+        n = self.n
+        zl, zu, sf = np.empty(n), np.empty(n), C.c_double()
+        check(lib.ncl_solver_bound_duals(self._h, _ptr(zl), _ptr(zu), C.byref(sf)))
+        return zl, zu, sf.value
 
     def solve(self, options: NclOptions | None = None) -> SolveOutput:
         o = options if options is not None else default_options()
