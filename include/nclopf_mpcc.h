@@ -25,7 +25,7 @@ typedef struct ncl_mpcc_cert {
   int n_p0, n_0p, n_00;       /* index-set sizes */
   double grad_residual;       /* ||grad_w L^MPCC||_inf (caller-supplied) */
   double feas_residual;       /* feasibility residual (caller-supplied) */
-  double comp_residual;       /* max_i |min(w1_i, w2_i)| */
+  double comp_residual;       /* max_i |w1_i w2_i| */
   int inactive_violations;    /* |mu1| > tol on I+0 or |mu2| > tol on I0+ */
   int sign_violations;        /* mu1 or mu2 < -tol on I00 (Eq. 11) */
   int first_violation;        /* first violating pair or -1 */

@@ -5,4 +5,4 @@ package is a thin ctypes mirror of the reference API used by tests and the
 bench. There is no CPU fallback anywhere on the numeric path.
 """
 from . import _lib  # noqa: F401  (fails loudly when the library is missing)
-from . import sparse, model, kkt, scopf, ipm, dist, mpcc  # noqa: F401,E402
+from . import sparse, model, kkt, scopf, ipm, dist, mpcc, matpower  # noqa: F401,E402

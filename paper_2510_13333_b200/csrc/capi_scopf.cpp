@@ -10,6 +10,8 @@
 
 #include "../../include/nclopf_b200.h"
 #include "capi_internal.hpp"
+#include "../../include/nclopf_matpower.h"
+#include "host/matpower.hpp"
 #include "host/scopf.hpp"
 #include "host/sparse.hpp"
 
@@ -49,6 +51,26 @@ struct ncl_scopf {
   ModelSpec spec;
 };
 
+namespace {
+void finish_scopf(ncl_scopf* s, int K, const int* branch_ids) {
+  std::vector<int> cont;
+  if (branch_ids) {
+    const auto ok = select_contingencies(s->grid, s->grid.nl);  // non-islanding set
+    for (int k = 0; k < K; ++k) {
+      const int id = branch_ids[k];  // branch + nl * load level (host/scopf.hpp)
+      if (id < 0 || id / s->grid.nl >= kLoadLevels || !std::binary_search(ok.begin(), ok.end(), id % s->grid.nl))
+        throw Error{NCL_E_INVALID, "scopf: contingency islands the network or is out of range"};
+      cont.push_back(id);
+    }
+  } else {
+    cont = select_contingencies(s->grid, K);
+  }
+  if (static_cast<int>(cont.size()) < K)
+    throw Error{NCL_E_INVALID, "scopf: fewer non-islanding contingencies than requested"};
+  s->spec = build_scopf(s->grid, cont);
+}
+}  // namespace
+
 API int ncl_scopf_create_list(int grid, int nb, int nl, int ng, uint64_t seed, int K, const int* branch_ids,
                               ncl_scopf_t* out) {
   GUARD({
@@ -58,21 +80,7 @@ API int ncl_scopf_create_list(int grid, int nb, int nl, int ng, uint64_t seed, i
     } catch (const std::invalid_argument& e) {
       throw Error{NCL_E_INVALID, e.what()};
     }
-    std::vector<int> cont;
-    if (branch_ids) {
-      const auto ok = select_contingencies(s->grid, s->grid.nl);  // non-islanding set
-      for (int k = 0; k < K; ++k) {
-        const int id = branch_ids[k];  // branch + nl * load level (host/scopf.hpp)
-        if (id < 0 || id / s->grid.nl >= kLoadLevels || !std::binary_search(ok.begin(), ok.end(), id % s->grid.nl))
-          throw Error{NCL_E_INVALID, "scopf: contingency islands the network or is out of range"};
-        cont.push_back(id);
-      }
-    } else {
-      cont = select_contingencies(s->grid, K);
-    }
-    if (static_cast<int>(cont.size()) < K)
-      throw Error{NCL_E_INVALID, "scopf: fewer non-islanding contingencies than requested"};
-    s->spec = build_scopf(s->grid, cont);
+    finish_scopf(s.get(), K, branch_ids);
     *out = s.release();
   });
 }
@@ -190,5 +198,90 @@ API int ncl_scopf_comp_pairs(ncl_scopf_t S, int* rows, int* w1var, int* xvar, in
     cp(xvar, p.comp_x);
     cp(side, p.comp_side);
     cp(bound, p.comp_bound);
+  });
+}
+
+// ---- matpower_io (include/nclopf_matpower.h) -------------------------------
+struct ncl_network {
+  matpower::PowerNetwork net;
+};
+namespace {
+template <class F>
+void rethrow_invalid(F&& f) {
+  try {
+    f();
+  } catch (const std::invalid_argument& e) {  // ParseError / ValidationError
+    throw Error{NCL_E_INVALID, e.what()};
+  }
+}
+void text_out(const std::string& t, char* buf, int64_t cap, int64_t* len) {
+  *len = static_cast<int64_t>(t.size());
+  if (buf && cap > 0) {
+    const int64_t k = std::min<int64_t>(cap - 1, *len);
+    std::memcpy(buf, t.data(), k);
+    buf[k] = 0;
+  }
+}
+}  // namespace
+API int ncl_matpower_parse(const char* text, ncl_network_t* out) {
+  GUARD({
+    auto n = std::make_unique<ncl_network>();
+    rethrow_invalid([&] { n->net = matpower::parse_case(text); });
+    *out = n.release();
+  });
+}
+API void ncl_network_destroy(ncl_network_t N) { delete N; }
+API int ncl_network_info_get(ncl_network_t N, ncl_network_info* info) {
+  GUARD({
+    const auto& n = N->net;
+    info->base_mva = n.base_mva;
+    info->nbus = static_cast<int>(n.bus.size());
+    info->nbranch = static_cast<int>(n.branch.size());
+    info->ngen = static_cast<int>(n.gen.size());
+    info->ref = n.ref;
+    info->nbranch_in = 0;
+    for (const auto& e : n.branch) info->nbranch_in += e.status;
+    info->ngen_in = 0;
+    for (const auto& g : n.gen) info->ngen_in += g.status;
+  });
+}
+API int ncl_network_buses(ncl_network_t N, int* id, int* type, double* pd, double* qd, double* vmin, double* vmax) {
+  GUARD({
+    const auto& b = N->net.bus;
+    for (size_t i = 0; i < b.size(); ++i) {
+      if (id) id[i] = b[i].id;
+      if (type) type[i] = b[i].type;
+      if (pd) pd[i] = b[i].pd;
+      if (qd) qd[i] = b[i].qd;
+      if (vmin) vmin[i] = b[i].vmin;
+      if (vmax) vmax[i] = b[i].vmax;
+    }
+  });
+}
+API int ncl_network_branch_admittances(ncl_network_t N, double* y) {
+  GUARD({
+    std::vector<matpower::TwoPort> v;
+    rethrow_invalid([&] { v = matpower::branch_admittances(N->net); });
+    for (size_t l = 0; l < v.size(); ++l) {
+      const std::complex<double> a[4] = {v[l].yff, v[l].yft, v[l].ytf, v[l].ytt};
+      for (int k = 0; k < 4; ++k) {
+        y[8 * l + 2 * k] = a[k].real();
+        y[8 * l + 2 * k + 1] = a[k].imag();
+      }
+    }
+  });
+}
+API int ncl_network_serialize(ncl_network_t N, char* buf, int64_t cap, int64_t* len) {
+  GUARD(text_out(matpower::serialize(N->net), buf, cap, len));
+}
+API int ncl_network_json(ncl_network_t N, char* buf, int64_t cap, int64_t* len) {
+  GUARD(text_out(matpower::to_json(N->net), buf, cap, len));
+}
+API int ncl_scopf_create_network(ncl_network_t N, int K, const int* branch_ids, ncl_scopf_t* out) {
+  GUARD({
+    auto s = std::make_unique<ncl_scopf>();
+    s->grid = matpower::to_grid(N->net);
+    finish_scopf(s.get(), K, branch_ids);
+    *out = s.release();
   });
 }

@@ -215,7 +215,11 @@ constexpr int kGrpFront = 32;       // fronts of group nodes: nr <= 32 (packed l
 constexpr int kGrpStack = 512;      // doubles: A values + contribution-block stack
 constexpr int kGrpProg = 1280;      // ints: the group program (read in place: bounds group size only)
 
-constexpr int kTickets = 40;  // ticket counters per symbolic handle
+constexpr int kTickets = 64;  // ticket counters per symbolic handle
+// [kTicketSeg0, kTickets): per-segment tickets of the unsharded factorization,
+// zeroed once per factorization so consecutive segment launches have no
+// memset between them (programmatic dependent launch, csrc/cuda/ldlt.cu)
+constexpr int kTicketSeg0 = 40;
 
 extern unsigned long long* g_task_trace;  // device buffer [2 * tasks] or nullptr
 void dev_phase_trace(unsigned long long* buf);  // device buffer [4 * nsn] or nullptr

@@ -51,6 +51,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
+// Programmatic dependent launch: a persistent kernel lets the next one in the
+// stream launch once every CTA has claimed one of its last tasks (or run out
+// of tasks), so the next phase's CTAs take over SMs as this phase drains.
+// The next phase synchronises through the completion flags only (it never
+// executes griddepcontrol.wait), which is why only phases whose every task
+// waits on its dependencies' flags are launched this way.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ void wait_flag(const int* f, int epoch) {
   while (ld_acquire(f) != epoch) __nanosleep(32);
 }
@@ -1213,8 +1221,10 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 6 : NT == 128 
   double* gST = F + kFrontPk;
   const double thresh = __ldcg(a.thresh);
   Claim<NT> cl;
+  const int tail = a.t1 - static_cast<int>(gridDim.x) * (NT == 32 ? 4 : 1);  // the last claims of the launch
   for (;;) {
     const int t = cl.next(a.ticket, a.t0, a.t1, a.nleaf, tid, &s_ticket);
+    if (tid == 0 && (t < 0 || t >= tail)) pdl_trigger();
     if (t < 0) break;
     // a task is a whole small subtree in postorder (one warp, no scheduling
     // between its nodes) or a single supernode
@@ -1854,8 +1864,10 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 8 : 4) fwd_ker
   extern __shared__ double s_sol[];
   const int tid = NT == 32 ? (threadIdx.x & 31) : threadIdx.x;
   Claim<NT> cl;
+  const int tail = a.t1 - static_cast<int>(gridDim.x) * (NT == 32 ? 4 : 1);
   for (;;) {
     const int t = cl.next(a.ticket, a.t0, a.t1, a.nleaf, tid, &s_ticket);
+    if (tid == 0 && (t < 0 || t >= tail)) pdl_trigger();
     if (t < 0) break;
     if (a.trace && tid == 0) a.trace[2 * t] = gtimer();
     if (NT == 32 && a.prog && t < a.nleaf) {
@@ -1887,6 +1899,7 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 8 : 4) bwd_ker
       t = s_ticket;
     }
     const int k = a.t1 - 1 - t;
+    if (tid == 0 && k < a.t0 + static_cast<int>(gridDim.x) * (NT == 32 ? 4 : 1)) pdl_trigger();
     if (k < a.t0) break;
     if (a.trace && tid == 0) a.trace[2 * k] = gtimer();
     if (NT == 32 && a.prog && k < a.nleaf) {
@@ -2173,6 +2186,27 @@ static int g_fg = 0, g_fg2 = 0, g_fg3 = 0, g_sf = 0, g_sf2 = 0, g_sb = 0, g_sb2 
 constexpr int kFacSmem1 = 4 * (kGrpFront * (kGrpFront + 1) / 2 + kGrpStack) * sizeof(double);
 constexpr int kFacSmem2 = kCtaFront * (kCtaFront + 1) / 2 * sizeof(double);  // packed lower front
 constexpr int kFacSmem3 = kCtaFrontS * (kCtaFrontS + 1) / 2 * sizeof(double);  // small-CTA segments
+// NCL_NO_PDL=1: plain stream-ordered launches (A/B)
+static const bool g_pdl = std::getenv("NCL_NO_PDL") == nullptr;
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*k)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, Args&&... args) {
+  if (!g_pdl) {
+    k<<<grid, block, smem, st>>>(std::forward<Args>(args)...);
+    return;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
 static void init_grids() {
   if (g_fg) return;
   cudaFuncSetAttribute(factor_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFacSmem1);
@@ -2288,13 +2322,26 @@ void dev_factor_list(const DevSymb& S, DevFactor& F, const double* kvals, const 
       const int b = ts.lvl_begin[L], e = ts.lvl_end[L];
       const int nsmall = (e - b) - static_cast<int>(ts.big[L].size());
       if (nsmall > 0) {
-        cudaMemsetAsync(S.tickets + kTickets - 1, 0, sizeof(int), st);
-        a.ticket = S.tickets + kTickets - 1;
+        // unsharded: a pre-zeroed ticket per segment and a programmatic
+        // dependent launch (every segment task waits on its children's
+        // flags); sharded phases reuse one ticket
+        const bool pdl = slot == 0 && kTicketSeg0 + static_cast<int>(L) < kTickets;
+        if (pdl) {
+          a.ticket = S.tickets + kTicketSeg0 + L;
+        } else {
+          cudaMemsetAsync(S.tickets + kTickets - 1, 0, sizeof(int), st);
+          a.ticket = S.tickets + kTickets - 1;
+        }
         a.t0 = b;
         a.t1 = e;
         COUNT(1);
-        if (ts.small[L]) factor_kernel<128><<<std::min(g_fg3, e - b), 128, kFacSmem3, st>>>(a);
-        else factor_kernel<256><<<std::min(g_fg2, e - b), 256, kFacSmem2, st>>>(a);
+        if (pdl) {
+          if (ts.small[L]) launch_pdl(factor_kernel<128>, std::min(g_fg3, e - b), 128, kFacSmem3, st, a);
+          else launch_pdl(factor_kernel<256>, std::min(g_fg2, e - b), 256, kFacSmem2, st, a);
+        } else {
+          if (ts.small[L]) factor_kernel<128><<<std::min(g_fg3, e - b), 128, kFacSmem3, st>>>(a);
+          else factor_kernel<256><<<std::min(g_fg2, e - b), 256, kFacSmem2, st>>>(a);
+        }
       }
       if (!ts.big[L].empty()) dev_factor_big_batch(S, F, kvals, ts.big[L], ts.big_dev[L], st);
     }
@@ -2366,7 +2413,7 @@ void dev_solve_fwd_list(const DevSymb& S, DevFactor& F, const double* b, const D
     fa.t0 = T.split;
     fa.t1 = T.n;
     COUNT(1);
-    fwd_kernel<256><<<std::min(g_sf2, T.n - T.split), 256, 0, st>>>(fa);
+    launch_pdl(fwd_kernel<256>, std::min(g_sf2, T.n - T.split), 256, 0, st, fa);  // CTA tasks wait on children
   }
 }
 
@@ -2382,7 +2429,7 @@ void dev_solve_bwd_list(const DevSymb& S, DevFactor& F, double* x, const DevTask
     ba.t0 = 0;
     ba.t1 = T.split;
     COUNT(1);
-    bwd_kernel<32><<<g_sb, 128, kSolSmem, st>>>(ba);
+    launch_pdl(bwd_kernel<32>, g_sb, 128, kSolSmem, st, ba);  // every warp task waits on its parent
   }
   // the batched forest last: every parent is in this list or earlier
   if (T.batch) reg_solve(S, *T.batch, ba, false, st);

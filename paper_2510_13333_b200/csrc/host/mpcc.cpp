@@ -44,7 +44,7 @@ Certificate certify(int p, const double* w1, const double* w2, const double* mu1
   }
   const int bad = index_sets(p, w1, w2, tol_act, cls);
   for (int i = 0; i < p; ++i) {
-    C.comp_residual = std::max(C.comp_residual, std::fabs(std::min(w1[i], w2[i])));
+    C.comp_residual = std::max(C.comp_residual, std::fabs(w1[i] * w2[i]));
     bool viol = false;
     switch (cls[i]) {
       case kPlusZero:

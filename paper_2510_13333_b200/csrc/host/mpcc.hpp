@@ -27,7 +27,7 @@ struct Certificate {
   int n_p0 = 0, n_0p = 0, n_00 = 0;
   double grad_residual = 0.0;  // ||grad_w L^MPCC||_inf (the caller's, = the NLP's by the recovery identity)
   double feas_residual = 0.0;
-  double comp_residual = 0.0;  // max_i min(w1_i, w2_i)^+ ... max |min(w1, w2)|
+  double comp_residual = 0.0;  // max_i |w1_i w2_i|
   int inactive_violations = 0; // |mu1| > tol on I+0, |mu2| > tol on I0+
   int sign_violations = 0;     // mu1 or mu2 < -tol on I00
   int first_violation = -1;

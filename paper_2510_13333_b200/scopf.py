@@ -18,6 +18,7 @@ class ScopfInfo(C.Structure):
 
 
 register({
+    "ncl_scopf_create_network": (i32, [P, i32, P, C.POINTER(P)]),
     "ncl_scopf_create": (i32, [i32, i32, i32, i32, C.c_uint64, i32, C.POINTER(P)]),
     "ncl_scopf_create_list": (i32, [i32, i32, i32, i32, C.c_uint64, i32, P, C.POINTER(P)]),
     "ncl_scopf_destroy": (None, [P]),
@@ -84,22 +85,30 @@ class Family:
 
 
 class Scopf:
-    def __init__(self, grid: str = "case9", K: int = 0, seed: int = 2510, contingencies=None):
+    def __init__(self, grid: str = "case9", K: int = 0, seed: int = 2510, contingencies=None, network=None):
         """contingencies: explicit contingency ids (branch + nl * load level);
         default = contingency_ids(grid, K, seed): the committed screened
         outages (data/screened_<grid>_<seed>.json,
         tools/screen_contingencies.py), then the same outages at lower load
         levels, when a screened list exists, else the first K non-islanding
         branches."""
+        h = C.c_void_p()
+        if network is not None:  # a parsed MATPOWER case (paper_2510_13333_b200.matpower)
+            ids = None if contingencies is None else np.ascontiguousarray(np.asarray(contingencies)[:K], np.int32)
+            check(lib.ncl_scopf_create_network(network.handle, K, _ptr(ids), C.byref(h)))
+            self._finish(h, network.name)
+            return
         kind, nb, nl, ng = GRIDS[grid]
         if contingencies is None and K > 0:
             contingencies = contingency_ids(grid, K, seed)
-        h = C.c_void_p()
         if contingencies is None:
             check(lib.ncl_scopf_create(kind, nb, nl, ng, seed, K, C.byref(h)))
         else:
             ids = np.ascontiguousarray(np.asarray(contingencies)[:K], np.int32)
             check(lib.ncl_scopf_create_list(kind, nb, nl, ng, seed, K, _ptr(ids), C.byref(h)))
+        self._finish(h, grid)
+
+    def _finish(self, h, grid):
         self._h = h
         s = ScopfInfo()
         check(lib.ncl_scopf_get_info(h, C.byref(s)))

@@ -75,11 +75,13 @@ def test_scopf_solution_certificate(gpu, grid, K):
     S = NclSolver(s.build_model(), s.bounds())
     out = S.solve(default_options())
     assert out.status == "optimal"
-    d = mpcc.certify_scopf(s, S, out, tol=1e-5, tol_act=1e-5)
+    # NCL meets w1 w2 <= 0 up to r (|r| <= eta* = 1e-7), so the pairs are
+    # complementary to ~sqrt(1e-7) componentwise: activity at 1e-3
+    d = mpcc.certify_scopf(s, S, out, tol=1e-5, tol_act=1e-3)
     p = s.info.ncomp
     assert p == 4 * s.info.ng * K
     assert d["n_p0"] + d["n_0p"] + d["n_00"] == p
-    assert d["comp_residual"] <= 1e-5
+    assert d["comp_residual"] <= 1e-6
     # the multipliers of an interior solution: nu >= 0 up to the barrier
     assert np.min(d["nu0"]) >= -1e-8
     # every pair is classified and the certificate is internally consistent
