@@ -346,7 +346,15 @@ std::vector<int> select_contingencies(const Grid& g, int K) {
   return out;
 }
 
-ModelSpec build_scopf(const Grid& g, const std::vector<int>& cont) {
+ModelSpec build_scopf(const Grid& g, const std::vector<int>& cont) { return build_scopf(g, cont, nullptr, nullptr); }
+
+ModelSpec build_scopf(const Grid& g, const std::vector<int>& cont, const double* pg0, const double* v0) {
+  // screening mode (pg0, v0 given, SPEC.md:264-271 / PAPER.md Eq. 5): no base
+  // scenario; every contingency scenario with the base set points fixed as
+  // constants (moved to the row bounds of its AGC and PV/PQ rows) and no
+  // objective — a feasibility system per contingency, all of them side by
+  // side in one problem
+  const bool screen = pg0 != nullptr;
   ModelSpec S;
   const int nb = g.nb, nl = g.nl, ng = g.ng, K = static_cast<int>(cont.size());
   S.nb = nb;
@@ -359,7 +367,7 @@ ModelSpec build_scopf(const Grid& g, const std::vector<int>& cont) {
   S.ncon_scen = 1 + 2 * nb + 6 * nl;
 
   // ---- templates
-  enum { T_FP, T_FQ, T_PLUS, T_MINUS, T_SHUNT, T_SQ2, T_AGC, T_PVPQ, T_COMPU, T_COMPL, T_COST, T_N };
+  enum { T_FP, T_FQ, T_PLUS, T_MINUS, T_SHUNT, T_SQ2, T_AGC, T_PVPQ, T_COMPU, T_COMPL, T_COST, T_AGCS, T_PVPQS, T_N };
   S.fams.resize(T_N);
   auto def = [&](int id, const char* name, int nslots, int np, bool obj, NB& nbld) {
     S.fams[id].name = name;
@@ -441,6 +449,20 @@ ModelSpec build_scopf(const Grid& g, const std::vector<int>& cont) {
     def(T_COMPL, "comp_lower", 2, 1, false, e);
   }
   {
+    // screening: pi+ - pi- - p_k + alpha Delta (= -p_0, a row constant)
+    NB e;
+    int pp = e.var(0), pm = e.var(1), pk = e.var(2), dl = e.var(3);
+    e.add(e.sub(e.sub(pp, pm), pk), e.mul(e.par(0), dl));
+    def(T_AGCS, "agc_droop_fixed_base", 4, 1, false, e);
+  }
+  {
+    // screening: nu+ - nu- - v_k (= -v_0)
+    NB e;
+    int np_ = e.var(0), nm = e.var(1), vk = e.var(2);
+    e.sub(e.sub(np_, nm), vk);
+    def(T_PVPQS, "pvpq_switch_fixed_base", 3, 0, false, e);
+  }
+  {
     // c2 p^2 + c1 p + c0
     NB e;
     int p = e.var(0);
@@ -455,7 +477,7 @@ ModelSpec build_scopf(const Grid& g, const std::vector<int>& cont) {
   };
 
   // ---- variables
-  const int nvar = B + K * (B + 1 + 4 * ng);
+  const int nvar = (screen ? 0 : B) + K * (B + 1 + 4 * ng);
   S.n = nvar;
   S.xl.assign(nvar, -kInf);
   S.xu.assign(nvar, kInf);
@@ -469,7 +491,7 @@ ModelSpec build_scopf(const Grid& g, const std::vector<int>& cont) {
     gu.push_back(hi);
     return row++;
   };
-  for (int s = 0; s <= K; ++s) {
+  for (int s = screen ? 1 : 0; s <= K; ++s) {
     // contingency id = outaged branch + nl * load level (contingency_load_scale)
     if (s > 0 && (cont[s - 1] < 0 || cont[s - 1] / nl >= kLoadLevels))
       throw std::invalid_argument("build_scopf: contingency id out of range");
@@ -565,11 +587,16 @@ ModelSpec build_scopf(const Grid& g, const std::vector<int>& cont) {
     for (int k = 0; k < ng; ++k) {
       S.xl[opp + k] = S.xl[opm + k] = S.xl[onp + k] = S.xl[onm + k] = 0.0;
     }
-    for (int k = 0; k < ng; ++k)
-      term(T_AGC, newrow(0.0, 0.0), {opp + k, opm + k, opg + k, S.off_pg[0] + k, odl}, {g.pmax[k] / psum});
+    for (int k = 0; k < ng; ++k) {
+      if (screen)
+        term(T_AGCS, newrow(-pg0[k], -pg0[k]), {opp + k, opm + k, opg + k, odl}, {g.pmax[k] / psum});
+      else
+        term(T_AGC, newrow(0.0, 0.0), {opp + k, opm + k, opg + k, S.off_pg[0] + k, odl}, {g.pmax[k] / psum});
+    }
     for (int k = 0; k < ng; ++k) {
       const int vb = g.gbus[k];
-      term(T_PVPQ, newrow(0.0, 0.0), {onp + k, onm + k, ov + vb, S.off_v[0] + vb}, {});
+      if (screen) term(T_PVPQS, newrow(-v0[vb], -v0[vb]), {onp + k, onm + k, ov + vb}, {});
+      else term(T_PVPQ, newrow(0.0, 0.0), {onp + k, onm + k, ov + vb, S.off_v[0] + vb}, {});
     }
     auto pair = [&](int tmpl, int w1, int x, double bound) {
       const int r = newrow(-kInf, 0.0);
@@ -587,8 +614,9 @@ ModelSpec build_scopf(const Grid& g, const std::vector<int>& cont) {
       pair(T_COMPL, onp + k, oqg + k, g.qmin[k]);
     }
   }
-  // objective: base-case generation cost
-  for (int k = 0; k < ng; ++k) term(T_COST, -1, {S.off_pg[0] + k}, {g.c2[k], g.c1[k], g.c0[k]});
+  // objective: base-case generation cost (none in screening mode)
+  if (!screen)
+    for (int k = 0; k < ng; ++k) term(T_COST, -1, {S.off_pg[0] + k}, {g.c2[k], g.c1[k], g.c0[k]});
   S.m = row;
   S.gl = std::move(gl);
   S.gu = std::move(gu);

@@ -87,5 +87,11 @@ struct ModelSpec {
 
 // contingencies: ids as above (branch + nl * load level)
 ModelSpec build_scopf(const Grid& g, const std::vector<int>& contingencies);
+// Screening system (Eq. 5): the contingency scenarios only, with the
+// base set points fixed — pg0[ng] generator outputs and v0[nb] bus voltages
+// (read at generator buses) of a solved base case — and no objective. The
+// scenarios are independent blocks: one NCL solve screens them all, each
+// block's |r|^2 (r on its rows) its infeasibility measure.
+ModelSpec build_scopf(const Grid& g, const std::vector<int>& contingencies, const double* pg0, const double* v0);
 
 }  // namespace nclb
