@@ -222,6 +222,14 @@ int ncl_scopf_var_groups(ncl_scopf_t S, int* groups);
 /* every non-islanding single-branch outage of the grid (ascending); ids may be NULL */
 int ncl_scopf_candidates(ncl_scopf_t S, int* ids, int* count);
 int ncl_scopf_build_model(ncl_scopf_t S, ncl_model_t* out); /* this library's ModelBuilder */
+/* screening system (Eq. 5): the K contingency
+ * scenarios of `base`'s grid with the base set points fixed — pg0[ng]
+ * generator outputs, v0[nb] bus voltages (read at generator buses) — and no
+ * objective; the scenarios are independent row/variable blocks of equal size,
+ * so one NCL solve screens them all. ids as
+ * ncl_scopf_create_list (NULL: the first K non-islanding outages). */
+int ncl_scopf_create_screening(ncl_scopf_t base, const double* pg0, const double* v0, int K, const int* ids,
+                               ncl_scopf_t* out);
 
 #ifdef __cplusplus
 }

@@ -72,7 +72,7 @@ def lib():
             "ref_mf_fd_check": (i32, [P, P, C.c_uint, f64, P, pi]),
             "ref_ipm_last_error": (C.c_char_p, []),
             "ref_ipm_default_options": (None, [P]),
-            "ref_ncl_solve": (i32, [P, P, P, P, P, P, P, P, P, P, P, C.c_char_p, i64, C.POINTER(i64)]),
+            "ref_ncl_solve": (i32, [P, P, P, P, P, P, P, P, P, P, P, P, C.c_char_p, i64, C.POINTER(i64)]),
             "ref_scopf_last_error": (C.c_char_p, []),
             "ref_scopf_new": (i32, [i32, i32, i32, i32, C.c_uint64, i32, P, C.POINTER(P), pi, pi]),
             "ref_scopf_free": (None, [P]),
@@ -410,14 +410,14 @@ def ref_ncl_solve(model: RefModel, bounds, perm=None, options=None, trace_cap=1 
     arrs = [np.ascontiguousarray(bounds[k], np.float64) for k in ("xl", "xu", "x0", "gl", "gu")]
     pm = None if perm is None else np.ascontiguousarray(perm, np.int32)
     res = NclResult()
-    x, y = np.empty(model.n), np.empty(model.m)
+    x, y, r = np.empty(model.n), np.empty(model.m), np.empty(model.m)
     buf = C.create_string_buffer(trace_cap)
     ln = C.c_int64()
     rc = L.ref_ncl_solve(model.h, *[_p(a) for a in arrs], _p(pm), C.byref(options), C.byref(res), _p(x), _p(y),
-                         buf, trace_cap, C.byref(ln))
+                         _p(r), buf, trace_cap, C.byref(ln))
     if rc != 0:
         raise RefError(rc, L.ref_ipm_last_error().decode())
     from paper_2510_13333_b200.ipm import parse_trace
 
     trace = parse_trace(buf.value.decode())
-    return dict(result=res.as_dict(), status=STATUS.get(res.status, str(res.status)), x=x, y=y, trace=trace)
+    return dict(result=res.as_dict(), status=STATUS.get(res.status, str(res.status)), x=x, y=y, r=r, trace=trace)

@@ -280,14 +280,14 @@ REF_API void ref_ipm_default_options(ncl_options* o) { *o = ipm::default_options
 // symbolic_order permutation of the K pattern (NULL = run the reference's).
 REF_API int ref_ncl_solve(void* model, const double* xl, const double* xu, const double* x0, const double* gl,
                           const double* gu, const int* perm, const ncl_options* opt, ncl_result* res, double* x_out,
-                          double* y_out, char* trace, int64_t cap, int64_t* len) {
+                          double* y_out, double* r_out, char* trace, int64_t cap, int64_t* len) {
   try {
     const auto& M = *static_cast<const nclopf::ModelFunctions*>(model);
     RefBackend be(M, xl, xu, x0, gl, gu, perm);
     const ncl_options o = opt ? *opt : ipm::default_options();
     ipm::Solver sol(be, o);
     *res = sol.solve();
-    be.get_solution(x_out, y_out, nullptr);
+    be.get_solution(x_out, y_out, r_out);
     const std::string& t = sol.trace();
     if (len) *len = static_cast<int64_t>(t.size());
     if (trace && cap > 0) {

@@ -509,12 +509,6 @@ void build_batches(const Supernodal& Z, const std::vector<int>& list, int split,
     }
     if (l == nlev / 2 - 1) B.nchunk1 = static_cast<int>(B.chunks.size());
   }
-  // backward solve: a front whose parent is batched too waits on the parent's
-  // flag; any other parent finished in an earlier launch
-  for (RegInst& I : B.inst) {
-    const int p = Z.sn_parent[I.s];
-    if (p >= 0 && batched[p]) I.shape |= kRegParentBatched;
-  }
 }
 
 // Task layout of a list (leaves-first height order, CTA part from `split`):
@@ -560,7 +554,7 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
     for (int q = Z.cptr[s]; q < Z.cptr[s + 1]; ++q) {
       const int c = Z.child[q];
       if (batched[c]) {
-        pr += 6 + (nrof(c) - wof(c));
+        pr += 7 + (nrof(c) - wof(c));
         continue;
       }
       ok = ok && fits[c];
@@ -599,7 +593,7 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
     L.tptr.push_back(static_cast<int>(L.nodes.size()));
     // program: [nnodes, nA, tab, len] [aoff x nA] [asrc x nA] then per node
     // [s, f, w, nr, nch, push_off(-1 = root), a_first, a_cnt, loff lo/hi, cboff lo/hi, rptr lo/hi] and per child
-    // [m2c, stack_off, rel x m2c] ([m2c, -1, cboff lo/hi, cvoff lo/hi, rel x m2c] for an external child),
+    // [m2c, stack_off, rel x m2c] ([m2c, -1, cboff lo/hi, cvoff lo/hi, child, rel x m2c] for an external child),
     // then the record offsets [tab .. tab + nnodes);
     // stack offsets from a postorder simulation
     const size_t base = L.prog.size();
@@ -640,6 +634,7 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
           L.prog.push_back(static_cast<int>(Z.cb_off[c] >> 32));
           L.prog.push_back(static_cast<int>(cv & 0xffffffff));
           L.prog.push_back(static_cast<int>(cv >> 32));
+          L.prog.push_back(c);  // its completion flag (the group may start before the register phase ends)
         } else {
           L.prog.push_back(cboff[c]);
         }
@@ -1585,7 +1580,7 @@ API int ncl_shard_diagonal(ncl_fact_t F, ncl_shard_t sh, double* d) {
 // (they write disjoint CBs, so no exchange is needed), then phase B once.
 API int ncl_shard_refactorize_emulated(ncl_fact_t F, ncl_sym_t M, ncl_shard_t* plans, int G, double tol) {
   GUARD({
-    if (G < 1 || 2 * (G + 1) > kTickets) throw Error{NCL_E_INVALID, "emulated shards: bad G"};
+    if (G < 1 || 2 * (G + 1) > kTicketSeg0) throw Error{NCL_E_INVALID, "emulated shards: bad G"};
     check_match(M, F->S);
     ensure_dev(M, "factorize");
     for (int r = 0; r < G; ++r) {

@@ -285,3 +285,27 @@ API int ncl_scopf_create_network(ncl_network_t N, int K, const int* branch_ids, 
     *out = s.release();
   });
 }
+
+// ---- screening (Eq. 5) ----------------------------
+API int ncl_scopf_create_screening(ncl_scopf_t base, const double* pg0, const double* v0, int K, const int* ids,
+                                   ncl_scopf_t* out) {
+  GUARD({
+    if (!pg0 || !v0 || K < 1) throw Error{NCL_E_INVALID, "screening: base set points and K >= 1 contingencies"};
+    auto s = std::make_unique<ncl_scopf>();
+    s->grid = base->grid;
+    std::vector<int> cont;
+    const auto ok = select_contingencies(s->grid, s->grid.nl);
+    for (int k = 0; k < K; ++k) {
+      const int id = ids ? ids[k] : (k < static_cast<int>(ok.size()) ? ok[k] : -1);
+      if (id < 0 || id / s->grid.nl >= kLoadLevels || !std::binary_search(ok.begin(), ok.end(), id % s->grid.nl))
+        throw Error{NCL_E_INVALID, "screening: contingency islands the network or is out of range"};
+      cont.push_back(id);
+    }
+    try {
+      s->spec = build_scopf(s->grid, cont, pg0, v0);
+    } catch (const std::invalid_argument& e) {
+      throw Error{NCL_E_INVALID, e.what()};
+    }
+    *out = s.release();
+  });
+}

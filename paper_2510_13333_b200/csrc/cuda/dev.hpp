@@ -66,11 +66,10 @@ struct alignas(16) RegInst {
                         // (word w of child q at cmap + (q * words + w) * 32), and the A map interleaved the
                         // same way (entry p at amap + 32 p): coalesced
   int64_t ccb;          // offset of the children's CB offsets (int64 each) and supernode ids (int each)
-  int s, f, nch, shape;  // shape = kRegShapes index | kRegParentBatched
+  int s, f, nch, shape;  // shape = kRegShapes index
   int cid[4];            // the first four children inline (supernode ids, CB offsets): one round trip less
   int64_t cb[4];
 };
-constexpr int kRegParentBatched = 1 << 8;  // RegInst::shape flag: the parent is a register front too
 struct RegChunk {
   int shape, n, first;  // n fronts inst[first .. first + n) of one shape
   int smap;             // word offset of the chunk's forward-solve child records in smapw: for front lane
@@ -216,9 +215,13 @@ constexpr int kGrpStack = 512;      // doubles: A values + contribution-block st
 constexpr int kGrpProg = 1280;      // ints: the group program (read in place: bounds group size only)
 
 constexpr int kTickets = 64;  // ticket counters per symbolic handle
-// [kTicketSeg0, kTickets): per-segment tickets of the unsharded factorization,
-// zeroed once per factorization so consecutive segment launches have no
-// memset between them (programmatic dependent launch, csrc/cuda/ldlt.cu)
+// [kTicketSeg0, kTickets - 8): per-segment tickets of the unsharded
+// factorization, zeroed once per factorization so consecutive segment
+// launches have no memset between them (programmatic dependent launch,
+// csrc/cuda/ldlt.cu); [kTickets - 8, kTickets - 4): backward register-front
+// solve per slot (zeroed by dev_solve_begin); kTickets - 4 .. - 1: the
+// forward register-front solve, the register factor phases, the sharded
+// segments
 constexpr int kTicketSeg0 = 40;
 
 extern unsigned long long* g_task_trace;  // device buffer [2 * tasks] or nullptr

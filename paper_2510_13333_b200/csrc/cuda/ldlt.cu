@@ -992,7 +992,9 @@ __device__ __forceinline__ void group_task(const FactorArgs& a, int g, int lane,
       const double* Cc = stack + off;
       if (off < 0) {  // external child (register-front phase): its CB in the standard layout
         Cc = a.CB + (static_cast<int64_t>(static_cast<uint32_t>(PG[p + 2])) | (static_cast<int64_t>(PG[p + 3]) << 32));
-        p += 4;  // + CB offset, CV offset
+        if (lane == 0) wait_flag(a.flags + PG[p + 6], a.epoch);  // the register phase may still run (PDL)
+        __syncwarp();
+        p += 5;  // + CB offset, CV offset, child
       }
       const int reli = lane < m2c ? PG[p + 2 + lane] : 0;
       extend_add_flat(F, nr, Cc, m2c, reli, lane);
@@ -1199,10 +1201,12 @@ __global__ void __launch_bounds__(128) reg_factor_kernel(FactorArgs a, const Reg
                                                          const int64_t* __restrict__ ccb, const int* __restrict__ cid) {
   const int lane = threadIdx.x & 31;
   const double thresh = __ldcg(a.thresh);
+  const int tail = nchunk - static_cast<int>(gridDim.x) * 4;
   for (;;) {
     int c = 0;
     if (lane == 0) c = atomicAdd(a.ticket, 1);
     c = __shfl_sync(kFull, c, 0);
+    if (lane == 0 && c >= tail) pdl_trigger();
     if (c >= nchunk) break;
     const RegChunk ch = chunks[c];
     reg_dispatch<K0>(a, ch, lane, inst, amap, cmap, cmapw, ccb, cid, thresh,
@@ -1375,8 +1379,10 @@ __device__ void fwd_group(const SolveArgs& a, int g, int lane, double* VS, doubl
       const int m2c = PG[p], off = PG[p + 1];
       if (off < 0) {  // external child (register-front phase): its CV in the standard layout
         const int64_t cv = rec64(PG + p + 4);
-        if (lane < m2c) VS[PG[p + 6 + lane]] += __ldcg(a.CV + cv + lane);
-        p += 6 + m2c;
+        if (lane == 0) wait_flag(a.flags + PG[p + 6], a.epoch);  // the register phase may still run (PDL)
+        __syncwarp();
+        if (lane < m2c) VS[PG[p + 7 + lane]] += __ldcg(a.CV + cv + lane);
+        p += 7 + m2c;
       } else {
         if (lane < m2c) VS[PG[p + 2 + lane]] += ST[off + lane];
         p += 2 + m2c;
@@ -1473,6 +1479,12 @@ __device__ void bwd_group(const SolveArgs& a, int g, int lane) {
       }
     }
     __syncwarp();
+    // the node's x is final: register fronts below it (a later, possibly
+    // overlapping launch) wait on this flag
+    if (lane == 0) {
+      __threadfence();
+      st_release(a.flags + s, a.epoch);
+    }
   }
 }
 
@@ -2010,9 +2022,9 @@ __device__ __forceinline__ void reg_bwd_front(const SolveArgs& a, const RegInst&
     pl[c] = __ldg(S.perm + I.f + c);
     xs[c] = __ldcg(a.xp + I.f + c);
   }
-  // only a batched parent can still be running (every other parent finished
-  // in an earlier launch, and group members publish no backward flags)
-  if (I.shape & kRegParentBatched) wait_flag(a.flags + ps, a.epoch);
+  // the parent may still be running: a register front, or (the launch
+  // overlaps the warp phase's tail) a group member / warp single
+  if (ps >= 0) wait_flag(a.flags + ps, a.epoch);
   double xi[NR];
 #pragma unroll
   for (int i = W; i < NR; ++i) xi[i] = __ldcg(a.xp + ri[i]);
@@ -2058,10 +2070,12 @@ __global__ void __launch_bounds__(128) reg_solve_kernel(SolveArgs a, const RegIn
                                                         const int* __restrict__ cid,
                                                         const uint32_t* __restrict__ smapw) {
   const int lane = threadIdx.x & 31;
+  const int tail = nchunk - static_cast<int>(gridDim.x) * 4;
   for (;;) {
     int c = 0;
     if (lane == 0) c = atomicAdd(a.ticket, 1);
     c = __shfl_sync(kFull, c, 0);
+    if (lane == 0 && c >= tail) pdl_trigger();
     if (c >= nchunk) break;
     const RegChunk ch = chunks[FWD ? c : nchunk - 1 - c];
     reg_solve_dispatch<FWD>(a, ch, lane, inst, cid, smapw, std::make_integer_sequence<int, kNumRegShapes>{});
@@ -2308,7 +2322,9 @@ void dev_factor_list(const DevSymb& S, DevFactor& F, const double* kvals, const 
   g_ptimer.mark(1, st);
   if (T.split > 0 && T.tptr) {
     COUNT(1);
-    factor_kernel<32><<<g_fg, 128, kFacSmem1, st>>>(a);
+    // groups wait on their external (register-front) children's flags, so
+    // the warp phase may overlap the register phase's tail
+    launch_pdl(factor_kernel<32>, g_fg, 128, kFacSmem1, st, a);
   }
   g_ptimer.mark(2, st);
   if (T.top && (T.top->any_big || T.top->any_small)) {
@@ -2325,7 +2341,7 @@ void dev_factor_list(const DevSymb& S, DevFactor& F, const double* kvals, const 
         // unsharded: a pre-zeroed ticket per segment and a programmatic
         // dependent launch (every segment task waits on its children's
         // flags); sharded phases reuse one ticket
-        const bool pdl = slot == 0 && kTicketSeg0 + static_cast<int>(L) < kTickets;
+        const bool pdl = slot == 0 && kTicketSeg0 + static_cast<int>(L) < kTickets - 8;
         if (pdl) {
           a.ticket = S.tickets + kTicketSeg0 + L;
         } else {
@@ -2385,20 +2401,24 @@ void dev_solve_begin(const DevSymb& S0, cudaStream_t st) {
 }
 
 // the batched forest of a task list (one launch; its chunks, children first)
-static void reg_solve(const DevSymb& S, const BatchSched& bs, SolveArgs a, bool fwd, cudaStream_t st) {
+static void reg_solve(const DevSymb& S, const BatchSched& bs, SolveArgs a, bool fwd, int slot, cudaStream_t st) {
   static int grid = 0;
   if (!grid) grid = persistent_grid(reg_solve_kernel<true>, 128, 1 << 30);
   const int n = static_cast<int>(bs.chunks.size());
   if (n == 0) return;
-  a.ticket = S.tickets + kTickets - (fwd ? 4 : 5);
-  cudaMemsetAsync(a.ticket, 0, sizeof(int), st);
+  if (fwd) {
+    a.ticket = S.tickets + kTickets - 4;
+    cudaMemsetAsync(a.ticket, 0, sizeof(int), st);
+  } else {  // zeroed by dev_solve_begin: no memset between it and the warp phase (PDL)
+    a.ticket = S.tickets + kTickets - 8 + slot;
+  }
   COUNT(1);
   if (fwd)
     reg_solve_kernel<true><<<std::min(grid, (n + 3) / 4), 128, 0, st>>>(a, bs.dev_inst, bs.dev_chunks, n, bs.dev_cid,
                                                                        bs.dev_smapw);
-  else
-    reg_solve_kernel<false><<<std::min(grid, (n + 3) / 4), 128, 0, st>>>(a, bs.dev_inst, bs.dev_chunks, n,
-                                                                        bs.dev_cid, bs.dev_smapw);
+  else  // every front waits on its parent's flag: may overlap the warp phase's tail
+    launch_pdl(reg_solve_kernel<false>, std::min(grid, (n + 3) / 4), 128, 0, st, a, bs.dev_inst, bs.dev_chunks, n,
+               bs.dev_cid, bs.dev_smapw);
 }
 
 void dev_solve_fwd_list(const DevSymb& S, DevFactor& F, const double* b, const DevTasks& T, int slot,
@@ -2406,8 +2426,8 @@ void dev_solve_fwd_list(const DevSymb& S, DevFactor& F, const double* b, const D
   if (T.n == 0 && !T.batch) return;
   SolveArgs fa{S, F.L, F.D, F.CV, F.xp, b, nullptr, S.flags + S.nsn, S.tickets + 2 * slot, S.epoch, 0, T.split,
                T.ids, T.tptr, T.prog, T.gpo, T.nleaf, g_solve_trace};
-  if (T.batch) reg_solve(S, *T.batch, fa, true, st);
-  if (T.split > 0) COUNT(1), fwd_kernel<32><<<g_sf, 128, kSolSmem, st>>>(fa);
+  if (T.batch) reg_solve(S, *T.batch, fa, true, slot, st);
+  if (T.split > 0) COUNT(1), launch_pdl(fwd_kernel<32>, g_sf, 128, kSolSmem, st, fa);
   if (T.split < T.n) {
     fa.ticket = S.tickets + 2 * slot + 1;
     fa.t0 = T.split;
@@ -2432,7 +2452,7 @@ void dev_solve_bwd_list(const DevSymb& S, DevFactor& F, double* x, const DevTask
     launch_pdl(bwd_kernel<32>, g_sb, 128, kSolSmem, st, ba);  // every warp task waits on its parent
   }
   // the batched forest last: every parent is in this list or earlier
-  if (T.batch) reg_solve(S, *T.batch, ba, false, st);
+  if (T.batch) reg_solve(S, *T.batch, ba, false, slot, st);
 }
 
 void dev_solve(const DevSymb& S, DevFactor& F, const double* b, double* x, cudaStream_t st) {

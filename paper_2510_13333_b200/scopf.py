@@ -19,6 +19,7 @@ class ScopfInfo(C.Structure):
 
 register({
     "ncl_scopf_create_network": (i32, [P, i32, P, C.POINTER(P)]),
+    "ncl_scopf_create_screening": (i32, [P, P, P, i32, P, C.POINTER(P)]),
     "ncl_scopf_create": (i32, [i32, i32, i32, i32, C.c_uint64, i32, C.POINTER(P)]),
     "ncl_scopf_create_list": (i32, [i32, i32, i32, i32, C.c_uint64, i32, P, C.POINTER(P)]),
     "ncl_scopf_destroy": (None, [P]),
@@ -107,6 +108,19 @@ class Scopf:
             ids = np.ascontiguousarray(np.asarray(contingencies)[:K], np.int32)
             check(lib.ncl_scopf_create_list(kind, nb, nl, ng, seed, K, _ptr(ids), C.byref(h)))
         self._finish(h, grid)
+
+    @classmethod
+    def screening(cls, base: "Scopf", pg0, v0, ids) -> "Scopf":
+        """Eq. 5 screening system of `base`'s grid: the contingencies `ids`
+        with the base set points pg0 (ng) and v0 (nb) fixed, no objective;
+        K equal blocks of n / K variables and m / K rows."""
+        obj = cls.__new__(cls)
+        pg0, v0 = np.ascontiguousarray(pg0, np.float64), np.ascontiguousarray(v0, np.float64)
+        ids = np.ascontiguousarray(ids, np.int32)
+        h = C.c_void_p()
+        check(lib.ncl_scopf_create_screening(base.handle, _ptr(pg0), _ptr(v0), len(ids), _ptr(ids), C.byref(h)))
+        obj._finish(h, base.grid)
+        return obj
 
     def _finish(self, h, grid):
         self._h = h
