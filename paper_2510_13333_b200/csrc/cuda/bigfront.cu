@@ -103,7 +103,8 @@ __global__ void __launch_bounds__(256) bf_panel(BigArgs a, int step) {
       a.D[b.f + k0 + c] = dd;
       if (fabs(dd) <= thresh) atomicMin(a.zp, b.f + k0 + c);
     }
-    for (int i = c + 1 + threadIdx.x; i < ld; i += blockDim.x) Pc[i] = Pc[i] != 0.0 ? Pc[i] / dd : 0.0;  // zero numerators skip the slow path
+    const double rd = 1.0 / dd;  // one division per column; the column scales by multiplies
+    for (int i = c + 1 + threadIdx.x; i < ld; i += blockDim.x) Pc[i] *= rd;
     __syncthreads();
     for (int c2 = c + 1 + warp; c2 < kw; c2 += 8) {
       const double dl = dd * Pc[c2];

@@ -449,6 +449,7 @@ __device__ __forceinline__ void cta_dense(double* F, int nr, int w, int f, doubl
     //      8 x 8 tiles, two k-steps), tiles dealt round-robin to the warps.
     constexpr int kPb = 8;
     constexpr int nw = NT / 32;
+    __shared__ double s_rd[kPb], s_dl[kPb][kPb];  // 1 / d_k and d_k L(k2, k) of the current diagonal block
     const int lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, tg = lane & 3;
     // (a) the kb x kb diagonal block of the panel at c0, by warp 0
@@ -476,6 +477,17 @@ __device__ __forceinline__ void cta_dense(double* F, int nr, int w, int f, doubl
 #pragma unroll
       for (int k = 0; k < kPb; ++k)
         if (k < kb && k <= lane && lane < kb) F[cb_col(c0 + k, nr) + i] = x[k];
+      // the rows below need only 1 / d_k and d_k L(k2, k): computed once here
+      // (the same product the row update formed per row) so the row chains
+      // are multiplies instead of divisions
+#pragma unroll
+      for (int k = 0; k < kPb; ++k) {
+        if (k < kb) {
+          const double dk = __shfl_sync(kFull, x[k], k);
+          if (lane == k) s_rd[k] = 1.0 / dk;
+          if (lane > k && lane < kb) s_dl[k][lane] = dk * x[k];
+        }
+      }
       if (lane < kb) {  // lane k's diagonal entry is the pivot d_k
         double dk = 0.0;
 #pragma unroll
@@ -491,7 +503,9 @@ __device__ __forceinline__ void cta_dense(double* F, int nr, int w, int f, doubl
       const int kb = min(kPb, w - c0);
       DPROF(0)
       DPROF(1)
-      // (b) rows below the diagonal block, one per thread
+      // (b) rows below the diagonal block, one per thread: L(i, k) = x_k / d_k
+      //     as x_k * (1 / d_k), then x_k2 -= L(i, k) (d_k L(k2, k)) from the
+      //     block's precomputed factors (s_rd, s_dl)
       for (int i = c0 + kb + tid; i < nr; i += NT) {
         double x[kPb];
 #pragma unroll
@@ -499,12 +513,10 @@ __device__ __forceinline__ void cta_dense(double* F, int nr, int w, int f, doubl
 #pragma unroll
         for (int k = 0; k < kPb; ++k) {
           if (k < kb) {
-            const double* Lk = F + cb_col(c0 + k, nr);
-            const double d = Lk[c0 + k];
-            x[k] = divz(x[k], d);
+            x[k] *= s_rd[k];
 #pragma unroll
             for (int k2 = 0; k2 < kPb; ++k2)
-              if (k2 > k && k2 < kb) x[k2] -= x[k] * (d * Lk[c0 + k2]);
+              if (k2 > k && k2 < kb) x[k2] -= x[k] * s_dl[k][k2];
           }
         }
 #pragma unroll
