@@ -1086,11 +1086,25 @@ API int ncl_factorize(ncl_sym_t M, ncl_symb_t S, double pivot_tol, ncl_fact_t* o
       f->S = f->owned.get();
     }
     check_match(M, f->S);
+    // NCL_ANALYZE_TIMING=1: the one-time costs of the first factorization
+    static const bool timing = std::getenv("NCL_ANALYZE_TIMING") != nullptr;
+    auto t = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+      if (!timing) return;
+      ck(cudaStreamSynchronize(g_stream), "sync");
+      const auto now = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[factorize] %-16s %.3f s\n", what, std::chrono::duration<double>(now - t).count());
+      t = now;
+    };
     ensure_dev(M, "factorize");
+    lap("matrix upload");
     upload_symb(f->S);
+    lap("symbolic upload");
     alloc_fact(f.get());
+    lap("factor alloc");
     run_factor(f.get(), M, pivot_tol);
     ck(cudaStreamSynchronize(g_stream), "factorize");
+    lap("first factor");
     *out = f.release();
   });
 }

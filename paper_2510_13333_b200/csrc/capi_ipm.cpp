@@ -8,6 +8,10 @@
 // host sees scalars only: one pinned D2H of <= 8 doubles per reduction.
 #include <cuda_runtime.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include <cstring>
 #include <memory>
 #include <string>
@@ -101,6 +105,9 @@ class GpuBackend final : public ipm::Backend {
     if (S_) ncl_symb_destroy(S_);
     if (kkt_) ncl_kkt_destroy(kkt_);
     if (hsc_) cudaFreeHost(hsc_);
+    if (tm_[3] > 0)
+      std::fprintf(stderr, "[ipm] %d refactorizations: assembly %.3f ms + factor %.3f ms on the device, %.3f ms host wall per call\n",
+                   static_cast<int>(tm_[3]), tm_[0] / tm_[3], tm_[1] / tm_[3], tm_[2] / tm_[3]);
   }
   int n() const override { return n_; }
   int m() const override { return m_; }
@@ -148,12 +155,34 @@ class GpuBackend final : public ipm::Backend {
   }
   void form_newton(const ipm::Scal& S) override { dev_ipm_elem(IE_NEWTON, V_, S, g_stream); }
   ipm::FactorOut factor(double dw, double pivot_tol) override {
+    // NCL_IPM_TIMING=1: device time of assembly / factorization per call vs
+    // the host's wall time of the call (printed at exit; debug only)
+    static const bool timing = std::getenv("NCL_IPM_TIMING") != nullptr;
+    const auto h0 = std::chrono::steady_clock::now();
+    if (timing) {
+      if (!ev_[0]) for (auto& e : ev_) cudaEventCreate(&e);
+      cudaEventRecord(ev_[0], g_stream);
+    }
     chk(ncl_kkt_assemble(kkt_, hess_, jac_, V_.sigx, dw, V_.D, NCL_DEVICE));
+    if (timing) cudaEventRecord(ev_[1], g_stream);
+    const bool first = !F_;
     if (!F_) chk(ncl_factorize(K_, S_, pivot_tol, &F_));
     else chk(ncl_refactorize(F_, K_, pivot_tol));
+    if (timing) cudaEventRecord(ev_[2], g_stream);
     ipm::FactorOut o;
     int zp = -1;
     chk(ncl_fact_status(F_, &o.status, &zp, &o.npos, &o.nneg, &o.nzero));
+    if (timing && !first) {
+      float a = 0, f = 0;
+      cudaEventElapsedTime(&a, ev_[0], ev_[1]);
+      cudaEventElapsedTime(&f, ev_[1], ev_[2]);
+      tm_[0] += a, tm_[1] += f;
+      tm_[2] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+      tm_[3] += 1;
+    }
+    if (timing && first)
+      std::fprintf(stderr, "[ipm] first factorization (allocation + upload): %.3f ms\n",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count());
     return o;
   }
   ipm::SolveOut solve(const ipm::Scal& S, double target, int max_sweeps) override {
@@ -265,6 +294,8 @@ class GpuBackend final : public ipm::Backend {
     ck(cudaStreamSynchronize(g_stream), "sync");
   }
 
+  cudaEvent_t ev_[3] = {};
+  double tm_[4] = {0, 0, 0, 0};
   ncl_model_t M_;
   int n_ = 0, m_ = 0;
   int64_t nnzj_ = 0, nnzh_ = 0, nbd_ = 0;

@@ -1,0 +1,31 @@
+"""compute-sanitizer over a small SCOPF factor + solve: memcheck
+(out-of-bounds / misaligned device accesses), racecheck (shared-memory
+hazards of the persistent flag-synchronised kernels) and synccheck (barrier
+misuse) report zero errors."""
+import os
+import re
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+def test_compute_sanitizer_clean(gpu, tool):
+    cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(cs):
+        pytest.skip("compute-sanitizer not found")
+    cmd = [cs, "--tool", tool, "--error-exitcode", "3", "--print-limit", "20"]
+    if tool == "memcheck":
+        cmd += ["--leak-check", "no"]
+    cmd += [sys.executable, os.path.join(ROOT, "tools", "sanitize_case.py"), "case118", "4"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1500)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    # memcheck / synccheck: "ERROR SUMMARY: 0 errors"; racecheck: "RACECHECK SUMMARY: 0 hazards displayed (0 errors, 0 warnings)"
+    assert re.search(r"ERROR SUMMARY: 0 errors|\(0 errors, 0 warnings\)", out), out[-4000:]
+    assert "ok ok" in out
