@@ -187,10 +187,6 @@ void upload_pattern(ncl_sym* M) {
   M->mv_ptr.upload(ptr);
   M->mv_val.upload(mval);
   M->mv_col.upload(mcol);
-  std::vector<int> sptr, sidx;
-  M->pat.slot_trip_csr(sptr, sidx);
-  M->slot_ptr.upload(sptr);
-  M->slot_trip.upload(sidx);
   M->scratch.alloc(8);
   M->dp.n = n;
   M->dp.nnz = nnz;
@@ -204,6 +200,15 @@ void upload_pattern(ncl_sym* M) {
 void ensure_dev(ncl_sym* M, const char* what) {
   if (!M->pat.finalized()) throw Error{NCL_E_LOGIC, std::string(what) + ": matrix not finalized"};
   upload_pattern(M);
+}
+// the triplet -> slot gather of the GPU refill (built on first use: matrices
+// whose values are assembled on the device, like the condensed K, never need it)
+void ensure_refill_map(ncl_sym* M) {
+  if (M->slot_ptr.p) return;
+  std::vector<int> sptr, sidx;
+  M->pat.slot_trip_csr(sptr, sidx);
+  M->slot_ptr.upload(sptr);
+  M->slot_trip.upload(sidx);
 }
 }  // namespace nclb
 
@@ -228,6 +233,7 @@ API int ncl_sym_refill(ncl_sym_t M) {
   GUARD({
     if (!M->pat.finalized()) throw Error{NCL_E_LOGIC, "SparseSym::refill: not finalized"};
     ensure_dev(M, "SparseSym::refill");
+    ensure_refill_map(M);
     M->trip_vals.upload(M->pat.trip_vals());
     dev_gather_sum(M->pat.nnz(), M->slot_ptr.p, M->slot_trip.p, M->trip_vals.p, M->vals.p, g_stream);
     check_launch("refill");
@@ -237,6 +243,7 @@ API int ncl_sym_refill_values(ncl_sym_t M, const double* tv, int where) {
   GUARD({
     if (!M->pat.finalized()) throw Error{NCL_E_LOGIC, "SparseSym::refill: not finalized"};
     ensure_dev(M, "SparseSym::refill");
+    ensure_refill_map(M);
     const int64_t nt = M->pat.num_trips();
     const double* src = tv;
     if (where == NCL_HOST) {

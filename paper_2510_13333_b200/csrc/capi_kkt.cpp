@@ -1,6 +1,8 @@
 // C-ABI for the condensed Newton matrix (K2 assembly).
 #include <cuda_runtime.h>
 
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <memory>
 #include <vector>
@@ -39,46 +41,54 @@ struct ncl_kkt {
 namespace {
 void kkt_upload(ncl_kkt* k) {
   if (k->dev_ready) return;
+  static const bool timing = std::getenv("NCL_ANALYZE_TIMING") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
   ensure_dev(k->K.get(), "kkt");
   k->slot_h.upload(k->map.slot_h);
-  k->slot_diag.upload(k->map.slot_diag);
-  k->jptr.upload(k->map.jptr);
-  k->jterm.upload(k->map.jterm);
-  // compact form (NCL_KKT_GATHER=1 keeps the per-slot gather kernel: A/B only)
-  static const bool gather = std::getenv("NCL_KKT_GATHER") != nullptr;
+  // compact form (csrc/host/kkt.hpp); the per-slot gather form only when a
+  // Jacobian row is too long for the byte offsets or the term count
+  // overflows 32 bits
   const KktMap& M = k->map;
   const int64_t nnz = static_cast<int64_t>(M.slot_h.size()), nt = M.jptr.empty() ? 0 : M.jptr.back();
-  bool ok = !gather && nt < (int64_t(1) << 32) && M.nnzj < (int64_t(1) << 31);
-  std::vector<uint32_t> tp(nnz + 1);
-  std::vector<int> ta(nt), jrow(M.nnzj, 0), dgrank((nnz + 63) / 64 + 1, 0);
-  std::vector<uint8_t> td(nt);
-  std::vector<uint64_t> dgmask((nnz + 63) / 64 + 1, 0);
-  for (int64_t s = 0; ok && s <= nnz; ++s) tp[s] = static_cast<uint32_t>(M.jptr[s]);
-  for (int64_t t = 0; ok && t < nt; ++t) {
-    const int r = M.jterm[3 * t], a = M.jterm[3 * t + 1], b = M.jterm[3 * t + 2];
-    if (a - b < 0 || a - b > 255) ok = false;
-    ta[t] = a;
-    td[t] = static_cast<uint8_t>(a - b);
-    jrow[a] = r;
-    jrow[b] = r;
-  }
-  int next = 0;  // diagonal slots carry variables 0, 1, 2, ... in slot order
-  for (int64_t s = 0; ok && s < nnz; ++s)
-    if (M.slot_diag[s] >= 0) {
-      if (M.slot_diag[s] != next++) ok = false;
-      dgmask[s >> 6] |= 1ull << (s & 63);
+  const bool ok = M.compact && nt < (int64_t(1) << 32) && M.nnzj < (int64_t(1) << 31);
+  if (!ok) {
+    KktMap& W = k->map;
+    if (W.jterm.empty()) {  // rebuild the triples from the compact terms
+      W.jterm.resize(3 * nt);
+      for (int64_t t = 0; t < nt; ++t) {
+        W.jterm[3 * t] = W.jrow[W.ta[t]];
+        W.jterm[3 * t + 1] = W.ta[t];
+        W.jterm[3 * t + 2] = W.ta[t] - W.td[t];
+      }
     }
-  for (size_t w = 1; ok && w < dgmask.size(); ++w) dgrank[w] = dgrank[w - 1] + __builtin_popcountll(dgmask[w - 1]);
-  k->compact = ok;
-  if (ok) {
+    k->slot_diag.upload(W.slot_diag);
+    k->jptr.upload(W.jptr);
+    k->jterm.upload(W.jterm);
+  } else {
+    std::vector<uint32_t> tp(nnz + 1);
+    for (int64_t s = 0; s <= nnz; ++s) tp[s] = static_cast<uint32_t>(M.jptr[s]);
+    std::vector<uint64_t> dgmask((nnz + 63) / 64 + 1, 0);
+    std::vector<int> dgrank(dgmask.size(), 0);
+    // diagonal slots carry variables 0, 1, 2, ... in slot order (one per column, its first slot)
+    int next = 0;
+    for (int64_t s = 0; s < nnz; ++s)
+      if (M.slot_diag[s] >= 0) {
+        if (M.slot_diag[s] != next++) throw Error{NCL_E_INTERNAL, "kkt: diagonal slots out of order"};
+        dgmask[s >> 6] |= 1ull << (s & 63);
+      }
+    for (size_t w = 1; w < dgmask.size(); ++w) dgrank[w] = dgrank[w - 1] + __builtin_popcountll(dgmask[w - 1]);
     k->tp.upload(tp);
-    k->ta.upload(ta);
-    k->td.upload(td);
-    k->jrow.upload(jrow);
+    k->ta.upload(M.ta);
+    k->td.upload(M.td);
+    k->jrow.upload(M.jrow);
     k->dgmask.upload(dgmask);
     k->dgrank.upload(dgrank);
   }
+  k->compact = ok;
   k->dev_ready = true;
+  if (timing)
+    std::fprintf(stderr, "[kkt] device maps      %.3f s\n",
+                 std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
 }
 void assemble(ncl_kkt* K, const double* hess, const double* jac, const double* sigx, double dw, const double* D,
               double* out) {

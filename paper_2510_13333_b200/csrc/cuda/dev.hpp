@@ -223,6 +223,12 @@ constexpr int kTickets = 64;  // ticket counters per symbolic handle
 // forward register-front solve, the register factor phases, the sharded
 // segments
 constexpr int kTicketSeg0 = 40;
+// panel width of the one-CTA dense front factorization (ldlt.cu cta_dense):
+// the diagonal block is factored by one warp in registers, the trailing
+// update is a rank-NCL_CTA_PANEL DMMA update (kPb / 4 k-steps per tile)
+#ifndef NCL_CTA_PANEL
+#define NCL_CTA_PANEL 8
+#endif
 
 extern unsigned long long* g_task_trace;  // device buffer [2 * tasks] or nullptr
 void dev_phase_trace(unsigned long long* buf);  // device buffer [4 * nsn] or nullptr

@@ -447,7 +447,7 @@ __device__ __forceinline__ void cta_dense(double* F, int nr, int w, int f, doubl
     //  (c) all warps apply the rank-8 update F22 -= L21 (D L21)ᵀ to the
     //      trailing lower triangle on the FP64 tensor cores (mma.m8n8k4.f64,
     //      8 x 8 tiles, two k-steps), tiles dealt round-robin to the warps.
-    constexpr int kPb = 8;
+    constexpr int kPb = NCL_CTA_PANEL;  // panel width (csrc/cuda/dev.hpp)
     constexpr int nw = NT / 32;
     __shared__ double s_rd[kPb], s_dl[kPb][kPb];  // 1 / d_k and d_k L(k2, k) of the current diagonal block
     const int lane = tid & 31, warp = tid >> 5;
@@ -532,34 +532,36 @@ __device__ __forceinline__ void cta_dense(double* F, int nr, int w, int f, doubl
       const bool ahead = c1 < w;
       if (m > 0) {
         const int T = (m + 7) >> 3;
-        const int ka = tg, kc = tg + 4;  // this lane's two k indices (A column / B row)
-        const double* La = F + cb_col(c0 + ka, nr);
-        const double* Lc = F + cb_col(c0 + kc, nr);
-        const double da = ka < kb ? La[c0 + ka] : 0.0;
-        const double dc = kc < kb ? Lc[c0 + kc] : 0.0;
+        // this lane's k indices (A column / B row of every m8n8k4 k-step):
+        // k = 4 s + tg, s < kPb / 4
+        constexpr int kS = kPb / 4;
+        const double* Lk[kS];
+        double dk[kS];
+#pragma unroll
+        for (int q = 0; q < kS; ++q) {
+          const int k = 4 * q + tg;
+          Lk[q] = F + cb_col(c0 + min(k, kb - 1), nr);
+          dk[q] = k < kb ? Lk[q][c0 + k] : 0.0;
+        }
         // tiles (ti, tj), tj in [tj_lo, ti]: A fragments in registers, four
-        // tiles in flight (loads, 8 DMMAs, then the read-modify-writes)
+        // tiles in flight (loads, the rank-kb DMMAs, then the read-modify-writes)
         auto tile_row = [&](int ti, int tj_lo, int tj_hi) {
           const int i = c1 + ti * 8 + g;
-          double a0 = 0.0, a1 = 0.0;
-          if (i < nr) {
-            if (ka < kb) a0 = La[i];
-            if (kc < kb) a1 = Lc[i];
-          }
+          double av[kS];
+#pragma unroll
+          for (int q = 0; q < kS; ++q) av[q] = (i < nr && 4 * q + tg < kb) ? Lk[q][i] : 0.0;
           for (int tj0 = tj_lo; tj0 <= tj_hi; tj0 += 4) {
-            double b0[4], b1[4], acc[4][2];
+            double acc[4][2];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const int j = c1 + (tj0 + u) * 8 + g;
               const bool ok = tj0 + u <= tj_hi && j < nr;
-              b0[u] = ok && ka < kb ? da * La[j] : 0.0;
-              b1[u] = ok && kc < kb ? dc * Lc[j] : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
               acc[u][0] = acc[u][1] = 0.0;
-              dmma(acc[u][0], acc[u][1], a0, b0[u]);
-              dmma(acc[u][0], acc[u][1], a1, b1[u]);
+#pragma unroll
+              for (int q = 0; q < kS; ++q) {
+                const double bv = ok && 4 * q + tg < kb ? dk[q] * Lk[q][j] : 0.0;
+                dmma(acc[u][0], acc[u][1], av[q], bv);
+              }
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {

@@ -1,11 +1,22 @@
 #include "kkt.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 
 namespace nclb {
 
 KktMap build_kkt(int n, int m, const std::vector<std::pair<int, int>>& hc,
                  const std::vector<std::pair<int, int>>& jc, SymPattern& P) {
+  static const bool timing = std::getenv("NCL_ANALYZE_TIMING") != nullptr;
+  auto t = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!timing) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[kkt] %-16s %.3f s\n", what, std::chrono::duration<double>(now - t).count());
+    t = now;
+  };
   KktMap K;
   K.n = n;
   K.m = m;
@@ -25,19 +36,22 @@ KktMap build_kkt(int n, int m, const std::vector<std::pair<int, int>>& hc,
   K.tcol.reserve(nt);
   for (const auto& e : hc) K.trow.push_back(e.first), K.tcol.push_back(e.second);
   for (int i = 0; i < n; ++i) K.trow.push_back(i), K.tcol.push_back(i);
-  std::vector<int> terms;
-  terms.reserve(3 * njt);
-  for (int r = 0; r < m; ++r)
-    for (int64_t a = rp[r]; a < rp[r + 1]; ++a)
+  K.jrow.resize(K.nnzj);
+  for (int r = 0; r < m; ++r) {
+    if (rp[r + 1] - rp[r] > 256) K.compact = false;  // a - b would not fit a byte
+    for (int64_t a = rp[r]; a < rp[r + 1]; ++a) {
+      K.jrow[a] = r;
       for (int64_t b = rp[r]; b <= a; ++b) {
         K.trow.push_back(jc[a].second);  // columns ascending inside a row: col[a] >= col[b]
         K.tcol.push_back(jc[b].second);
-        terms.push_back(r);
-        terms.push_back(static_cast<int>(a));
-        terms.push_back(static_cast<int>(b));
       }
+    }
+  }
+  lap("triplets");
   P.add_pattern(K.trow, K.tcol);
+  lap("add_pattern");
   P.finalize();
+  lap("finalize");
   const int nnz = P.nnz();
   const auto& slot = P.trip_slot();
   K.slot_h.assign(nnz, -1);
@@ -45,22 +59,33 @@ KktMap build_kkt(int n, int m, const std::vector<std::pair<int, int>>& hc,
   K.jptr.assign(nnz + 1, 0);
   for (int64_t k = K.nnzh + n; k < nt; ++k) K.jptr[slot[k] + 1]++;
   for (int s = 0; s < nnz; ++s) K.jptr[s + 1] += K.jptr[s];
-  K.jterm.resize(3 * njt);
+  for (int64_t k = 0; k < K.nnzh; ++k) K.slot_h[slot[k]] = static_cast<int>(k);
+  for (int64_t k = K.nnzh; k < K.nnzh + n; ++k) K.slot_diag[slot[k]] = static_cast<int>(k - K.nnzh);
+  // terms in triplet order (rows ascending, a ascending, b <= a) dealt to
+  // their slots: inside a slot they stay in triplet order (the refill's
+  // summation order)
   std::vector<int64_t> fp(K.jptr.begin(), K.jptr.end() - 1);
-  for (int64_t k = 0; k < nt; ++k) {
-    const int s = slot[k];
-    if (k < K.nnzh) {
-      K.slot_h[s] = static_cast<int>(k);
-    } else if (k < K.nnzh + n) {
-      K.slot_diag[s] = static_cast<int>(k - K.nnzh);
-    } else {
-      const int64_t t = k - K.nnzh - n;
-      const int64_t q = fp[s]++;
-      K.jterm[3 * q] = terms[3 * t];
-      K.jterm[3 * q + 1] = terms[3 * t + 1];
-      K.jterm[3 * q + 2] = terms[3 * t + 2];
-    }
+  if (K.compact) {
+    K.ta.resize(njt);
+    K.td.resize(njt);
+  } else {
+    K.jterm.resize(3 * njt);
   }
+  int64_t k = K.nnzh + n;
+  for (int r = 0; r < m; ++r)
+    for (int64_t a = rp[r]; a < rp[r + 1]; ++a)
+      for (int64_t b = rp[r]; b <= a; ++b, ++k) {
+        const int64_t q = fp[slot[k]]++;
+        if (K.compact) {
+          K.ta[q] = static_cast<int>(a);
+          K.td[q] = static_cast<uint8_t>(a - b);
+        } else {
+          K.jterm[3 * q] = r;
+          K.jterm[3 * q + 1] = static_cast<int>(a);
+          K.jterm[3 * q + 2] = static_cast<int>(b);
+        }
+      }
+  lap("slot maps");
   return K;
 }
 

@@ -29,8 +29,15 @@ struct KktMap {
   // per K slot: Hessian entry index or -1; diagonal flag; JᵀDJ terms
   std::vector<int> slot_h;
   std::vector<int> slot_diag;   // variable index if the slot is a diagonal, else -1
-  std::vector<int64_t> jptr;    // [nnzK+1]
-  std::vector<int> jterm;       // (r, a, b) triples
+  std::vector<int64_t> jptr;    // [nnzK+1] term range of each slot (triplet order inside)
+  // the terms D_r J_a J_b of every slot, a >= b in the same Jacobian row r:
+  // ta = a, td = a - b (uint8: a row has <= 256 entries, else `compact` is
+  // false and jterm holds (r, a, b) triples instead), jrow = row of each
+  // Jacobian entry
+  bool compact = true;
+  std::vector<int> ta, jrow;
+  std::vector<uint8_t> td;
+  std::vector<int> jterm;
 };
 
 // Builds the triplet order and finalizes `pattern` (a fresh SymPattern of

@@ -21,6 +21,7 @@ void SymPattern::add(int row, int col, double value) {
   if (row < col) fail(NCL_E_INVALID, "SparseSym::add: row < col (store lower triangle)");
   if (col < 0 || row >= n_) fail(NCL_E_INVALID, "SparseSym::add: index out of range");
   if (!finalized_) {
+    ensure_tvals();
     trows_.push_back(row);
     tcols_.push_back(col);
     tvals_.push_back(value);
@@ -29,6 +30,7 @@ void SymPattern::add(int row, int col, double value) {
   // refill mode: coordinates must replay the original assembly order
   if (cursor_ >= static_cast<int64_t>(trows_.size()) || trows_[cursor_] != row || tcols_[cursor_] != col)
     fail(NCL_E_LOGIC, "SparseSym::add: refill coordinates do not match original assembly");
+  ensure_tvals();
   tvals_[cursor_] = value;
   ++cursor_;
 }
@@ -39,9 +41,9 @@ void SymPattern::add_pattern(const std::vector<int>& rows, const std::vector<int
     if (rows[k] < cols[k]) fail(NCL_E_INVALID, "SparseSym::add: row < col (store lower triangle)");
     if (cols[k] < 0 || rows[k] >= n_) fail(NCL_E_INVALID, "SparseSym::add: index out of range");
   }
+  ensure_tvals();  // earlier explicit values keep their positions; these are implicit zeros
   trows_.insert(trows_.end(), rows.begin(), rows.end());
   tcols_.insert(tcols_.end(), cols.begin(), cols.end());
-  tvals_.resize(trows_.size(), 0.0);
 }
 
 // --- SparseSym::finalize (sparse_sym.cpp:28-56) -----------------------------
@@ -101,6 +103,7 @@ void SymPattern::begin_refill() {
 void SymPattern::refill() {
   if (!finalized_) fail(NCL_E_LOGIC, "SparseSym::refill: not finalized");
   vals_.assign(rowind_.size(), 0.0);
+  // triplets past tvals_.size() are implicit zeros (add_pattern): nothing to add
   for (size_t k = 0; k < tvals_.size(); ++k) vals_[trip_slot_[k]] += tvals_[k];
 }
 

@@ -48,7 +48,12 @@ class SymPattern {
   int64_t num_trips() const { return static_cast<int64_t>(trows_.size()); }
   const std::vector<int>& trip_rows() const { return trows_; }
   const std::vector<int>& trip_cols() const { return tcols_; }
-  const std::vector<double>& trip_vals() const { return tvals_; }
+  // triplet values; triplets added by add_pattern carry an implicit 0.0
+  // that is materialised only when a value is asked for
+  const std::vector<double>& trip_vals() const {
+    ensure_tvals();
+    return tvals_;
+  }
   // CSR over value slots listing triplet indices in triplet order; the GPU
   // refill gathers with it so sums happen in the reference order (:66).
   void slot_trip_csr(std::vector<int>& ptr, std::vector<int>& idx) const;
@@ -59,7 +64,10 @@ class SymPattern {
   int n_;
   bool finalized_ = false;
   std::vector<int> trows_, tcols_;
-  std::vector<double> tvals_;
+  mutable std::vector<double> tvals_;  // may be shorter than trows_: the rest are 0.0
+  void ensure_tvals() const {
+    if (tvals_.size() < trows_.size()) tvals_.resize(trows_.size(), 0.0);
+  }
   std::vector<int> trip_slot_;
   std::vector<int> colptr_, rowind_;
   std::vector<double> vals_;
