@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 
 #include "dev.hpp"
@@ -123,6 +124,93 @@ __global__ void __launch_bounds__(256) bf_panel(BigArgs a, int step) {
     const int c = e / k0, i = e % k0;
     W[static_cast<int64_t>(c) * nr + i] = 0.0;
   }
+}
+
+// --- panel step split in two (the single-CTA bf_panel above was bound by its
+// column-by-column shared-memory updates over the whole tall panel):
+// bf_diag: one warp per front factors the kw x kw diagonal block of panel
+// `step` in registers (lane i = row k0 + i, pivots broadcast by shuffles) and
+// leaves 1 / d_c on W's diagonal and d_c L(c2, c) below it (W's rows
+// [k0, k1) are otherwise unused); bf_rows: every row below the block is
+// independent given those — one thread per row, rows spread over many CTAs —
+// L(i, c) = x_c / d_c as x_c (1 / d_c), x_c2 -= L(i, c) (d_c L(c2, c)), and
+// W(i, c) = L(i, c) d_c for the trailing update. Per row and per column the
+// operations and their order are bf_panel's.
+__global__ void __launch_bounds__(32) bf_diag(BigArgs a, int step) {
+  const BigDesc b = a.d[blockIdx.x];
+  if (step >= b.npan) return;
+  const int nr = b.nr, k0 = step * b.pw, k1 = min(b.w, k0 + b.pw), kw = k1 - k0;
+  const int lane = threadIdx.x;
+  double* F = a.Fs + b.foff;
+  double* W = a.Ws + b.woff;
+  const double thresh = __ldcg(a.thresh);
+  double x[kBs];
+#pragma unroll
+  for (int c = 0; c < kBs; ++c)
+    x[c] = (c < kw && c <= lane && lane < kw) ? F[static_cast<int64_t>(k0 + c) * nr + k0 + lane] : 0.0;
+#pragma unroll
+  for (int c = 0; c < kBs; ++c) {
+    if (c < kw) {
+      const double d = __shfl_sync(kFullMask, x[c], c);
+      const double rd = 1.0 / d;
+      if (lane == 0) {
+        a.D[b.f + k0 + c] = d;
+        if (fabs(d) <= thresh) atomicMin(a.zp, b.f + k0 + c);
+      }
+      if (lane > c && lane < kw) x[c] *= rd;
+      const double dlo = d * x[c];  // lane c2: d_c L(c2, c)
+      if (lane == c) W[static_cast<int64_t>(c) * nr + k0 + c] = rd;
+      if (lane > c && lane < kw) W[static_cast<int64_t>(c) * nr + k0 + lane] = dlo;
+#pragma unroll
+      for (int c2 = c + 1; c2 < kBs; ++c2) {
+        if (c2 < kw) {
+          const double dl = __shfl_sync(kFullMask, dlo, c2);
+          if (lane >= c2 && lane < kw) x[c2] -= x[c] * dl;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < kBs; ++c)
+    if (c < kw && c <= lane && lane < kw) F[static_cast<int64_t>(k0 + c) * nr + k0 + lane] = x[c];
+}
+
+__global__ void __launch_bounds__(256) bf_rows(BigArgs a, int step) {
+  __shared__ double s_dl[kBs][kBs + 1];  // [c][c2]: d_c L(c2, c); [c][c]: 1 / d_c
+  __shared__ double s_d[kBs];
+  const BigDesc b = a.d[blockIdx.y];
+  if (step >= b.npan) return;
+  const int nr = b.nr, k0 = step * b.pw, k1 = min(b.w, k0 + b.pw), kw = k1 - k0;
+  const int i0 = k1 + blockIdx.x * blockDim.x;
+  if (i0 >= nr) return;
+  double* F = a.Fs + b.foff;
+  double* W = a.Ws + b.woff;
+  for (int e = threadIdx.x; e < kw * kw; e += blockDim.x) {
+    const int c = e / kw, c2 = e % kw;
+    if (c2 >= c) s_dl[c][c2] = W[static_cast<int64_t>(c) * nr + k0 + c2];
+  }
+  for (int c = threadIdx.x; c < kw; c += blockDim.x) s_d[c] = F[static_cast<int64_t>(k0 + c) * nr + k0 + c];
+  __syncthreads();
+  const int i = i0 + threadIdx.x;
+  if (i >= nr) return;
+  double x[kBs];
+#pragma unroll
+  for (int c = 0; c < kBs; ++c) x[c] = c < kw ? F[static_cast<int64_t>(k0 + c) * nr + i] : 0.0;
+#pragma unroll
+  for (int c = 0; c < kBs; ++c) {
+    if (c < kw) {
+      x[c] *= s_dl[c][c];
+#pragma unroll
+      for (int c2 = c + 1; c2 < kBs; ++c2)
+        if (c2 < kw) x[c2] -= x[c] * s_dl[c][c2];
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < kBs; ++c)
+    if (c < kw) {
+      F[static_cast<int64_t>(k0 + c) * nr + i] = x[c];
+      W[static_cast<int64_t>(c) * nr + i] = x[c] * s_d[c];
+    }
 }
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double av, double bv) {
@@ -257,8 +345,18 @@ void dev_factor_big_batch(const DevSymb& S, DevFactor& Fa, const double* kvals, 
       const int nt = (b.nr - k1 + kTile - 1) / kTile;
       tiles = std::max(tiles, nt * (nt + 1) / 2);
     }
-    bf_panel<<<nf, 256, psmem, st>>>(a, k);
-    g_kernel_launches += 1;
+    static const bool one_cta = std::getenv("NCL_BF_PANEL") != nullptr;  // A/B: the single-CTA panel step
+    if (one_cta) {
+      bf_panel<<<nf, 256, psmem, st>>>(a, k);
+      g_kernel_launches += 1;
+    } else {
+      int rows = 0;
+      for (const BigDesc& b : h)
+        if (k < b.npan) rows = std::max(rows, b.nr - std::min(b.w, k * b.pw + b.pw));
+      bf_diag<<<nf, 32, 0, st>>>(a, k);
+      if (rows > 0) bf_rows<<<dim3((rows + 255) / 256, nf), 256, 0, st>>>(a, k);
+      g_kernel_launches += 1 + (rows > 0);
+    }
     if (tiles > 0) {
       bf_syrk_dmma<<<dim3(tiles, nf), 128, 0, st>>>(a, k);
       g_kernel_launches += 1;
