@@ -340,11 +340,20 @@ def main():
     # ---- e2e through the C-ABI with host buffers
     vals_h = torch.from_numpy(A.values()).pin_memory()
     x_h = torch.empty(n, dtype=torch.float64).pin_memory()
-    for _ in range(2):
-        A.set_values(vals_h, where=ps.HOST)
-        refactor()
-        x_h.copy_(b_h)
-        solve(x_h, ps.HOST)
+    def e2e_step():
+        if plan is None:
+            # one C-ABI call: H2D of K's values and of b (the latter under the
+            # factorization), factor, solve, D2H of x and of the status words
+            F.factor_solve_host(A, vals_h, b_h, x_h)
+        else:
+            A.set_values(vals_h, where=ps.HOST)  # H2D of K's values
+            refactor()
+            x_h.copy_(b_h)
+            solve(x_h, ps.HOST)  # H2D of b, D2H of x (synchronous)
+            F._status()  # D2H of status + inertia
+
+    for _ in range(max(2, a.warmup)):  # the same calls as the timed steps
+        e2e_step()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -354,11 +363,7 @@ def main():
             flush.fill_(1.0)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        A.set_values(vals_h, where=ps.HOST)  # H2D of K's values
-        refactor()
-        x_h.copy_(b_h)
-        solve(x_h, ps.HOST)  # H2D of b, D2H of x (synchronous)
-        sp, zp, *_ = F._status()  # D2H of status + inertia
+        e2e_step()
         e2e.append(time.perf_counter() - t0)
     e2e_ms = 1e3 * sum(e2e) / len(e2e)
     if dist:

@@ -116,6 +116,13 @@ int ncl_fact_solve(ncl_fact_t F, double* x, int where);           /* solve_in_pl
 /* solve_refined(F, M, b, target, max_sweeps) -> RefinedSolve */
 int ncl_solve_refined(ncl_fact_t F, ncl_sym_t M, const double* b, double target, int max_sweeps, double* x,
                       int where, double* residual, int* sweeps, int* converged);
+/* refill(values) + factorize + solve of a host caller in one call: M's
+ * values (nnz) and b (n) from host memory, x (n) back; the rhs upload runs
+ * on a copy stream underneath the factorization, one synchronisation at the
+ * end (pinned host buffers for the overlap). status / zero_pivot_index /
+ * inertia as ncl_fact_status; x is meaningful only when status == 0. */
+int ncl_factor_solve_host(ncl_fact_t F, ncl_sym_t M, const double* vals, const double* b, double* x,
+                          double pivot_tol, int* status, int* zero_pivot_index, int* n_pos, int* n_neg, int* n_zero);
 /* test/inspection only: L as reference-layout CSC over permuted indices
  * (lp[n+1], li[l_nnz], lx[l_nnz]) */
 int ncl_fact_get_L(ncl_fact_t F, int* lp, int* li, double* lx);

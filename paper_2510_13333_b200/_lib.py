@@ -72,6 +72,7 @@ _SIGS = {
     "ncl_fact_status": (i32, [P, pi32, pi32, pi32, pi32, pi32]),
     "ncl_fact_diagonal": (i32, [P, P]),
     "ncl_fact_solve": (i32, [P, P, i32]),
+    "ncl_factor_solve_host": (i32, [P, P, P, P, P, C.c_double] + [C.POINTER(C.c_int)] * 5),
     "ncl_solve_refined": (i32, [P, P, P, f64, i32, P, i32, pf64, pi32, pi32]),
     "ncl_fact_get_L": (i32, [P, P, P, P]),
 }

@@ -691,8 +691,12 @@ TaskLayout build_layout(const Supernodal& Z, const std::vector<int>& list, int s
         b.f = Z.sn_first[s];
         b.w = Z.sn_first[s + 1] - Z.sn_first[s];
         b.nr = nr;
-        b.pw = 32;  // panel width: while a panel fits 220 KB of shared memory (a function of nr only)
-        while (b.pw > 8 && static_cast<int64_t>(nr) * b.pw * 8 > 220 * 1024) b.pw /= 2;
+        // panel width: 32 (the diagonal block is one warp, the rows below
+        // stream through registers: no shared-memory cap on nr); the
+        // NCL_BF_PANEL=1 A/B path stages the whole panel and keeps the cap
+        static const bool staged = std::getenv("NCL_BF_PANEL") != nullptr;
+        b.pw = 32;
+        while (staged && b.pw > 8 && static_cast<int64_t>(nr) * b.pw * 8 > 220 * 1024) b.pw /= 2;
         b.npan = nr <= kCtaFront ? 0 : (b.w + b.pw - 1) / b.pw;  // one CTA (dev_big_cta)
         b.g0 = Z.gm_ptr[s];
         b.g1 = Z.gm_ptr[s + 1];
@@ -1229,6 +1233,54 @@ API int ncl_solve_refined(ncl_fact_t F, ncl_sym_t M, const double* b, double tar
     solve_refined_dev(F, M, F->work3.p, F->work1.p, target, max_sweeps, residual, sweeps, converged);
     ck(cudaMemcpyAsync(x, F->work1.p, n * sizeof(double), cudaMemcpyDeviceToHost, g_stream), "D2H");
     ck(cudaStreamSynchronize(g_stream), "sync");
+  });
+}
+
+// One factor + solve from host buffers with a single synchronisation: the
+// values' H2D and the factorization on the library stream, the right-hand
+// side's H2D on a copy stream underneath the factorization, then the solve,
+// the D2H of x and of the status words.
+API int ncl_factor_solve_host(ncl_fact_t F, ncl_sym_t M, const double* vals, const double* b, double* x,
+                              double pivot_tol, int* status, int* zero_pivot_index, int* n_pos, int* n_neg,
+                              int* n_zero) {
+  GUARD({
+    if (F->sharded_world > 1) throw Error{NCL_E_LOGIC, "factor_solve: factor of a sharded world > 1 run"};
+    check_match(M, F->S);
+    ensure_dev(M, "factor_solve");
+    static cudaStream_t cs = nullptr;
+    static cudaEvent_t eb = nullptr;
+    if (!cs) {
+      ck(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "cudaStreamCreate");
+      ck(cudaEventCreateWithFlags(&eb, cudaEventDisableTiming), "event");
+    }
+    const int n = F->S->core.n;
+    const int64_t nz = M->pat.nnz();
+    // the copy stream may only overwrite work1 once the previous solve is done
+    ck(cudaEventRecord(eb, g_stream), "event");
+    ck(cudaStreamWaitEvent(cs, eb, 0), "wait");
+    if (n > 0) ck(cudaMemcpyAsync(F->work1.p, b, n * sizeof(double), cudaMemcpyHostToDevice, cs), "H2D b");
+    ck(cudaEventRecord(eb, cs), "event");
+    ck(cudaMemcpyAsync(M->vals.p, vals, nz * sizeof(double), cudaMemcpyHostToDevice, g_stream), "H2D values");
+    run_factor(F, M, pivot_tol);
+    F->sharded_world = 1;
+    ck(cudaStreamWaitEvent(g_stream, eb, 0), "wait");
+    dev_solve(F->S->d, F->F, F->work1.p, F->work1.p, g_stream);
+    if (n > 0) ck(cudaMemcpyAsync(x, F->work1.p, n * sizeof(double), cudaMemcpyDeviceToHost, g_stream), "D2H x");
+    int h[4];
+    ck(cudaMemcpyAsync(h, F->istat.p, sizeof(h), cudaMemcpyDeviceToHost, g_stream), "D2H status");
+    ck(cudaStreamSynchronize(g_stream), "sync");
+    check_launch("factor_solve");
+    if (h[0] < n) {
+      *status = 1;
+      *zero_pivot_index = F->S->core.perm[h[0]];
+      *n_pos = *n_neg = *n_zero = 0;
+    } else {
+      *status = 0;
+      *zero_pivot_index = -1;
+      *n_pos = h[1];
+      *n_neg = h[2];
+      *n_zero = h[3];
+    }
   });
 }
 

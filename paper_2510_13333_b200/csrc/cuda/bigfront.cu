@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(32) bf_diag(BigArgs a, int step) {
   for (int c = 0; c < kBs; ++c) {
     if (c < kw) {
       const double d = __shfl_sync(kFullMask, x[c], c);
-      const double rd = 1.0 / d;
+      const double rd = __drcp_rn(d);  // correctly rounded: = 1.0 / d
       if (lane == 0) {
         a.D[b.f + k0 + c] = d;
         if (fabs(d) <= thresh) atomicMin(a.zp, b.f + k0 + c);

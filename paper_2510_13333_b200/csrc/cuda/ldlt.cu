@@ -484,7 +484,7 @@ __device__ __forceinline__ void cta_dense(double* F, int nr, int w, int f, doubl
       for (int k = 0; k < kPb; ++k) {
         if (k < kb) {
           const double dk = __shfl_sync(kFull, x[k], k);
-          if (lane == k) s_rd[k] = 1.0 / dk;
+          if (lane == k) s_rd[k] = __drcp_rn(dk);  // correctly rounded: = 1.0 / dk, half the latency
           if (lane > k && lane < kb) s_dl[k][lane] = dk * x[k];
         }
       }

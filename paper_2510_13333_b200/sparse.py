@@ -298,6 +298,15 @@ class Factorization:
     def refactorize(self, M: SparseSym, pivot_tol: float = 1e-12) -> None:
         check(lib.ncl_refactorize(self._h, M.handle, float(pivot_tol)))
 
+    def factor_solve_host(self, M: SparseSym, vals, b, x, pivot_tol: float = 1e-12):
+        """ncl_factor_solve_host: M's values and b from host buffers (numpy
+        or pinned torch CPU tensors), x back, one synchronisation; returns
+        (status, zero_pivot_index, Inertia)"""
+        st, zp, a, bb, c = (C.c_int() for _ in range(5))
+        check(lib.ncl_factor_solve_host(self._h, M.handle, _ptr(vals), _ptr(b), _ptr(x), float(pivot_tol),
+                                        C.byref(st), C.byref(zp), C.byref(a), C.byref(bb), C.byref(c)))
+        return ("ok" if st.value == 0 else "zero_pivot"), zp.value, Inertia(a.value, bb.value, c.value)
+
     def L_csc(self):
         """Test-only: L in the reference's CSC layout (permuted indices)."""
         info = self._symb.info() if self._symb is not None else None

@@ -219,3 +219,28 @@ def test_scopf_kkt_parity(gpu, grid, K, min_big=0):
     D1 = F.diagonal()
     F.refactorize(A)
     assert np.array_equal(F.diagonal(), D1)
+
+
+@pytest.mark.gpu
+def test_factor_solve_host_matches_separate_calls(gpu):
+    """ncl_factor_solve_host (values + rhs from host, one synchronisation)
+    gives bitwise the refill -> refactorize -> solve sequence's result"""
+    from paper_2510_13333_b200.kkt import Kkt
+    from paper_2510_13333_b200.scopf import Scopf
+    s = Scopf("case118", 4)
+    M = s.build_model()
+    kk = Kkt(M)
+    rng = np.random.default_rng(11)
+    kk.assemble(0.1 * rng.standard_normal(M.nnzh), rng.standard_normal(M.nnzj), 1.0 + rng.random(s.n), 0.0,
+                10.0 + rng.random(M.m))
+    A = kk.matrix
+    S = ps.analyze(A)
+    F = ps.factorize(A, S)
+    vals = A.values().copy() * 1.25
+    b = rng.standard_normal(s.n)
+    x = np.empty(s.n)
+    st, zp, ia = F.factor_solve_host(A, vals, b, x)
+    A.set_values(vals, where=ps.HOST)
+    F2 = ps.factorize(A, S)
+    assert st == F2.status == "ok" and ia == F2.inertia
+    assert np.array_equal(x, F2.solve(b))
