@@ -449,14 +449,18 @@ void build_batches(const Supernodal& Z, const std::vector<int>& list, int split,
       for (size_t x = 0; x < v.size(); ++x) {
         const int s = v[x];
         const int ix = static_cast<int>(x % 32);
-        if (R == 1 && ix == 0) {
+        const int ixc = static_cast<int>(x % per);  // front index inside its chunk (the solve's lane)
+        if (ixc == 0) {
           int maxnch = 0;
-          for (size_t y = x; y < std::min(v.size(), x + 32); ++y) maxnch = std::max(maxnch, Z.cptr[v[y] + 1] - Z.cptr[v[y]]);
-          abase = static_cast<int64_t>(B.amap.size());
-          B.amap.resize(B.amap.size() + static_cast<size_t>(np) * 32, -1);
-          wbase = static_cast<int64_t>(B.cmapw.size());
-          B.cmapw.resize(B.cmapw.size() + static_cast<size_t>(maxnch) * nw * 32, 0xffffffffu);
-          B.chunks[chunk0 + x / 32].smap = static_cast<int>(B.smapw.size());
+          for (size_t y = x; y < std::min(v.size(), x + per); ++y)
+            maxnch = std::max(maxnch, Z.cptr[v[y] + 1] - Z.cptr[v[y]]);
+          if (R == 1) {
+            abase = static_cast<int64_t>(B.amap.size());
+            B.amap.resize(B.amap.size() + static_cast<size_t>(np) * 32, -1);
+            wbase = static_cast<int64_t>(B.cmapw.size());
+            B.cmapw.resize(B.cmapw.size() + static_cast<size_t>(maxnch) * nw * 32, 0xffffffffu);
+          }
+          B.chunks[chunk0 + x / per].smap = static_cast<int>(B.smapw.size());
           B.smapw.resize(B.smapw.size() + static_cast<size_t>(maxnch) * kSmapStride * 32, 0xffffffffu);
         }
         batched[s] = 1;
@@ -483,16 +487,18 @@ void build_batches(const Supernodal& Z, const std::vector<int>& list, int split,
           const int c = Z.child[q], qi = q - Z.cptr[s];
           const int m2c = nrof(c) - wof(c);
           const int* rel = Z.relp.data() + Z.sn_rptr[c] + wof(c);
-          if (R == 1) {
-            // forward solve: parent row rel[kk] <- the child's CV entry kk
-            const int64_t sb = B.chunks[chunk0 + x / 32].smap;
+          {
+            // forward solve (one thread per front, any R): parent row rel[kk] <- the child's CV entry kk
+            const int64_t sb = B.chunks[chunk0 + x / per].smap;
             for (int kk = 0; kk < m2c; ++kk) {
-              uint32_t& wd = B.smapw[sb + (static_cast<int64_t>(qi) * kSmapStride + rel[kk] / 4) * 32 + ix];
+              uint32_t& wd = B.smapw[sb + (static_cast<int64_t>(qi) * kSmapStride + rel[kk] / 4) * 32 + ixc];
               wd = (wd & ~(0xffu << (8 * (rel[kk] % 4)))) | (static_cast<uint32_t>(kk) << (8 * (rel[kk] % 4)));
             }
             const int64_t cvo = Z.sn_rptr[c] + wof(c);
             if (cvo >= (int64_t(1) << 31)) throw Error{NCL_E_INVALID, "analyze: row list exceeds int32 addressing"};
-            B.smapw[sb + (static_cast<int64_t>(qi) * kSmapStride + kSmapWords) * 32 + ix] = static_cast<uint32_t>(cvo);
+            B.smapw[sb + (static_cast<int64_t>(qi) * kSmapStride + kSmapWords) * 32 + ixc] = static_cast<uint32_t>(cvo);
+          }
+          if (R == 1) {
             for (int j = 0; j < m2c; ++j)
               for (int ii = j; ii < m2c; ++ii) {
                 const int64_t pp = cb_col(rel[j], nr) + rel[ii];

@@ -2067,7 +2067,6 @@ __device__ __forceinline__ void reg_solve_dispatch(const SolveArgs& a, const Reg
                                                    const uint32_t* smapw, std::integer_sequence<int, K...>) {
   (((ch.shape == K) ? [&] {
     constexpr int NR = kRegShapes[K][0], W = kRegShapes[K][1];
-    static_assert(kRegShapes[K][2] == 1, "register-front solves assume one thread per front");
     if (lane < ch.n) {
       const RegInst I = inst[ch.first + lane];
       if constexpr (FWD) reg_fwd_front<NR, W>(a, I, cid, smapw + ch.smap + lane);

@@ -17,6 +17,10 @@ static_assert(kCtaFront * (kCtaFront + 1) / 2 * 8 <= 113 * 1024, "two CTA fronts
 // front in registers (<= 46 doubles per lane).
 constexpr int kRegShapes[][3] = {{5, 2, 1}, {6, 1, 1}, {7, 1, 1}, {8, 1, 1}, {8, 2, 1},
                                  {9, 1, 1}, {10, 1, 1}, {10, 2, 1}};
+// measured (r02): adding (11..14, 1..4) with four lanes per front moved 31 k
+// supernodes out of the subtree groups (warp phase 375 -> 301 us) but grew
+// the register phase 226 -> 345 us and the forward register solve 89 -> 155
+// us (195 registers): a net loss
 constexpr int kNumRegShapes = sizeof(kRegShapes) / sizeof(kRegShapes[0]);
 // shapes [0, kRegTier1) run first as their own closed forest in a kernel
 // compiled for them alone (small register footprint, high occupancy); the
