@@ -761,7 +761,7 @@ void upload_top(TopSched& t, std::vector<DevBuf<BigDesc>>& store) {
     }
 }
 
-DevTasks upload_layout(TaskLayout& L, LayoutDev& D) {
+DevTasks upload_layout(TaskLayout& L, LayoutDev& D, const Supernodal& Z) {
   upload_top(L.top, D.top);
   D.nodes.upload(L.nodes);
   D.tptr.upload(L.tptr);
@@ -786,8 +786,22 @@ DevTasks upload_layout(TaskLayout& L, LayoutDev& D) {
     L.batch.dev_cmap = D.bcmap.p;
     L.batch.dev_ccb = D.bccb.p;
   }
-  return DevTasks{D.nodes.p, D.tptr.p, D.prog.p, D.gpo.p, static_cast<int>(L.tptr.size()) - 1, L.nleaf, L.split,
-                  &L.top, has_batch ? &L.batch : nullptr};
+  DevTasks T{D.nodes.p, D.tptr.p, D.prog.p, D.gpo.p, static_cast<int>(L.tptr.size()) - 1, L.nleaf, L.split,
+             &L.top, has_batch ? &L.batch : nullptr};
+  // a last CTA task with many contributing children (the separator root)
+  // gathers its contribution vectors GPU-wide in the forward solve
+  if (T.n > T.split + 1) {
+    const int s = L.nodes[L.tptr[T.n - 1]];
+    if (s < static_cast<int>(Z.cv_ptr.size()) - 1 && Z.cv_ptr[s + 1] > Z.cv_ptr[s]) {
+      const int nr = static_cast<int>(Z.sn_rptr[s + 1] - Z.sn_rptr[s]);
+      const int64_t nsrc = Z.cvsp[Z.cv_ptr[s + 1]] - Z.cvsp[Z.cv_ptr[s]];
+      if (nsrc > 32 * static_cast<int64_t>(nr) && nsrc >= 8192) {
+        T.root_heavy = s;
+        T.root_nr = nr;
+      }
+    }
+  }
+  return T;
 }
 
 void upload_symb(ncl_symb* S) {
@@ -890,7 +904,7 @@ void upload_symb(ncl_symb* S) {
   d.cvsp = S->cvsp.p;
   d.cvsrc = S->cvsrc.p;
   d.meta = S->meta.p;
-  d.ftasks = upload_layout(S->flay, S->fdev);
+  d.ftasks = upload_layout(S->flay, S->fdev, Z);
   d.tasks = S->lay.tptr.empty()
                 ? d.ftasks
                 : DevTasks{S->lay_nodes.p, S->lay_tptr.p, S->lay_prog.p, S->lay_gpo.p,
@@ -1415,8 +1429,8 @@ void shard_upload(ncl_shard* sh) {
   if (sh->dev_ready) return;
   ensure_init();
   upload_symb(sh->S);
-  sh->ftA = upload_layout(sh->flayA, sh->fdevA);
-  sh->ftB = upload_layout(sh->flayB, sh->fdevB);
+  sh->ftA = upload_layout(sh->flayA, sh->fdevA, sh->S->Z);
+  sh->ftB = upload_layout(sh->flayB, sh->fdevB, sh->S->Z);
   sh->bids.upload(sh->P.boundary);
   sh->bowner.upload(sh->P.bowner);
   sh->cb_off.upload(sh->P.cb_pack_off);

@@ -132,6 +132,8 @@ struct DevTasks {
   int n = 0, nleaf = 0, split = 0;  // counts / indices in TASKS
   const TopSched* top = nullptr;    // host pointer; nullptr or !any_big -> one persistent launch
   const BatchSched* batch = nullptr;  // host pointer; batched subtrees run before the task list (factor)
+  int root_heavy = -1;  // the last task's node when its forward CV gather runs GPU-wide (fwd_root_gather)
+  int root_nr = 0;
 };
 
 // Symbolic schedule resident in HBM (built once from host Supernodal).

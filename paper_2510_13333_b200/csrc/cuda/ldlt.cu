@@ -64,11 +64,15 @@ __device__ __forceinline__ void wait_flag(const int* f, int epoch) {
 }
 
 
-// x / d with a zero numerator short-circuited: the FP64 division's fast path
-// rejects x == 0 (exponent check) and CALLs the slow-path subroutine, and
-// fronts are full of structural zeros. Divides 1 / d instead (the operand is
-// laundered through asm so the compiler cannot fold the select back into the
-// division) and returns +0 (instead of a signed zero). Branch-free.
+// x / d with a zero numerator short-circuited (kept for reference; the
+// factor and solve chains now multiply by the correctly rounded reciprocal
+// __drcp_rn(d) — 60 cycles once per pivot instead of a 113-cycle division per
+// element on the dependency chain, and no slow path on zero numerators):
+// the FP64 division's fast path rejects x == 0 (exponent check) and CALLs
+// the slow-path subroutine, and fronts are full of structural zeros. Divides
+// 1 / d instead (the operand is laundered through asm so the compiler cannot
+// fold the select back into the division) and returns +0 (instead of a
+// signed zero). Branch-free.
 __device__ __forceinline__ double divz(double x, double d) {
   const bool z = x == 0.0;
   double xs = z ? 1.0 : x;
@@ -222,7 +226,8 @@ __device__ __forceinline__ void factor_task(const FactorArgs& a, int s, int tid,
         a.D[f + c] = dc;
         if (fabs(dc) <= thresh) atomicMin(a.zp, f + c);
       }
-      for (int i = c + 1 + tid; i < nr; i += NT) Pc[i] = divz(Pc[i], dc);
+      const double rdc = __drcp_rn(dc);  // one reciprocal per pivot; the column scales by multiplies
+      for (int i = c + 1 + tid; i < nr; i += NT) Pc[i] *= rdc;
       team_sync<NT>();
       for (int c2 = c + 1; c2 < c1; ++c2) {
         const double dl = dc * Pc[c2];
@@ -426,7 +431,7 @@ __device__ __forceinline__ void cta_dense(double* F, int nr, int w, int f, doubl
       }
       double l = 0.0;
       if (i > c && i < nr) {
-        l = divz(F[cb_col(c, nr) + i], d);
+        l = F[cb_col(c, nr) + i] * __drcp_rn(d);
         F[cb_col(c, nr) + i] = l;
       }
       const double dl = d * l;
@@ -463,7 +468,7 @@ __device__ __forceinline__ void cta_dense(double* F, int nr, int w, int f, doubl
       for (int k = 0; k < kPb; ++k) {
         if (k < kb) {
           const double d = __shfl_sync(kFull, x[k], k);
-          if (lane > k && lane < kb) x[k] = divz(x[k], d);
+          if (lane > k && lane < kb) x[k] *= __drcp_rn(d);
           const double dlo = d * x[k];  // lane k2: d * L(c0 + k2, c0 + k)
 #pragma unroll
           for (int k2 = 0; k2 < kPb; ++k2) {  // full range: unrolls with k
@@ -832,7 +837,7 @@ __device__ __forceinline__ void small_task(const FactorArgs& a, int s, int lane,
     }
     double l = 0.0;
     if (i > c && i < nr) {
-      l = divz(F[offc + i], d);
+      l = F[offc + i] * __drcp_rn(d);
       F[offc + i] = l;
     }
     const double dl = d * l;
@@ -936,11 +941,11 @@ __device__ __forceinline__ void mid_task(const FactorArgs& a, int s, int lane, d
     }
     double y0 = 0.0, y1 = 0.0;
     if (i0 > c && i0 < nr) {
-      y0 = divz(F[offc + i0], d);
+      y0 = F[offc + i0] * __drcp_rn(d);
       F[offc + i0] = y0;
     }
     if (i1 > c && i1 < nr) {
-      y1 = divz(F[offc + i1], d);
+      y1 = F[offc + i1] * __drcp_rn(d);
       F[offc + i1] = y1;
     }
     const double dl0 = d * y0, dl1 = d * y1;
@@ -1025,7 +1030,7 @@ __device__ __forceinline__ void group_task(const FactorArgs& a, int g, int lane,
       }
       double l = 0.0;
       if (i > c && i < nr) {
-        l = divz(F[offc + i], d);
+        l = F[offc + i] * __drcp_rn(d);
         F[offc + i] = l;
       }
       const double dl = d * l;
@@ -1163,7 +1168,7 @@ __device__ __forceinline__ void reg_front(const FactorArgs& a, const RegInst& I,
     }
 #pragma unroll
     for (int k = 0; k < KR; ++k)
-      if (row(k) > c && row(k) < NR) F[k][c] = divz(F[k][c], d);
+      if (row(k) > c && row(k) < NR) F[k][c] *= __drcp_rn(d);
 #pragma unroll
     for (int c2 = c + 1; c2 < NR; ++c2) {
       const double lc2 = d * bcast(F[c2 / R][c], c2 % R);
@@ -1363,6 +1368,7 @@ struct SolveArgs {
   const int64_t* gpo;
   int nleaf;
   unsigned long long* trace;  // optional (NCL_SOLVE_TRACE): globaltimer start/end per task
+  int pregathered = -1;       // node whose heavy contribution-vector gather ran GPU-wide (fwd_root_gather)
 };
 
 __device__ __forceinline__ void prefetch_l2(const double* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
@@ -1453,7 +1459,8 @@ __device__ void bwd_group(const SolveArgs& a, int g, int lane) {
     const double* P = a.L + loff;
     const bool below = lane >= w && lane < nr;
     const double xi = below ? __ldcg(a.xp + __ldg(S.rows + rb + lane)) : 0.0;
-    const double dl = lane < w ? __ldg(a.D + f + lane) : 1.0;
+    // 1 / d off the column chain (each lane its own pivot, before the chain)
+    const double rl = lane < w ? __drcp_rn(__ldg(a.D + f + lane)) : 1.0;
     const int pl = lane < w ? __ldg(S.perm + f + lane) : 0;
     double T = 0.0;  // lane c < w holds T[c]
     for (int c0 = 0; c0 < w; c0 += 8) {  // eight columns' loads and reductions in flight
@@ -1482,7 +1489,7 @@ __device__ void bwd_group(const SolveArgs& a, int g, int lane) {
         if (c >= 0) {
           double vv = 0.0;
           if (lane == c) {
-            vv = divz(xs, dl) - T;
+            vv = xs * rl - T;
             xs = vv;
             a.xp[f + c] = vv;
             a.x[pl] = vv;
@@ -1550,6 +1557,55 @@ __device__ __forceinline__ void fwd_warp_reg(const double* __restrict__ P, int n
   __syncwarp();
 }
 
+// Rows of a node with many contributing children (the separator roots): a
+// warp per row, lanes over its sources, fixed xor-butterfly combine, then b
+// (deterministic); four rows per warp interleaved so their loads are in
+// flight together. Rows k0, k0 + 4 kstep_rows ... of this warp.
+__device__ __forceinline__ void heavy_cv_rows(const SolveArgs& a, int s, int f, int w, int nr, int64_t v0, int kfirst,
+                                              int kstep, int lane) {
+  const DevSymb& S = a.S;
+  double* cv = a.CV + __ldg(S.sn_rptr + s);
+  double* xs = a.xp + f;
+  for (int k0 = kfirst; k0 < nr; k0 += kstep) {
+    int64_t qa[4], qb[4];
+    double acc[4];
+    int64_t len = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = k0 + u;
+      qa[u] = k < nr ? __ldg(S.cvsp + v0 + k) : 0;
+      qb[u] = k < nr ? __ldg(S.cvsp + v0 + k + 1) : 0;
+      acc[u] = 0.0;
+      len = max(len, qb[u] - qa[u]);
+    }
+    for (int64_t o = lane; o < len; o += 64) {  // two sources per row per lane in flight
+      int64_t src[8];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        src[u] = qa[u] + o < qb[u] ? __ldg(S.cvsrc + qa[u] + o) : -1;
+        src[u + 4] = qa[u] + o + 32 < qb[u] ? __ldg(S.cvsrc + qa[u] + o + 32) : -1;
+      }
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = src[u] >= 0 ? __ldcg(a.CV + src[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (src[u] >= 0) acc[u] += v[u];
+        if (src[u + 4] >= 0) acc[u] += v[u + 4];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      for (int o = 16; o > 0; o >>= 1) acc[u] += __shfl_xor_sync(kFull, acc[u], o);
+      const int k = k0 + u;
+      if (lane == 0 && k < nr) {
+        if (k < w) xs[k] = __ldcg(a.b + __ldg(S.perm + f + k)) + acc[u];
+        else cv[k] = acc[u];
+      }
+    }
+  }
+}
+
 template <int NT>
 __device__ __forceinline__ void fwd_task(const SolveArgs& a, int s, int tid) {
   const DevSymb& S = a.S;
@@ -1577,45 +1633,7 @@ __device__ __forceinline__ void fwd_task(const SolveArgs& a, int s, int tid) {
       // many children (the separator roots): a warp per row, lanes over its
       // sources, fixed xor-butterfly combine, then b (deterministic)
       // (four rows per warp interleaved: their loads are in flight together)
-      const int lane = tid & 31, warp = tid >> 5;
-      for (int k0 = 4 * warp; k0 < nr; k0 += 4 * (NT / 32)) {
-        int64_t qa[4], qb[4];
-        double acc[4];
-        int64_t len = 0;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int k = k0 + u;
-          qa[u] = k < nr ? __ldg(S.cvsp + v0 + k) : 0;
-          qb[u] = k < nr ? __ldg(S.cvsp + v0 + k + 1) : 0;
-          acc[u] = 0.0;
-          len = max(len, qb[u] - qa[u]);
-        }
-        for (int64_t o = lane; o < len; o += 64) {  // two sources per row per lane in flight
-          int64_t src[8];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            src[u] = qa[u] + o < qb[u] ? __ldg(S.cvsrc + qa[u] + o) : -1;
-            src[u + 4] = qa[u] + o + 32 < qb[u] ? __ldg(S.cvsrc + qa[u] + o + 32) : -1;
-          }
-          double v[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) v[u] = src[u] >= 0 ? __ldcg(a.CV + src[u]) : 0.0;
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            if (src[u] >= 0) acc[u] += v[u];
-            if (src[u + 4] >= 0) acc[u] += v[u + 4];
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          for (int o = 16; o > 0; o >>= 1) acc[u] += __shfl_xor_sync(kFull, acc[u], o);
-          const int k = k0 + u;
-          if (lane == 0 && k < nr) {
-            if (k < w) xs[k] = __ldcg(a.b + __ldg(S.perm + f + k)) + acc[u];
-            else cv[k] = acc[u];
-          }
-        }
-      }
+      if (a.pregathered != s) heavy_cv_rows(a, s, f, w, nr, v0, 4 * (tid >> 5), 4 * (NT / 32), tid & 31);
     } else {
       // gather per row: b (pivot rows) then the children's CV entries in
       // child order — the sequential extend-add's summation order
@@ -1718,7 +1736,7 @@ __device__ __forceinline__ void bwd_warp_reg(const SolveArgs& a, const double* _
     xi[q] = i < nr ? __ldcg(a.xp + __ldg(Rs + i)) : 0.0;
     Tq[q] = 0.0;
     xq[q] = c < w ? xs[c] : 0.0;
-    dq[q] = c < w ? __ldg(a.D + f + c) : 1.0;
+    dq[q] = c < w ? __drcp_rn(__ldg(a.D + f + c)) : 1.0;  // 1 / d, off the column chain
     pq[q] = c < w ? __ldg(S.perm + f + c) : 0;
   }
   for (int c0 = 0; c0 < w; c0 += 4) {
@@ -1762,7 +1780,7 @@ __device__ __forceinline__ void bwd_warp_reg(const SolveArgs& a, const double* _
 #pragma unroll
         for (int q = 0; q < kSl; ++q)
           if (c == lane + 32 * q) {
-            v = divz(xq[q], dq[q]) - Tq[q];
+            v = xq[q] * dq[q] - Tq[q];
             xq[q] = v;
             xs[c] = v;
             a.x[pq[q]] = v;
@@ -1807,7 +1825,7 @@ __device__ __forceinline__ void bwd_task(const SolveArgs& a, int s, int tid) {
     team_sync<NT>();
     for (int c = w - 1; c >= 0; --c) {
       if (tid == 0) {
-        const double v = divz(xs[c], __ldg(a.D + f + c)) - T[c];
+        const double v = xs[c] * __drcp_rn(__ldg(a.D + f + c)) - T[c];
         xs[c] = v;
         a.x[__ldg(S.perm + f + c)] = v;
       }
@@ -1836,7 +1854,7 @@ __device__ __forceinline__ void bwd_task(const SolveArgs& a, int s, int tid) {
         const int c2 = c0 + lane;
         const bool in = c2 < c1;
         double Tl = in ? T[c2] : 0.0, xl = in ? xs[c2] : 0.0;
-        const double dl = in ? __ldg(a.D + f + c2) : 1.0;
+        const double rl = in ? __drcp_rn(__ldg(a.D + f + c2)) : 1.0;  // 1 / d, off the column chain
         const int pl = in ? __ldg(S.perm + f + c2) : 0;  // loaded up front: off the column chain
         for (int cb = c1 - 1; cb >= c0; cb -= 8) {
           double pu[8];
@@ -1851,7 +1869,7 @@ __device__ __forceinline__ void bwd_task(const SolveArgs& a, int s, int tid) {
             if (c >= c0) {
               double v = 0.0;
               if (c2 == c) {
-                v = divz(xl, dl) - Tl;
+                v = xl * rl - Tl;
                 xl = v;
                 a.x[pl] = v;
               }
@@ -1904,6 +1922,21 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 8 : 4) fwd_ker
     }
     if (a.trace && tid == 0) a.trace[2 * t + 1] = gtimer();
   }
+}
+
+// GPU-wide forward gather of the last CTA task's contribution vectors (the
+// separator root: one row per warp-quad across many CTAs instead of one
+// CTA), the same per-row arithmetic as heavy_cv_rows inside fwd_task; the
+// root's own task then skips its gather (SolveArgs::pregathered).
+__global__ void __launch_bounds__(256) fwd_root_gather(SolveArgs a, int s) {
+  const DevSymb& S = a.S;
+  for (int q = __ldg(S.cptr + s) + threadIdx.x; q < __ldg(S.cptr + s + 1); q += blockDim.x)
+    wait_flag(a.flags + __ldg(S.child + q), a.epoch);
+  __syncthreads();
+  const int f = __ldg(S.sn_first + s), w = __ldg(S.sn_first + s + 1) - f;
+  const int nr = static_cast<int>(__ldg(S.sn_rptr + s + 1) - __ldg(S.sn_rptr + s));
+  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), nwg = gridDim.x * (blockDim.x >> 5);
+  heavy_cv_rows(a, s, f, w, nr, __ldg(S.cv_ptr + s), 4 * gw, 4 * nwg, threadIdx.x & 31);
 }
 
 // tickets in reverse order (roots first); no leaf chunking
@@ -2032,7 +2065,7 @@ __device__ __forceinline__ void reg_bwd_front(const SolveArgs& a, const RegInst&
   for (int c = 0; c < W; ++c) {
 #pragma unroll
     for (int i = 0; i < NR; ++i) P[c][i] = (i > c) ? __ldg(Pg + c * NR + i) : 0.0;
-    d[c] = __ldg(a.D + I.f + c);
+    d[c] = __drcp_rn(__ldg(a.D + I.f + c));  // 1 / d, before the parent wait
     pl[c] = __ldg(S.perm + I.f + c);
     xs[c] = __ldcg(a.xp + I.f + c);
   }
@@ -2052,7 +2085,7 @@ __device__ __forceinline__ void reg_bwd_front(const SolveArgs& a, const RegInst&
   }
 #pragma unroll
   for (int c = W - 1; c >= 0; --c) {
-    const double vv = divz(xs[c], d[c]) - T[c];
+    const double vv = xs[c] * d[c] - T[c];
     a.xp[I.f + c] = vv;
     a.x[pl[c]] = vv;
 #pragma unroll
@@ -2445,8 +2478,23 @@ void dev_solve_fwd_list(const DevSymb& S, DevFactor& F, const double* b, const D
     fa.ticket = S.tickets + 2 * slot + 1;
     fa.t0 = T.split;
     fa.t1 = T.n;
+    // the last task (the separator root) gathers its many children's CVs
+    // GPU-wide in its own launch, then runs its triangular part
+    const int root = T.root_heavy;
+    if (root >= 0 && T.n - T.split > 1) fa.t1 = T.n - 1;
     COUNT(1);
-    launch_pdl(fwd_kernel<256>, std::min(g_sf2, T.n - T.split), 256, 0, st, fa);  // CTA tasks wait on children
+    launch_pdl(fwd_kernel<256>, std::min(g_sf2, fa.t1 - fa.t0), 256, 0, st, fa);  // CTA tasks wait on children
+    if (root >= 0 && T.n - T.split > 1) {
+      const int nr = T.root_nr;
+      COUNT(2);
+      launch_pdl(fwd_root_gather, std::max(1, std::min(2 * num_sms(), (nr + 31) / 32)), 256, 0, st, fa, root);
+      fa.pregathered = root;
+      fa.ticket = S.tickets + kTickets - 6;
+      cudaMemsetAsync(fa.ticket, 0, sizeof(int), st);
+      fa.t0 = T.n - 1;
+      fa.t1 = T.n;
+      fwd_kernel<256><<<1, 256, 0, st>>>(fa);
+    }
   }
 }
 
