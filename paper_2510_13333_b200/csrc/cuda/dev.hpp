@@ -216,15 +216,20 @@ constexpr int kGrpFront = 32;       // fronts of group nodes: nr <= 32 (packed l
 constexpr int kGrpStack = 512;      // doubles: A values + contribution-block stack
 constexpr int kGrpProg = 1280;      // ints: the group program (read in place: bounds group size only)
 
-constexpr int kTickets = 64;  // ticket counters per symbolic handle
-// [kTicketSeg0, kTickets - 8): per-segment tickets of the unsharded
-// factorization, zeroed once per factorization so consecutive segment
-// launches have no memset between them (programmatic dependent launch,
-// csrc/cuda/ldlt.cu); [kTickets - 8, kTickets - 4): backward register-front
-// solve per slot (zeroed by dev_solve_begin); kTickets - 4 .. - 1: the
-// forward register-front solve, the register factor phases, the sharded
-// segments
+// Ticket counters per symbolic handle:
+//   [0, 40)             2 per task-list slot (warp / CTA phases of factor and solves)
+//   [40, 56)            the unsharded factorization's CTA segments (zeroed once per
+//                       factorization: consecutive segment launches have no memset
+//                       between them — programmatic dependent launch, ldlt.cu)
+//   [56, 60)            backward register-front solve per slot (zeroed by dev_solve_begin)
+//   60                  forward register-front solve
+//   61, 62              register-front factor phases
+//   63                  sharded CTA segments
+//   64                  the forward solve's separator-root task (after its GPU-wide gather)
+constexpr int kTickets = 72;
 constexpr int kTicketSeg0 = 40;
+constexpr int kTicketRegBwd0 = 56, kTicketRegFwd = 60, kTicketRegFac1 = 61, kTicketRegFac2 = 62,
+              kTicketShardSeg = 63, kTicketRoot = 64;
 // panel width of the one-CTA dense front factorization (ldlt.cu cta_dense):
 // the diagonal block is factored by one warp in registers, the trailing
 // update is a rank-NCL_CTA_PANEL DMMA update (kPb / 4 k-steps per tile)

@@ -2351,14 +2351,14 @@ void dev_factor_list(const DevSymb& S, DevFactor& F, const double* kvals, const 
     const int n1 = bs.nchunk1, n2 = static_cast<int>(bs.chunks.size()) - bs.nchunk1;
     FactorArgs ra = a;
     if (n1 > 0) {
-      ra.ticket = S.tickets + kTickets - 2;
+      ra.ticket = S.tickets + kTicketRegFac1;
       cudaMemsetAsync(ra.ticket, 0, sizeof(int), st);
       COUNT(1);
       reg_factor_kernel<0, kRegTier1><<<std::min(grid1, (n1 + 3) / 4), 128, 0, st>>>(
           ra, bs.dev_inst, bs.dev_chunks, n1, bs.dev_amap, bs.dev_cmap, bs.dev_cmapw, bs.dev_ccb, bs.dev_cid);
     }
     if (n2 > 0) {
-      ra.ticket = S.tickets + kTickets - 3;
+      ra.ticket = S.tickets + kTicketRegFac2;
       cudaMemsetAsync(ra.ticket, 0, sizeof(int), st);
       COUNT(1);
       reg_factor_kernel<kRegTier1, kNumRegShapes><<<std::min(grid2, (n2 + 3) / 4), 128, 0, st>>>(
@@ -2387,12 +2387,12 @@ void dev_factor_list(const DevSymb& S, DevFactor& F, const double* kvals, const 
         // unsharded: a pre-zeroed ticket per segment and a programmatic
         // dependent launch (every segment task waits on its children's
         // flags); sharded phases reuse one ticket
-        const bool pdl = slot == 0 && kTicketSeg0 + static_cast<int>(L) < kTickets - 8;
+        const bool pdl = slot == 0 && kTicketSeg0 + static_cast<int>(L) < kTicketRegBwd0;
         if (pdl) {
           a.ticket = S.tickets + kTicketSeg0 + L;
         } else {
-          cudaMemsetAsync(S.tickets + kTickets - 1, 0, sizeof(int), st);
-          a.ticket = S.tickets + kTickets - 1;
+          cudaMemsetAsync(S.tickets + kTicketShardSeg, 0, sizeof(int), st);
+          a.ticket = S.tickets + kTicketShardSeg;
         }
         a.t0 = b;
         a.t1 = e;
@@ -2453,10 +2453,10 @@ static void reg_solve(const DevSymb& S, const BatchSched& bs, SolveArgs a, bool 
   const int n = static_cast<int>(bs.chunks.size());
   if (n == 0) return;
   if (fwd) {
-    a.ticket = S.tickets + kTickets - 4;
+    a.ticket = S.tickets + kTicketRegFwd;
     cudaMemsetAsync(a.ticket, 0, sizeof(int), st);
   } else {  // zeroed by dev_solve_begin: no memset between it and the warp phase (PDL)
-    a.ticket = S.tickets + kTickets - 8 + slot;
+    a.ticket = S.tickets + kTicketRegBwd0 + slot;
   }
   COUNT(1);
   if (fwd)
@@ -2489,7 +2489,7 @@ void dev_solve_fwd_list(const DevSymb& S, DevFactor& F, const double* b, const D
       COUNT(2);
       launch_pdl(fwd_root_gather, std::max(1, std::min(2 * num_sms(), (nr + 31) / 32)), 256, 0, st, fa, root);
       fa.pregathered = root;
-      fa.ticket = S.tickets + kTickets - 6;
+      fa.ticket = S.tickets + kTicketRoot;
       cudaMemsetAsync(fa.ticket, 0, sizeof(int), st);
       fa.t0 = T.n - 1;
       fa.t1 = T.n;

@@ -190,7 +190,7 @@ def test_heavy_gather_fronts_multi_cta_assembly(gpu):
     _heavy_gather_fronts(2000)
 
 
-@pytest.mark.parametrize("grid,K", [("case118", 16), ("activsg500", 16)])
+@pytest.mark.parametrize("grid,K", [("case118", 16), ("activsg500", 16), ("activsg500", 64)])
 def test_scopf_kkt_parity(gpu, grid, K, min_big=0):
     """The condensed SCOPF KKT (subtree groups with mid-size fronts, CTA top,
     separator root) against the reference factorize / solve."""
