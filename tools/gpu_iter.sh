@@ -8,7 +8,7 @@ if [ "${TESTS}" != "none" ]; then
   echo "tests rc=$?"; tail -4 gpurun_out/${T}_tests.log
 fi
 if [ "${BENCH}" != "none" ]; then
-  timeout 900 python bench.py ${BENCH_ARGS:---no-solve --no-cpu-baseline --steps 20 --warmup 5} > gpurun_out/${T}_bench.json 2> gpurun_out/${T}_bench.err
+  timeout ${BENCH_TIMEOUT:-900} python bench.py ${BENCH_ARGS:---no-solve --no-cpu-baseline --steps 20 --warmup 5} > gpurun_out/${T}_bench.json 2> gpurun_out/${T}_bench.err
   echo "bench rc=$?"; python -c "
 import json,sys
 d=json.loads(open('gpurun_out/${T}_bench.json').read().strip().splitlines()[-1])
