@@ -322,13 +322,12 @@ API int ncl_sym_multiply(ncl_sym_t M, const double* x, double* y, int where) {
       check_launch("spmv");
       return NCL_OK;
     }
-    DevBuf<double> dx, dy;
-    dx.alloc(n);
-    dy.alloc(n);
-    ck(cudaMemcpyAsync(dx.p, x, n * sizeof(double), cudaMemcpyHostToDevice, g_stream), "H2D");
-    dev_spmv(M->dp, M->vals.p, dx.p, dy.p, g_stream);
+    M->mvx.alloc(n);  // no-ops after the first call
+    M->mvy.alloc(n);
+    ck(cudaMemcpyAsync(M->mvx.p, x, n * sizeof(double), cudaMemcpyHostToDevice, g_stream), "H2D");
+    dev_spmv(M->dp, M->vals.p, M->mvx.p, M->mvy.p, g_stream);
     check_launch("spmv");
-    ck(cudaMemcpyAsync(y, dy.p, n * sizeof(double), cudaMemcpyDeviceToHost, g_stream), "D2H");
+    ck(cudaMemcpyAsync(y, M->mvy.p, n * sizeof(double), cudaMemcpyDeviceToHost, g_stream), "D2H");
     ck(cudaStreamSynchronize(g_stream), "sync");
   });
 }

@@ -78,6 +78,7 @@ struct ncl_sym {
   nclb::DevBuf<double> trip_vals;
   nclb::DevBuf<double> scratch;
   nclb::DevBuf<double> rowsum;
+  nclb::DevBuf<double> mvx, mvy;  // host-path multiply staging (allocated once)
   nclb::DevPattern dp;
   uint64_t hash = 0;
   bool dev_ready = false;  // pattern + values uploaded (lazy: host-only use needs no GPU)

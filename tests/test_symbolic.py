@@ -105,7 +105,7 @@ def test_matrix_market_matches_reference():
 
 @pytest.mark.parametrize("seed", range(3))
 def test_high_degree_nodes_bit_exact(seed):
-    """Nodes above the ordering's bitmap threshold (degree > 1024), like the
+    """Nodes above the ordering's bitmap threshold (degree > kBig = 256), like the
     SCOPF base-case variables that couple every contingency block."""
     rng = np.random.default_rng(77 + seed)
     n = 2600
