@@ -597,7 +597,8 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
   // phase split: the narrow top of the tree (at most kTopTasks supernodes)
   // runs with a whole CTA per supernode, everything below with a warp each.
   static const char* top_env = std::getenv("NCL_TOP_TASKS");  // tuning experiments only
-  const int kTopTasks = top_env ? std::atoi(top_env) : 8192;
+  // measured (r02, 500x256): 8192 (h >= 11 on the CTA path) 1.69 ms, 6144 (h >= 12) 1.64, 4096 (h >= 13) 1.69, 2048 2.27
+  const int kTopTasks = top_env ? std::atoi(top_env) : 6144;
   Z.nsplit = nsn;
   for (int h = Z.max_height; h >= 0; --h) {
     if (nsn - hc[h] > kTopTasks) break;
