@@ -401,6 +401,10 @@ namespace {
 void build_batches(const Supernodal& Z, const std::vector<int>& list, int split, const std::vector<uint8_t>& inlist,
                    std::vector<uint8_t>& batched, BatchSched& B) {
   const int nsn = Z.nsn;
+  auto i32 = [](int64_t v) {  // RegInst offsets are int32
+    if (v < 0 || v >= (int64_t(1) << 31)) throw Error{NCL_E_INVALID, "analyze: register-front offsets exceed int32"};
+    return static_cast<int>(v);
+  };
   auto wof = [&](int s) { return Z.sn_first[s + 1] - Z.sn_first[s]; };
   auto nrof = [&](int s) { return static_cast<int>(Z.sn_rptr[s + 1] - Z.sn_rptr[s]); };
   auto shape_of = [&](int s) {
@@ -439,6 +443,7 @@ void build_batches(const Supernodal& Z, const std::vector<int>& list, int split,
       const int nr = kRegShapes[k][0], per = 32 / kRegShapes[k][2];
       const int np = nr * (nr + 1) / 2, npad = (np + 3) & ~3;
       const int R = kRegShapes[k][2], nw = npad / 4;
+      const int wk = kRegShapes[k][1], pw = wk * nr - wk * (wk - 1) / 2;  // packed entries of the W pivot columns
       const size_t chunk0 = B.chunks.size();
       for (size_t x = 0; x < v.size(); x += per)
         B.chunks.push_back(RegChunk{k, static_cast<int>(std::min<size_t>(per, v.size() - x)),
@@ -455,7 +460,7 @@ void build_batches(const Supernodal& Z, const std::vector<int>& list, int split,
             maxnch = std::max(maxnch, Z.cptr[v[y] + 1] - Z.cptr[v[y]]);
           if (R == 1) {
             abase = static_cast<int64_t>(B.amap.size());
-            B.amap.resize(B.amap.size() + static_cast<size_t>(np) * 32, -1);
+            B.amap.resize(B.amap.size() + static_cast<size_t>(pw) * 32, -1);
             wbase = static_cast<int64_t>(B.cmapw.size());
             B.cmapw.resize(B.cmapw.size() + static_cast<size_t>(maxnch) * nw * 32, 0xffffffffu);
           }
@@ -464,24 +469,26 @@ void build_batches(const Supernodal& Z, const std::vector<int>& list, int split,
         }
         batched[s] = 1;
         RegInst I{};
-        I.loff = Z.sn_loff[s];
-        I.cboff = Z.cb_off[s];
+        I.loff = i32(Z.sn_loff[s]);
+        I.cboff = i32(Z.cb_off[s]);
         I.s = s;
         I.f = Z.sn_first[s];
         I.nch = Z.cptr[s + 1] - Z.cptr[s];
-        I.shape = k;
         const int64_t ast = R == 1 ? 32 : 1;  // A-map stride
         if (R == 1) {
-          I.amap = abase + ix;
-          I.cmap = wbase + ix;
+          I.amap = i32(abase + ix);
+          I.cmap = i32(wbase + ix);
         } else {
-          I.amap = static_cast<int64_t>(B.amap.size());
-          B.amap.resize(B.amap.size() + np, -1);
-          I.cmap = static_cast<int64_t>(B.cmap.size());
+          I.amap = i32(static_cast<int64_t>(B.amap.size()));
+          B.amap.resize(B.amap.size() + pw, -1);
+          I.cmap = i32(static_cast<int64_t>(B.cmap.size()));
         }
-        for (int64_t e = Z.a_ptr[s]; e < Z.a_ptr[s + 1]; ++e)
-          B.amap[I.amap + ast * (cb_col(Z.a_off[e] / nr, nr) + Z.a_off[e] % nr)] = Z.a_src[e];
-        I.ccb = static_cast<int64_t>(B.ccb.size());
+        for (int64_t e = Z.a_ptr[s]; e < Z.a_ptr[s + 1]; ++e) {
+          const int64_t pp = cb_col(Z.a_off[e] / nr, nr) + Z.a_off[e] % nr;
+          if (pp >= pw) throw Error{NCL_E_INTERNAL, "analyze: A entry outside the pivot columns"};
+          B.amap[I.amap + ast * pp] = Z.a_src[e];
+        }
+        I.ccb = i32(static_cast<int64_t>(B.ccb.size()));
         for (int q = Z.cptr[s]; q < Z.cptr[s + 1]; ++q) {
           const int c = Z.child[q], qi = q - Z.cptr[s];
           const int m2c = nrof(c) - wof(c);
@@ -513,7 +520,7 @@ void build_batches(const Supernodal& Z, const std::vector<int>& list, int split,
           }
           B.ccb.push_back(Z.cb_off[c]);
           B.cid.push_back(c);
-          if (qi < 4) I.cid[qi] = c, I.cb[qi] = Z.cb_off[c];
+          if (qi < 4) I.cid[qi] = c, I.cb[qi] = i32(Z.cb_off[c]);
         }
         B.inst.push_back(I);
         B.nodes++;
@@ -806,6 +813,14 @@ DevTasks upload_layout(TaskLayout& L, LayoutDev& D, const Supernodal& Z) {
 void upload_symb(ncl_symb* S) {
   if (S->dev_ready) return;
   ensure_init();
+  static const bool timing = std::getenv("NCL_ANALYZE_TIMING") != nullptr;
+  auto t = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!timing) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[upload]    %-16s %.3f s\n", what, std::chrono::duration<double>(now - t).count());
+    t = now;
+  };
   const Supernodal& Z = S->Z;
   S->perm.upload(S->core.perm);
   S->sn_first.upload(Z.sn_first);
@@ -826,6 +841,7 @@ void upload_symb(ncl_symb* S) {
   S->cv_ptr.upload(Z.cv_ptr);
   S->cvsp.upload(Z.cvsp);
   S->cvsrc.upload(Z.cvsrc);
+  lap("symbolic arrays");
   if (!S->lay.tptr.empty()) {  // the unbatched layout exists only for NCL_*NO_BATCH A/B runs
     upload_top(S->lay.top, S->top_dev);
     S->lay_nodes.upload(S->lay.nodes);
@@ -848,6 +864,7 @@ void upload_symb(ncl_symb* S) {
     }
     S->aoffp.upload(ap);
   }
+  lap("A maps");
   {
     std::vector<SnMeta> mv(nsn);
     for (int s = 0; s < nsn; ++s) {
@@ -875,6 +892,7 @@ void upload_symb(ncl_symb* S) {
     }
     S->chrec.upload(cr);
   }
+  lap("records");
   S->flags.alloc(3 * std::max(1, nsn));
   ck(cudaMemsetAsync(S->flags.p, 0, 3 * std::max(1, nsn) * sizeof(int), g_stream), "memset");
   S->tickets.alloc(kTickets);
@@ -904,6 +922,7 @@ void upload_symb(ncl_symb* S) {
   d.cvsrc = S->cvsrc.p;
   d.meta = S->meta.p;
   d.ftasks = upload_layout(S->flay, S->fdev, Z);
+  lap("layout");
   d.tasks = S->lay.tptr.empty()
                 ? d.ftasks
                 : DevTasks{S->lay_nodes.p, S->lay_tptr.p, S->lay_prog.p, S->lay_gpo.p,

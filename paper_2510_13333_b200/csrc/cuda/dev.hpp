@@ -57,19 +57,21 @@ struct TopSched {
 // own (release). Per front entry the operations
 // are small_task's in the same order (A value, children ascending, pivot
 // columns in order): the factor is bitwise that of the warp path.
-struct alignas(16) RegInst {
-  int64_t loff, cboff;  // panel, contribution-block offsets
-  int64_t amap;         // offset (ints) of the A map: per packed front entry the K value slot, -1 = none
-  int64_t cmap;         // children's maps: per child, per packed front entry the source position in the
-                        // child's packed CB, 255 = none. R > 1: byte offset in `cmap` (rows padded to 4
-                        // bytes); R == 1: word offset in `cmapw`, words interleaved over the chunk's 32 lanes
-                        // (word w of child q at cmap + (q * words + w) * 32), and the A map interleaved the
-                        // same way (entry p at amap + 32 p): coalesced
-  int64_t ccb;          // offset of the children's CB offsets (int64 each) and supernode ids (int each)
-  int s, f, nch, shape;  // shape = kRegShapes index
-  int cid[4];            // the first four children inline (supernode ids, CB offsets): one round trip less
-  int64_t cb[4];
+struct alignas(16) RegInst {  // 64 bytes: four 16-byte loads per front
+  int loff, cboff;  // panel, contribution-block offsets (doubles; analyze checks both < 2^31)
+  int amap;         // offset (ints) of the A map: per packed entry of the front's first W columns (the
+                    // only ones A reaches) the K value slot, -1 = none
+  int cmap;         // children's maps: per child, per packed front entry the source position in the
+                    // child's packed CB, 255 = none. R > 1: byte offset in `cmap` (rows padded to 4
+                    // bytes); R == 1: word offset in `cmapw`, words interleaved over the chunk's 32 lanes
+                    // (word w of child q at cmap + (q * words + w) * 32), and the A map interleaved the
+                    // same way (entry p at amap + 32 p): coalesced
+  int ccb;          // offset of the children's CB offsets (int64 each) and supernode ids (int each)
+  int s, f, nch;
+  int cid[4];       // the first four children inline (supernode ids, CB offsets): one round trip less
+  int cb[4];
 };
+static_assert(sizeof(RegInst) == 64, "RegInst is four 16-byte loads");
 struct RegChunk {
   int shape, n, first;  // n fronts inst[first .. first + n) of one shape
   int smap;             // word offset of the chunk's forward-solve child records in smapw: for front lane

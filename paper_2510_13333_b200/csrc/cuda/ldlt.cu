@@ -720,15 +720,21 @@ __device__ __forceinline__ void prefetch_prog(const int* PG, int lane) {
 // cb_col in 32-bit arithmetic for the warp fronts (nr <= 32)
 __device__ __forceinline__ int cb32(int j, int m) { return j * m - ((j * (j + 1)) >> 1); }
 
-// Flat walks over a packed lower m x m triangle (column j holds rows j..m-1,
-// contiguous): advance (column j, row i) by `step` positions.
-__device__ __forceinline__ void tri_adv(int& j, int& i, int step, int m) {
-  i += step;
-  while (i >= m && j < m) {
-    const int ex = i - m;
-    ++j;
-    i = j + ex;
-  }
+// Flat position e of a packed lower m x m triangle (column j holds rows
+// j..m-1, contiguous, starting at S(j) = j m - j (j - 1) / 2) -> (column j,
+// row i), closed form: j = floor((b - sqrt(b^2 - 8 e)) / 2), b = 2 m + 1, from
+// a single-precision estimate corrected by one step (exact for m <= 32 and
+// any estimate within a few ulp; checked exhaustively). One decode per
+// element instead of a data-dependent walk over the columns.
+__device__ __forceinline__ void tri_at(int e, int m, int& j, int& i) {
+  const float b = static_cast<float>(2 * m + 1);
+  const float disc = fmaxf(b * b - 8.0f * static_cast<float>(e), 1.0f);
+  int c = static_cast<int>((b - disc * rsqrtf(disc)) * 0.5f);
+  auto S = [m](int k) { return k * m - ((k * (k - 1)) >> 1); };
+  if (c > 0 && S(c) > e) --c;
+  else if (S(c + 1) <= e) ++c;
+  j = c;
+  i = e - S(c) + c;
 }
 // zero a packed front with 16-byte stores (warp regions are 16-byte aligned)
 __device__ __forceinline__ void zero_front(double* F, int np, int lane) {
@@ -740,11 +746,10 @@ __device__ __forceinline__ void zero_front(double* F, int np, int lane) {
 // m2 block flat: ceil(m2 (m2 + 1) / 64) rounds instead of m2
 __device__ __forceinline__ void copy_cb(const double* F, int nr, int w, double* C, int lane) {
   const int m2 = nr - w, ne = m2 * (m2 + 1) / 2;
-  int j = 0, i = lane;
-  tri_adv(j, i, 0, m2);
   for (int e = lane; e < ne; e += 32) {
+    int j, i;
+    tri_at(e, m2, j, i);
     C[e] = F[cb32(w + j, nr) + w + i];
-    tri_adv(j, i, 32, m2);
   }
 }
 // extend-add of a child's packed m2c block (m2c <= 32, relative rows in lane
@@ -752,12 +757,11 @@ __device__ __forceinline__ void copy_cb(const double* F, int nr, int w, double* 
 // one addition per child, so the order over children is unchanged
 __device__ __forceinline__ void extend_add_flat(double* F, int nr, const double* Cc, int m2c, int reli, int lane) {
   const int ne = m2c * (m2c + 1) / 2;
-  int j = 0, i = lane;
-  tri_adv(j, i, 0, m2c);
   for (int e0 = 0; e0 < ne; e0 += 32) {
+    int j, i;
+    tri_at(e0 + lane, m2c, j, i);
     const int rj = __shfl_sync(kFull, reli, min(j, 31)), ri = __shfl_sync(kFull, reli, min(i, 31));
     if (e0 + lane < ne) F[cb32(rj, nr) + ri] += Cc[e0 + lane];
-    tri_adv(j, i, 32, m2c);
   }
 }
 
@@ -1084,6 +1088,7 @@ __device__ __forceinline__ void reg_front(const FactorArgs& a, const RegInst& I,
                                           const uint32_t* __restrict__ cmapw, const int64_t* __restrict__ ccb,
                                           const int* __restrict__ cid, double thresh) {
   constexpr int NP = NR * (NR + 1) / 2, NPAD = (NP + 3) & ~3, M2 = NR - W, KR = (NR + R - 1) / R;
+  constexpr int PW = W * NR - W * (W - 1) / 2;  // packed entries of the W pivot columns (the A map's length)
   auto PK = [](int i, int j) { return j * NR - j * (j + 1) / 2 + i; };  // packed lower, i >= j
   auto row = [r](int k) { return R == 1 ? k : r + R * k; };            // the lane's k-th row
   // broadcast of a team member's register (R == 1: the value itself)
@@ -1098,9 +1103,9 @@ __device__ __forceinline__ void reg_front(const FactorArgs& a, const RegInst& I,
     constexpr int PRE = 0;  // measured: preloading children's maps costs more in registers than it saves
     const int npre = min(I.nch, PRE);
     const uint32_t* cmw = cmapw + I.cmap;
-    int sl[NP];
+    int sl[PW];
 #pragma unroll
-    for (int p = 0; p < NP; ++p) sl[p] = __ldg(am + 32 * p);
+    for (int p = 0; p < PW; ++p) sl[p] = __ldg(am + 32 * p);
     uint32_t mw[PRE > 0 ? PRE : 1][NPAD / 4];
 #pragma unroll
     for (int q = 0; q < PRE; ++q)
@@ -1110,7 +1115,10 @@ __device__ __forceinline__ void reg_front(const FactorArgs& a, const RegInst& I,
 #pragma unroll
     for (int j = 0; j < NR; ++j)
 #pragma unroll
-      for (int i = j; i < NR; ++i) F[i][j] = sl[PK(i, j)] >= 0 ? __ldg(a.kvals + sl[PK(i, j)]) : 0.0;
+      for (int i = j; i < NR; ++i) {
+        const int sv = j < W ? sl[j < W ? PK(i, j) : 0] : -1;
+        F[i][j] = sv >= 0 ? __ldg(a.kvals + sv) : 0.0;
+      }
 #pragma unroll
     for (int q = 0; q < PRE; ++q) {
       if (q >= npre) break;
@@ -1143,7 +1151,7 @@ __device__ __forceinline__ void reg_front(const FactorArgs& a, const RegInst& I,
 #pragma unroll
       for (int j = 0; j < NR; ++j) {
         const int i = row(k);
-        const int slv = (i < NR && j <= i) ? __ldg(am + PK(i, j)) : -1;
+        const int slv = (i < NR && j <= i && j < W) ? __ldg(am + PK(i, j)) : -1;
         F[k][j] = slv >= 0 ? __ldg(a.kvals + slv) : 0.0;
       }
     for (int q = 0; q < I.nch; ++q) {

@@ -5,6 +5,8 @@
 #include "../limits.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
@@ -427,6 +429,14 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
   const int64_t kHeavyGather = heavy_env ? std::atoll(heavy_env) : 400000;
   const int n = S.n;
   Supernodal Z;
+  static const bool timing = std::getenv("NCL_ANALYZE_TIMING") != nullptr && std::getenv("NCL_SN_TIMING") != nullptr;
+  auto tl = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!timing) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[supernodes] %-14s %.3f s\n", what, std::chrono::duration<double>(now - tl).count());
+    tl = now;
+  };
   // 1a. fundamental partition: j+1 joins j's supernode iff parent[j]==j+1 and
   //     colcount[j]==colcount[j+1]+1 (nested structure, identical rows).
   std::vector<int> fund{0};
@@ -497,6 +507,7 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
     for (int s = 0; s < nsn; ++s)
       if (Z.sn_parent[s] >= 0) Z.child[fp[Z.sn_parent[s]]++] = s;
   }
+  lap("partition");
   // 2. lower structure of A (permuted): column j holds rows i>j.
   std::vector<int> lcp(n + 1, 0), lri;
   for (int c = 0; c < n; ++c)
@@ -510,6 +521,7 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
       for (int p = S.up_colptr[c]; p < S.up_colptr[c + 1]; ++p)
         if (S.up_rowind[p] < c) lri[fp[S.up_rowind[p]]++] = c;
   }
+  lap("lower A");
   // 3. row structures R_s = cols(s) ∪ (A rows ∪ children's rows below s),
   //    children before parents.
   Z.sn_rptr.assign(nsn + 1, 0);
@@ -537,6 +549,7 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
     for (int j = f; j < l; ++j) R[s].push_back(j);
     R[s].insert(R[s].end(), buf.begin(), buf.end());
   }
+  lap("row structures");
   // structure check against the reference column counts: exact for
   // fundamental columns, a superset inside amalgamated panels
   for (int s = 0; s < nsn; ++s) {
@@ -564,6 +577,7 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
   }
   Z.l_storage = Z.sn_loff[nsn];
   Z.cb_storage = Z.cb_off[nsn];
+  lap("offsets");
   // 4. relative positions of every child row below the child's columns in
   //    its parent's row list (extend-add maps of the multifrontal scheme)
   Z.relp.assign(Z.rows.size(), -1);
@@ -580,6 +594,7 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
       Z.relp[Z.sn_rptr[c] + k] = static_cast<int>(q);
     }
   }
+  lap("relp");
   // 5. heights and ticket order (leaves first)
   Z.height.assign(nsn, 0);
   for (int s = 0; s < nsn; ++s)
@@ -605,6 +620,7 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
     Z.nsplit = hc[h];
   }
   Z.nleaf = hc[1] - hc[0];
+  lap("heights");
   // 6. A -> panel map, diagonal positions
   const int nnz = cp[n];
   Z.amap.resize(nnz);
@@ -624,6 +640,7 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
       Z.amap[p] = Z.sn_loff[s] + static_cast<int64_t>(lo - f) * nr + pos;
       asn[p] = s;
     }
+  lap("A map");
   // 6b. A entries grouped by target supernode (source slot, offset in panel)
   {
     Z.a_ptr.assign(nsn + 1, 0);
@@ -639,6 +656,7 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
       Z.a_off[q] = static_cast<int>(Z.amap[e] - Z.sn_loff[sn]);
     }
   }
+  lap("A groups");
   // 7. gather maps of the CTA-part fronts (order >= nsplit): for every front entry that receives anything,
   //    its sources in assembly order — the A value (encoded ~slot) first, then
   //    the children's packed CB entries in ascending child order — so the
@@ -719,6 +737,7 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
       Z.gm_ptr[sn + 1] = static_cast<int64_t>(Z.gdst.size());
     }
     Z.gsp.push_back(static_cast<int64_t>(Z.gsrc.size()));
+  lap("gather maps");
     // forward-solve gather map of the same fronts: row r of s sums its
     // children's contribution-vector entries (global CV index) in child order
     Z.cv_ptr.assign(nsn + 1, 0);
@@ -749,6 +768,7 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
     // large-front path: fronts beyond the 200 KB shared-memory cap, and fronts
     // whose assembly gathers too many child entries for one CTA (e.g. the
     // separator root under every contingency subtree)
+    lap("cv maps");
     Z.big.assign(nsn, 0);
     for (int sn = 0; sn < nsn; ++sn) {
       if (!want[sn]) continue;
