@@ -400,7 +400,7 @@ __device__ __forceinline__ void gather4(const DevSymb& S, const double* __restri
 }
 
 #ifdef NCL_DENSE_PROF  // tools/front_bench.cu: per-phase clocks of cta_dense (thread 0)
-__device__ long long g_dense_prof[5];
+__device__ long long g_dense_prof[8];
 #define DPROF_T0 long long dp_t = clock64();
 #define DPROF(k)                                  \
   if (tid == 0) {                                 \
@@ -453,6 +453,16 @@ __device__ __forceinline__ void cta_dense(double* F, int nr, int w, int f, doubl
     //      trailing lower triangle on the FP64 tensor cores (mma.m8n8k4.f64,
     //      8 x 8 tiles, two k-steps), tiles dealt round-robin to the warps.
     constexpr int kPb = NCL_CTA_PANEL;  // panel width (csrc/cuda/dev.hpp)
+#ifdef NCL_DIAG_SHARE
+    constexpr bool kDiagShare = true;
+#else
+    constexpr bool kDiagShare = false;
+#endif
+#ifdef NCL_NO_LOOKAHEAD
+    constexpr bool kLookAhead = false;
+#else
+    constexpr bool kLookAhead = true;
+#endif
     constexpr int nw = NT / 32;
     __shared__ double s_rd[kPb], s_dl[kPb][kPb];  // 1 / d_k and d_k L(k2, k) of the current diagonal block
     const int lane = tid & 31, warp = tid >> 5;
@@ -464,11 +474,14 @@ __device__ __forceinline__ void cta_dense(double* F, int nr, int w, int f, doubl
       const int i = c0 + lane;
 #pragma unroll
       for (int k = 0; k < kPb; ++k) x[k] = (k < kb && k <= lane && lane < kb) ? F[cb_col(c0 + k, nr) + i] : 0.0;
+      double rk[kPb];  // 1 / d_k, formed by every lane (warp-uniform; no divergent region)
 #pragma unroll
       for (int k = 0; k < kPb; ++k) {
+        rk[k] = 0.0;
         if (k < kb) {
           const double d = __shfl_sync(kFull, x[k], k);
-          if (lane > k && lane < kb) x[k] *= __drcp_rn(d);
+          rk[k] = __drcp_rn(d);
+          if (lane > k && lane < kb) x[k] *= rk[k];
           const double dlo = d * x[k];  // lane k2: d * L(c0 + k2, c0 + k)
 #pragma unroll
           for (int k2 = 0; k2 < kPb; ++k2) {  // full range: unrolls with k
@@ -489,7 +502,7 @@ __device__ __forceinline__ void cta_dense(double* F, int nr, int w, int f, doubl
       for (int k = 0; k < kPb; ++k) {
         if (k < kb) {
           const double dk = __shfl_sync(kFull, x[k], k);
-          if (lane == k) s_rd[k] = __drcp_rn(dk);  // correctly rounded: = 1.0 / dk, half the latency
+          if (lane == k) s_rd[k] = rk[k];  // correctly rounded: = 1.0 / dk, half the latency
           if (lane > k && lane < kb) s_dl[k][lane] = dk * x[k];
         }
       }
@@ -534,7 +547,13 @@ __device__ __forceinline__ void cta_dense(double* F, int nr, int w, int f, doubl
       // the next panel (tile column 0) first, then — look-ahead — warp 0
       // factors the next diagonal block while the other warps finish the rest
       const int c1 = c0 + kb, m = nr - c1;
-      const bool ahead = c1 < w;
+      // look-ahead: warp 0 factors the next diagonal block during the
+      // trailing update. A DMMA-issuing neighbour stretches the block's
+      // dependent FP64 chain ~2.8x (tools/diag_bench.cu: 1.9 k -> 5.3 k
+      // cycles; a DMMA holds the sub-partition's FP64 pipe ~16 cycles), yet
+      // the overlap still wins: NCL_NO_LOOKAHEAD (block alone after the
+      // update) measured 1.652 vs 1.617 ms per step
+      const bool ahead = kLookAhead && c1 < w;
       if (m > 0) {
         const int T = (m + 7) >> 3;
         // this lane's k indices (A column / B row of every m8n8k4 k-step):
@@ -579,16 +598,34 @@ __device__ __forceinline__ void cta_dense(double* F, int nr, int w, int f, doubl
           }
         };
         if (ahead) {
+#ifdef NCL_DENSE_PROF
+          const long long sb0 = clock64();
+#endif
           for (int ti = warp; ti < T; ti += nw) tile_row(ti, 0, 0);  // the next panel's columns
           __syncthreads();
+#ifdef NCL_DENSE_PROF
+          if (tid == 0) g_dense_prof[6] += clock64() - sb0;
+#endif
         }
         const int tj_lo = ahead ? 1 : 0;
         if (ahead && warp == 0) {
+#ifdef NCL_DENSE_PROF
+          const long long db0 = clock64();
+#endif
           diag_block(c1);
+#ifdef NCL_DENSE_PROF
+          if (tid == 0) g_dense_prof[5] += clock64() - db0;
+#endif
         } else {
-          // remaining tile rows dealt in snake order to the working warps
-          const int nwk = ahead ? nw - 1 : nw, wk = ahead ? warp - 1 : warp;
-          for (int r = 0; r * nwk < T; ++r) {
+          // remaining tile rows dealt in snake order to the working warps.
+          // With look-ahead, the warps sharing warp 0's scheduler (warp % 4
+          // == 0) stay idle: the diagonal block's dependent FP64 chain would
+          // otherwise queue behind their DMMAs in the SM sub-partition's FP64
+          // pipe (NCL_DIAG_SHARE=1: A/B, they work too)
+          const bool iso = ahead && !kDiagShare;
+          const int nwk = !ahead ? nw : iso ? nw - nw / 4 : nw - 1;
+          const int wk = !ahead ? warp : iso ? warp - 1 - warp / 4 : warp - 1;
+          for (int r = 0; !(iso && (warp & 3) == 0) && r * nwk < T; ++r) {
             const int ti = (r & 1) ? r * nwk + nwk - 1 - wk : r * nwk + wk;
             if (ti >= T || ti < tj_lo) continue;
             tile_row(ti, tj_lo, ti);
@@ -598,6 +635,10 @@ __device__ __forceinline__ void cta_dense(double* F, int nr, int w, int f, doubl
         diag_block(c1);
       }
       __syncthreads();
+      if (!kLookAhead && c1 < w) {
+        if (warp == 0) diag_block(c1);
+        __syncthreads();
+      }
       DPROF(3)
     }
   }
@@ -1285,16 +1326,17 @@ __global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 6 : NT == 128 
 // Heavy-gather front that fits the CTA path: bf_gather assembled it (many
 // children, multi-CTA) into its full-layout scratch; one CTA factors it here
 // with the same arithmetic as the CTA smem path.
-__global__ void __launch_bounds__(256) big_cta_kernel(DevSymb S, const BigDesc* d, const double* Fs, double* L,
-                                                      double* CB, double* D, const double* thresh_p, int* zp) {
+template <int NT>
+__global__ void __launch_bounds__(NT) big_cta_kernel(DevSymb S, const BigDesc* d, const double* Fs, double* L,
+                                                     double* CB, double* D, const double* thresh_p, int* zp) {
   extern __shared__ double s_front[];
   const BigDesc b = d[blockIdx.x];
   if (b.npan != 0) return;
   const int nr = b.nr, tid = threadIdx.x;
   const double* G = Fs + b.foff;  // assembled in the packed layout (gdst, nr <= kCtaFront)
-  for (int k = tid; k < nr * (nr + 1) / 2; k += 256) s_front[k] = __ldcg(G + k);
+  for (int k = tid; k < nr * (nr + 1) / 2; k += NT) s_front[k] = __ldcg(G + k);
   __syncthreads();
-  cta_dense<256>(s_front, nr, b.w, b.f, __ldcg(thresh_p), D, zp, L + __ldg(S.sn_loff + b.s), CB + __ldg(S.cb_off + b.s),
+  cta_dense<NT>(s_front, nr, b.w, b.f, __ldcg(thresh_p), D, zp, L + __ldg(S.sn_loff + b.s), CB + __ldg(S.cb_off + b.s),
                  tid);
 }
 
@@ -2292,12 +2334,19 @@ static void init_grids() {
 }
 
 void dev_big_cta(const DevSymb& S, DevFactor& F, const BigDesc* d, int nf, cudaStream_t st) {
-  static int set = 0;
+  static int set = 0, nt = 256;
   if (!set) {
-    cudaFuncSetAttribute(big_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFacSmem2);
+    // NCL_ROOT_NT=512|1024 (A/B): threads of the one-CTA heavy fronts (the root)
+    const char* e = std::getenv("NCL_ROOT_NT");
+    nt = e ? std::atoi(e) : 256;
+    cudaFuncSetAttribute(big_cta_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFacSmem2);
+    cudaFuncSetAttribute(big_cta_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFacSmem2);
+    cudaFuncSetAttribute(big_cta_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFacSmem2);
     set = 1;
   }
-  big_cta_kernel<<<nf, 256, kFacSmem2, st>>>(S, d, F.bigF, F.L, F.CB, F.D, F.scal, F.istat);
+  if (nt == 1024) big_cta_kernel<1024><<<nf, 1024, kFacSmem2, st>>>(S, d, F.bigF, F.L, F.CB, F.D, F.scal, F.istat);
+  else if (nt == 512) big_cta_kernel<512><<<nf, 512, kFacSmem2, st>>>(S, d, F.bigF, F.L, F.CB, F.D, F.scal, F.istat);
+  else big_cta_kernel<256><<<nf, 256, kFacSmem2, st>>>(S, d, F.bigF, F.L, F.CB, F.D, F.scal, F.istat);
   COUNT(1);
 }
 

@@ -14,26 +14,30 @@
 
 using namespace nclb;
 
-__global__ void __launch_bounds__(256) front_kernel(const double* G, int nr, int w, double* L, double* CB, double* D,
+template <int NT>
+__global__ void __launch_bounds__(NT) front_kernel(const double* G, int nr, int w, double* L, double* CB, double* D,
                                                     int* zp, int reps, long long* cyc) {
   extern __shared__ double s_front[];
   const int tid = threadIdx.x;
   long long t0 = 0, tot = 0;
   for (int r = 0; r < reps; ++r) {
-    for (int c = tid >> 5; c < nr; c += 8)
+    for (int c = tid >> 5; c < nr; c += NT / 32)
       for (int i = c + (tid & 31); i < nr; i += 32) s_front[cb_col(c, nr) + i] = G[static_cast<int64_t>(c) * nr + i];
     __syncthreads();
     t0 = clock64();
-    cta_dense<256>(s_front, nr, w, 0, 0.0, D, zp, L, CB, tid);
+    cta_dense<NT>(s_front, nr, w, 0, 0.0, D, zp, L, CB, tid);
     __syncthreads();
     tot += clock64() - t0;
   }
   if (tid == 0) cyc[blockIdx.x] = tot / reps;
 }
 
-int main() {
+template <int NT>
+void run(bool root_only) {
+  std::printf("threads %d\n", NT);
   const int cases[][2] = {{27, 4}, {48, 6}, {84, 10}, {133, 22}, {155, 155}, {160, 64}};
   for (auto& cs : cases) {
+    if (root_only && cs[0] != 155) continue;
     const int nr = cs[0], w = cs[1];
     std::vector<double> h(static_cast<size_t>(nr) * nr, 0.0);
     std::mt19937_64 rng(nr);
@@ -51,16 +55,16 @@ int main() {
     cudaMalloc(&cyc, 148 * 8);
     cudaMemcpy(G, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
     const int smem = 160 * 161 / 2 * 8;
-    cudaFuncSetAttribute(front_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    front_kernel<<<1, 256, smem>>>(G, nr, w, L, CB, D, zp, 3, cyc);
+    cudaFuncSetAttribute(front_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    front_kernel<NT><<<1, NT, smem>>>(G, nr, w, L, CB, D, zp, 3, cyc);
     cudaDeviceSynchronize();
-    long long z[5] = {0, 0, 0, 0, 0};
+    long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     cudaMemcpyToSymbol(g_dense_prof, z, sizeof(z));
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    front_kernel<<<1, 256, smem>>>(G, nr, w, L, CB, D, zp, 20, cyc);
+    front_kernel<NT><<<1, NT, smem>>>(G, nr, w, L, CB, D, zp, 20, cyc);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms = 0;
@@ -68,8 +72,8 @@ int main() {
     long long c = 0;
     cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
     cudaMemcpyFromSymbol(z, g_dense_prof, sizeof(z));
-    std::printf("   per rep: diag block %lld  barrier %lld  rows %lld  trailing %lld  writeout %lld cycles\n", z[0] / 20,
-                z[1] / 20, z[2] / 20, z[3] / 20, z[4] / 20);
+    std::printf("   per rep: diag block %lld  barrier %lld  rows %lld  trailing %lld (look-ahead diag %lld, strip %lld)  writeout %lld cycles\n", z[0] / 20,
+                z[1] / 20, z[2] / 20, z[3] / 20, z[5] / 20, z[6] / 20, z[4] / 20);
     std::printf("nr=%3d w=%3d  cta_dense %8lld cycles (%.2f us at 1.965 GHz)  kernel %.1f us/rep  err=%s\n", nr, w, c,
                 c / 1965.0, ms * 1000 / 20, cudaGetErrorString(cudaGetLastError()));
     cudaFree(G);
@@ -79,5 +83,12 @@ int main() {
     cudaFree(zp);
     cudaFree(cyc);
   }
+}
+
+int main(int argc, char** argv) {
+  // "root": the 155 x 155 root front only, 256 threads (ncu source capture)
+  const bool root_only = argc > 1;
+  run<256>(root_only);
+  if (!root_only) run<512>(false);
   return 0;
 }
