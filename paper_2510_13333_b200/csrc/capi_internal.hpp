@@ -64,6 +64,11 @@ struct DevBuf {
 }  // namespace nclb
 
 #include "../../include/nclopf_b200.h"
+namespace nclb {
+// the condensed-KKT matrix's device maps (capi_kkt.cpp), built ahead of its
+// first assembly: NCL_OK or an error code (message in this thread's g_err)
+int kkt_prepare_device(ncl_kkt_t K);
+}  // namespace nclb
 #include "cuda/dev.hpp"
 #include "host/sparse.hpp"
 

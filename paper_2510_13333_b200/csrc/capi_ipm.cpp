@@ -15,6 +15,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../include/nclopf_ipm.h"
@@ -125,8 +126,27 @@ class GpuBackend final : public ipm::Backend {
     *f = hsc_[0];
     *gmax = hsc_[2];
     // one-time symbolic analysis of the fixed K pattern (exact MD, etree,
-    // supernodes) — values are irrelevant to it
-    chk(ncl_analyze(K_, nullptr, &S_));
+    // supernodes) — values are irrelevant to it. The KKT assembly's device
+    // maps (host-built, then uploaded) are independent of it: a second host
+    // thread prepares them meanwhile (same device; its error, if any, is
+    // reported after the analysis)
+    int dev = 0;
+    ck(cudaGetDevice(&dev), "cudaGetDevice");
+    int prc = NCL_OK;
+    std::string perr;
+    std::thread prep([&] {
+      if (cudaSetDevice(dev) != cudaSuccess) {
+        prc = NCL_E_CUDA;
+        perr = "kkt: cudaSetDevice failed in the preparation thread";
+        return;
+      }
+      prc = kkt_prepare_device(kkt_);
+      if (prc != NCL_OK) perr = g_err;
+    });
+    const int arc = ncl_analyze(K_, nullptr, &S_);
+    prep.join();
+    chk(arc);
+    if (prc != NCL_OK) throw Error{prc, perr};
   }
   void eval_derivatives(double sf) override {
     chk(ncl_model_eval_all_device(M_, V_.x, sf, V_.y, nullptr, V_.grad, nullptr, jac_, hess_));

@@ -101,6 +101,17 @@ void assemble(ncl_kkt* K, const double* hess, const double* jac, const double* s
 }
 }  // namespace
 
+namespace nclb {
+int kkt_prepare_device(ncl_kkt* K) {
+  try {
+    kkt_upload(K);
+  } catch (...) {
+    return map_exc();
+  }
+  return NCL_OK;
+}
+}  // namespace nclb
+
 API int ncl_kkt_create(int n, int m, int64_t nnzh, const int* hr, const int* hcl, int64_t nnzj, const int* jr,
                        const int* jcl, ncl_kkt_t* out) {
   GUARD({

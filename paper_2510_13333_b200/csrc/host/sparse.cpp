@@ -10,6 +10,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <atomic>
+#include <thread>
 #include <queue>
 
 #include "../../../include/nclopf_expr_program.h"
@@ -17,6 +19,46 @@
 namespace nclb {
 
 static inline void fail(int code, const char* msg) { throw Error{code, msg}; }
+
+// Host threads for the independent per-column / per-front passes of the
+// analysis (outputs are position-addressed, so the result does not depend on
+// the thread count). NCL_HOST_THREADS overrides (1 = sequential).
+static int host_threads() {
+  static const int n = [] {
+    const char* e = std::getenv("NCL_HOST_THREADS");
+    const int hw = static_cast<int>(std::thread::hardware_concurrency());
+    return std::max(1, e ? std::atoi(e) : std::min(8, hw > 0 ? hw : 1));
+  }();
+  return n;
+}
+// fn(t, begin, end) over [0, n) split into contiguous per-thread ranges
+template <class F>
+static void parallel_ranges(int64_t n, int64_t min_per_thread, F fn) {
+  const int nt = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(host_threads(), n / std::max<int64_t>(1, min_per_thread))));
+  if (nt <= 1) {
+    fn(0, int64_t(0), n);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t) th.emplace_back([&, t] { fn(t, n * t / nt, n * (t + 1) / nt); });
+  for (auto& x : th) x.join();
+}
+// fn(i) for the items of `order`, claimed dynamically (costly items first)
+template <class F>
+static void parallel_items(const std::vector<int>& order, F fn) {
+  const int nt = std::min<int>(host_threads(), static_cast<int>(order.size()));
+  if (nt <= 1) {
+    for (int i : order) fn(i);
+    return;
+  }
+  std::atomic<size_t> next{0};
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t)
+    th.emplace_back([&] {
+      for (size_t k; (k = next.fetch_add(1)) < order.size();) fn(order[k]);
+    });
+  for (auto& x : th) x.join();
+}
 
 // --- SparseSym::add (sparse_sym.cpp:12-26) ---------------------------------
 void SymPattern::add(int row, int col, double value) {
@@ -626,20 +668,26 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
   Z.amap.resize(nnz);
   std::vector<int> asn(nnz);  // target supernode of every A entry
   Z.diag_pos.clear();
-  for (int c = 0; c < n; ++c)
-    for (int p = cp[c]; p < cp[c + 1]; ++p) {
-      const int r = ri[p];
-      if (r == c) Z.diag_pos.push_back(p);
-      const int pi = S.iperm[r], pj = S.iperm[c];
-      const int lo = std::min(pi, pj), hi = std::max(pi, pj);
-      const int s = Z.sn_of_col[lo];
-      const int f = Z.sn_first[s];
-      const int* rb = Z.rows.data() + Z.sn_rptr[s];
-      const int nr = static_cast<int>(Z.sn_rptr[s + 1] - Z.sn_rptr[s]);
-      const int pos = static_cast<int>(std::lower_bound(rb, rb + nr, hi) - rb);
-      Z.amap[p] = Z.sn_loff[s] + static_cast<int64_t>(lo - f) * nr + pos;
-      asn[p] = s;
-    }
+  {
+    std::vector<std::vector<int>> dpos(host_threads());
+    parallel_ranges(n, 4096, [&](int t, int64_t c0, int64_t c1) {
+      for (int c = static_cast<int>(c0); c < c1; ++c)
+        for (int p = cp[c]; p < cp[c + 1]; ++p) {
+          const int r = ri[p];
+          if (r == c) dpos[t].push_back(p);
+          const int pi = S.iperm[r], pj = S.iperm[c];
+          const int lo = std::min(pi, pj), hi = std::max(pi, pj);
+          const int s = Z.sn_of_col[lo];
+          const int f = Z.sn_first[s];
+          const int* rb = Z.rows.data() + Z.sn_rptr[s];
+          const int nr = static_cast<int>(Z.sn_rptr[s + 1] - Z.sn_rptr[s]);
+          const int pos = static_cast<int>(std::lower_bound(rb, rb + nr, hi) - rb);
+          Z.amap[p] = Z.sn_loff[s] + static_cast<int64_t>(lo - f) * nr + pos;
+          asn[p] = s;
+        }
+    });
+    for (auto& v : dpos) Z.diag_pos.insert(Z.diag_pos.end(), v.begin(), v.end());  // column order
+  }
   lap("A map");
   // 6b. A entries grouped by target supernode (source slot, offset in panel)
   {
@@ -664,32 +712,41 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
   //    barriers; same summation order as the scatter/extend-add path).
   {
     Z.gm_ptr.assign(nsn + 1, 0);
-    std::vector<std::vector<int64_t>> asrc_of(nsn);
-    std::vector<std::vector<int>> adst_of(nsn);
     std::vector<uint8_t> want(nsn, 0);
     for (int t = Z.nsplit; t < nsn; ++t) {
       const int sn = Z.order[t];
       want[sn] = 1;
     }
-    for (int sn = 0; sn < nsn; ++sn)
-      if (want[sn])
-        for (int64_t q = Z.a_ptr[sn]; q < Z.a_ptr[sn + 1]; ++q) {
-          adst_of[sn].push_back(Z.a_off[q]);
-          asrc_of[sn].push_back(Z.a_src[q]);
-        }
     // counting sort by destination over the packed lower front (the only
-    // entries that receive anything), buffers reused across fronts
-    std::vector<int64_t> cnt, fill;
-    for (int sn = 0; sn < nsn; ++sn) {
-      if (!want[sn]) {
-        Z.gm_ptr[sn + 1] = Z.gm_ptr[sn];
-        continue;
+    // entries that receive anything); two passes over the fronts (sizes,
+    // then the fill at prefix-summed offsets), each front independent, so
+    // both run on host threads with the sequential result
+    std::vector<int> wl;
+    for (int sn = 0; sn < nsn; ++sn)
+      if (want[sn]) wl.push_back(sn);
+    std::vector<int64_t> cost(nsn, 0);
+    for (int sn : wl) {
+      int64_t c = Z.a_ptr[sn + 1] - Z.a_ptr[sn];
+      for (int q = Z.cptr[sn]; q < Z.cptr[sn + 1]; ++q) {
+        const int ch = Z.child[q];
+        const int64_t m2c = (Z.sn_rptr[ch + 1] - Z.sn_rptr[ch]) - (Z.sn_first[ch + 1] - Z.sn_first[ch]);
+        c += m2c * (m2c + 1) / 2;
       }
+      const int64_t nr = Z.sn_rptr[sn + 1] - Z.sn_rptr[sn];
+      cost[sn] = c + nr * (nr + 1) / 2;
+    }
+    std::vector<int> byc = wl;
+    std::stable_sort(byc.begin(), byc.end(), [&](int x, int y) { return cost[x] > cost[y]; });
+    // per front: the count of sources landing on every packed entry
+    auto count = [&](int sn, std::vector<int64_t>& cnt) {
       const int nr = static_cast<int>(Z.sn_rptr[sn + 1] - Z.sn_rptr[sn]);
       const size_t np = static_cast<size_t>(nr) * (nr + 1) / 2;
       auto pk = [nr](int rj, int ri) { return static_cast<size_t>(rj) * nr - static_cast<size_t>(rj) * (rj + 1) / 2 + ri; };
       cnt.assign(np + 1, 0);
-      for (int d : adst_of[sn]) cnt[pk(d / nr, d % nr) + 1]++;
+      for (int64_t q = Z.a_ptr[sn]; q < Z.a_ptr[sn + 1]; ++q) {
+        const int d = Z.a_off[q];
+        cnt[pk(d / nr, d % nr) + 1]++;
+      }
       for (int q = Z.cptr[sn]; q < Z.cptr[sn + 1]; ++q) {
         const int c = Z.child[q];
         const int wc = Z.sn_first[c + 1] - Z.sn_first[c];
@@ -698,18 +755,43 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
         for (int j = 0; j < m2c; ++j)
           for (int i = j; i < m2c; ++i) cnt[pk(rel[j], rel[i]) + 1]++;
       }
+    };
+    std::vector<int64_t> nsrc(nsn, 0), ndst(nsn, 0);
+    parallel_items(byc, [&](int sn) {
+      thread_local std::vector<int64_t> cnt;
+      count(sn, cnt);
+      int64_t a = 0, b = 0;
+      for (size_t d = 1; d < cnt.size(); ++d) a += cnt[d], b += cnt[d] != 0;
+      nsrc[sn] = a;
+      ndst[sn] = b;
+    });
+    std::vector<int64_t> sbase(nsn, 0);
+    int64_t ts = 0;
+    for (int sn = 0; sn < nsn; ++sn) {
+      sbase[sn] = ts;
+      ts += nsrc[sn];
+      Z.gm_ptr[sn + 1] = Z.gm_ptr[sn] + ndst[sn];
+    }
+    Z.gsrc.assign(ts, 0);
+    Z.gdst.assign(Z.gm_ptr[nsn], 0);
+    Z.gsp.assign(Z.gm_ptr[nsn] + 1, 0);
+    parallel_items(byc, [&](int sn) {
+      thread_local std::vector<int64_t> cnt, fill;
+      count(sn, cnt);
+      const int nr = static_cast<int>(Z.sn_rptr[sn + 1] - Z.sn_rptr[sn]);
+      const size_t np = static_cast<size_t>(nr) * (nr + 1) / 2;
+      auto pk = [nr](int rj, int ri) { return static_cast<size_t>(rj) * nr - static_cast<size_t>(rj) * (rj + 1) / 2 + ri; };
       // CSR over the entries that receive something, in front (column-major) order
-      const int64_t base = static_cast<int64_t>(Z.gsrc.size());
+      const int64_t base = sbase[sn];
       fill.resize(np);
       int64_t run = 0;
       for (size_t d = 0; d < np; ++d) {
         fill[d] = run;
         run += cnt[d + 1];
       }
-      Z.gsrc.resize(base + run);
-      for (size_t k = 0; k < adst_of[sn].size(); ++k) {
-        const int d = adst_of[sn][k];
-        Z.gsrc[base + fill[pk(d / nr, d % nr)]++] = ~asrc_of[sn][k];
+      for (int64_t q = Z.a_ptr[sn]; q < Z.a_ptr[sn + 1]; ++q) {
+        const int d = Z.a_off[q];
+        Z.gsrc[base + fill[pk(d / nr, d % nr)]++] = ~static_cast<int64_t>(Z.a_src[q]);
       }
       for (int q = Z.cptr[sn]; q < Z.cptr[sn + 1]; ++q) {
         const int c = Z.child[q];
@@ -724,19 +806,18 @@ Supernodal build_supernodes(const SymbolicCore& S, const std::vector<int>& cp,
       // destination: packed lower offset for fronts that fit the CTA path
       // (shared-memory and one-CTA large fronts), full column-major
       // rj * nr + ri for the wider ones (blocked DMMA path)
-      int64_t at = base;
+      int64_t at = base, e = Z.gm_ptr[sn];
       for (int rj = 0; rj < nr; ++rj)
         for (int ri = rj; ri < nr; ++ri) {
           const size_t d = pk(rj, ri);
           if (cnt[d + 1]) {
-            Z.gdst.push_back(nr <= kSmemFront ? static_cast<int>(d) : rj * nr + ri);
-            Z.gsp.push_back(at);
+            Z.gdst[e] = nr <= kSmemFront ? static_cast<int>(d) : rj * nr + ri;
+            Z.gsp[e++] = at;
             at += cnt[d + 1];
           }
         }
-      Z.gm_ptr[sn + 1] = static_cast<int64_t>(Z.gdst.size());
-    }
-    Z.gsp.push_back(static_cast<int64_t>(Z.gsrc.size()));
+    });
+    Z.gsp[Z.gm_ptr[nsn]] = static_cast<int64_t>(Z.gsrc.size());
   lap("gather maps");
     // forward-solve gather map of the same fronts: row r of s sums its
     // children's contribution-vector entries (global CV index) in child order
