@@ -818,7 +818,9 @@ void upload_symb(ncl_symb* S) {
   auto lap = [&](const char* what) {
     if (!timing) return;
     const auto now = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[upload]    %-16s %.3f s\n", what, std::chrono::duration<double>(now - t).count());
+    std::fprintf(stderr, "[upload]    %-16s %.3f s  (so far: cudaMalloc %.3f s, copies %.3f s, %.1f MB)\n", what,
+                 std::chrono::duration<double>(now - t).count(), g_upload_stats[0] * 1e-9, g_upload_stats[1] * 1e-9,
+                 g_upload_stats[2] * 1e-6);
     t = now;
   };
   const Supernodal& Z = S->Z;
@@ -944,6 +946,17 @@ void upload_symb(ncl_symb* S) {
   S->dev_ready = true;
 }
 }  // namespace
+
+namespace nclb {
+int symb_prepare_device(ncl_symb_t S) {
+  try {
+    upload_symb(S);
+  } catch (...) {
+    return map_exc();
+  }
+  return NCL_OK;
+}
+}  // namespace nclb
 
 API int ncl_symbolic_order(ncl_sym_t M, int* perm) {
   GUARD({

@@ -3,6 +3,9 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
+#include <chrono>
+
 #include <cmath>
 #include <cstdint>
 #include <limits>
@@ -22,6 +25,10 @@ void ensure_init();
 void check_launch(const char* what);
 int set_err(int code, const std::string& msg);
 int map_exc();
+
+// upload accounting (printed under NCL_ANALYZE_TIMING): nanoseconds in
+// cudaMalloc, nanoseconds in the copies, bytes copied (any thread)
+inline std::atomic<int64_t> g_upload_stats[3] = {0, 0, 0};
 
 // Owning device buffer (cudaMalloc/cudaFree), sized in elements.
 template <class T>
@@ -49,10 +56,15 @@ struct DevBuf {
     n = std::max<int64_t>(count, 1);
   }
   void upload(const std::vector<T>& v) {
+    const auto t0 = std::chrono::steady_clock::now();
     alloc(static_cast<int64_t>(v.size()));
+    const auto t1 = std::chrono::steady_clock::now();
     if (!v.empty())
       ck(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, g_stream), "upload");
     ck(cudaStreamSynchronize(g_stream), "upload sync");
+    g_upload_stats[0] += std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
+    g_upload_stats[1] += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t1).count();
+    g_upload_stats[2] += static_cast<int64_t>(v.size() * sizeof(T));
   }
   void download(std::vector<T>& v, int64_t count) const {
     v.resize(count);
@@ -68,6 +80,9 @@ namespace nclb {
 // the condensed-KKT matrix's device maps (capi_kkt.cpp), built ahead of its
 // first assembly: NCL_OK or an error code (message in this thread's g_err)
 int kkt_prepare_device(ncl_kkt_t K);
+// the symbolic factor's device copy (capi.cpp upload_symb), otherwise made by
+// the first factorization: NCL_OK or an error code
+int symb_prepare_device(ncl_symb_t S);
 }  // namespace nclb
 #include "cuda/dev.hpp"
 #include "host/sparse.hpp"

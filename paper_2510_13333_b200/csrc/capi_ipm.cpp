@@ -147,6 +147,9 @@ class GpuBackend final : public ipm::Backend {
     prep.join();
     chk(arc);
     if (prc != NCL_OK) throw Error{prc, perr};
+    // the symbolic factor's device copy is setup too (t_init), not the first
+    // factorization's cost
+    chk(symb_prepare_device(S_));
   }
   void eval_derivatives(double sf) override {
     chk(ncl_model_eval_all_device(M_, V_.x, sf, V_.y, nullptr, V_.grad, nullptr, jac_, hess_));

@@ -192,6 +192,8 @@ std::vector<int> symbolic_order(int n, const std::vector<int>& cp, const std::ve
     std::sort(a.begin(), a.end());
     a.erase(std::unique(a.begin(), a.end()), a.end());
   }
+  static const bool md_timing = std::getenv("NCL_SN_TIMING") != nullptr;
+  const auto md_t0 = std::chrono::steady_clock::now();
 
   // Bucket queue: one min-heap of node ids per degree. Popping the smallest
   // node of the smallest non-empty degree yields exactly the (degree, node)
@@ -363,6 +365,9 @@ std::vector<int> symbolic_order(int n, const std::vector<int>& cp, const std::ve
     clique.clear();
     std::vector<int>().swap(clique);
   }
+  if (md_timing)
+    std::fprintf(stderr, "[order] elimination loop %.3f s\n",
+                 std::chrono::duration<double>(std::chrono::steady_clock::now() - md_t0).count());
   return perm;
 }
 
