@@ -27,6 +27,9 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"factor_kernel" -s 4 -c 4 \
   -o gpurun_out/prof_factor -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-solve \
   > gpurun_out/ncu_full.log 2>&1
-NCL_TASK_TRACE=gpurun_out/trace.bin timeout 300 python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-solve \
-  > gpurun_out/trace.log 2>&1
+NCL_TASK_TRACE=gpurun_out/trace.bin NCL_SOLVE_TRACE=gpurun_out/strace.bin timeout 300 python bench.py --steps 3 --warmup 1 \
+  --no-cpu-baseline --no-solve > gpurun_out/trace.log 2>&1
+# the B200 NCL solve's full-precision iterate trace (tools/parity_record.py against the committed reference traces)
+NCL_ANALYZE_TIMING=1 timeout 600 python tools/gpu_solve.py activsg500 256 --trace gpurun_out/b200_trace_500x256.json \
+  > gpurun_out/solve_500x256.log 2>&1
 ls gpurun_out
