@@ -23,6 +23,9 @@ N, M, NNZH, NNZJ, NNZK, NNZL = 957100, 1263335, 1668284, 4662337, 5305003, 10330
 ALG = {
     # K2: read H, J, D, sigma_x; write K; + the 12 B/slot map
     "kkt_assemble_kernel": 8 * (NNZH + NNZJ + N + M) + 12 * NNZK,
+    # compact form: the same values in/out; its maps (slot, term start, term
+    # J position + byte offset) are counted at the per-slot form's 12 B/slot
+    "kkt_assemble_compact": 8 * (NNZH + NNZJ + N + M) + 12 * NNZK,
 }
 
 
