@@ -1346,8 +1346,20 @@ __global__ void __launch_bounds__(256) maxdiag_kernel(const int* __restrict__ po
                                                       double* out) {
   __shared__ double wm[8];
   double m = 0.0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nd; i += gridDim.x * blockDim.x)
-    m = fmax(m, fabs(__ldg(v + __ldg(pos + i))));
+  // four independent position -> value gathers in flight per thread
+  const int stride = gridDim.x * blockDim.x;
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < nd; i += 4 * stride) {
+    int p[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) p[u] = __ldg(pos + i + u * stride);
+    double x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = __ldg(v + p[u]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) m = fmax(m, fabs(x[u]));
+  }
+  for (; i < nd; i += stride) m = fmax(m, fabs(__ldg(v + __ldg(pos + i))));
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(kFull, m, o));
   if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
   __syncthreads();
@@ -2277,7 +2289,7 @@ int64_t g_kernel_launches = 0;
 void dev_max_abs_diag(const DevPattern& P, const double* kvals, double* out, cudaStream_t st) {
   cudaMemsetAsync(out, 0, sizeof(double), st);
   if (P.ndiag > 0)
-    COUNT(1), maxdiag_kernel<<<std::min(grid_for(P.ndiag, 256), 2 * num_sms()), 256, 0, st>>>(P.diag_pos, P.ndiag, kvals, out);
+    COUNT(1), maxdiag_kernel<<<std::min(grid_for(P.ndiag, 256), 8 * num_sms()), 256, 0, st>>>(P.diag_pos, P.ndiag, kvals, out);
 }
 
 template <class K>
@@ -2493,7 +2505,7 @@ void dev_factor(const DevSymb& S, const DevPattern& P, DevFactor& F, const doubl
 
 void dev_inertia(const DevSymb& S, DevFactor& F, cudaStream_t st, const uint8_t* report) {
   COUNT(1);
-  inertia_kernel<<<std::min(grid_for(S.n, 256), 2 * num_sms()), 256, 0, st>>>(F.D, S.n, F.scal, F.istat, report);
+  inertia_kernel<<<std::min(grid_for(S.n, 256), 8 * num_sms()), 256, 0, st>>>(F.D, S.n, F.scal, F.istat, report);
 }
 
 void dev_solve_begin(const DevSymb& S0, cudaStream_t st) {
