@@ -29,6 +29,16 @@ namespace nclb {
 
 namespace {
 
+// resident CTAs per SM the warp-part and small-CTA factor kernels are
+// compiled for (register budget 65536 / (128 x MINB)); measured (r02, same
+// box, step ms): 6/6 1.603, 5/6 1.614, 4/6 1.646 (no spills, 16 warps/SM),
+// 6/5 1.608, 6/4 1.607 — occupancy beats the spill-free register budgets
+#ifndef NCL_FK32_MINB
+#define NCL_FK32_MINB 6
+#endif
+#ifndef NCL_FK128_MINB
+#define NCL_FK128_MINB 6
+#endif
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kWarpFront = 32;    // nr cap of the warp smem path
 // kCtaFront (nr cap of the CTA smem path) lives in csrc/limits.hpp
@@ -1283,7 +1293,7 @@ __global__ void __launch_bounds__(128) reg_factor_kernel(FactorArgs a, const Reg
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 6 : NT == 128 ? 6 : 2) factor_kernel(FactorArgs a) {
+__global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? NCL_FK32_MINB : NT == 128 ? NCL_FK128_MINB : 2) factor_kernel(FactorArgs a) {
   __shared__ int s_ticket;
   extern __shared__ double s_front[];
   const int tid = NT == 32 ? (threadIdx.x & 31) : threadIdx.x;
