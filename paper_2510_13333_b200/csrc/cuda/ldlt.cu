@@ -36,6 +36,11 @@ namespace {
 #ifndef NCL_FK32_MINB
 #define NCL_FK32_MINB 6
 #endif
+// the warp solve kernels' (fwd/bwd_kernel<32>) resident 128-thread CTAs per
+// SM; shared memory (4 warps x kSolWarp doubles = 17 KB) allows up to 13
+#ifndef NCL_SK32_MINB
+#define NCL_SK32_MINB 8
+#endif
 #ifndef NCL_FK128_MINB
 #define NCL_FK128_MINB 6
 #endif
@@ -1975,7 +1980,7 @@ __device__ __forceinline__ void bwd_task(const SolveArgs& a, int s, int tid) {
 constexpr int kSolWarp = 32 + kGrpStack;  // doubles
 
 template <int NT>
-__global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 8 : 4) fwd_kernel(SolveArgs a) {
+__global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? NCL_SK32_MINB : 4) fwd_kernel(SolveArgs a) {
   __shared__ int s_ticket;
   extern __shared__ double s_sol[];
   const int tid = NT == 32 ? (threadIdx.x & 31) : threadIdx.x;
@@ -2013,7 +2018,7 @@ __global__ void __launch_bounds__(256) fwd_root_gather(SolveArgs a, int s) {
 
 // tickets in reverse order (roots first); no leaf chunking
 template <int NT>
-__global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? 8 : 4) bwd_kernel(SolveArgs a) {
+__global__ void __launch_bounds__(NT == 32 ? 128 : NT, NT == 32 ? NCL_SK32_MINB : 4) bwd_kernel(SolveArgs a) {
   __shared__ int s_ticket;
   extern __shared__ double s_sol[];
   const int tid = NT == 32 ? (threadIdx.x & 31) : threadIdx.x;
